@@ -1,0 +1,454 @@
+/*
+ * oracle/oracle.c — CPU ORACLE. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may
+ * load this library. The product path (paper_1812_08075_b200/) never links, imports or calls
+ * it, and shares no code, header, table or constant generator with it.
+ *
+ * What it computes: one application r = A x of the symmetric interior penalty DG operator
+ * for -div(c grad u) on a periodic hexahedral mesh, i.e. the residual R_I(x) = r(sum_J x_J phi_J,
+ * phi_I) of PAPER.md Eq. diffreac_weak with f = 0, no boundary facets (periodic),
+ * theta = -1, k(x) = c(x) I, no reaction term, and the penalty of BASELINE.json
+ * (gamma = penalty_scale * k (k+1) / h_d, reading R2).
+ *
+ * How: the PLAIN DEFINITION — tensor-product Gauss quadrature of every volume and face
+ * integral with the basis functions evaluated DIRECTLY at every quadrature point
+ * as products of 1D Lagrange polynomials (the unfactorised form, Eq. highcomplex),
+ * never sum factorisation. Cost O(n^3 m^3) per cell volume.
+ *
+ * Notation follows PAPER.md §2.1 and §5.2:
+ *   n = k+1 basis functions per direction, Lagrange on the n Gauss-Legendre nodes of [0,1]
+ *   (BASELINE.json cfg0; reading R8); m quadrature points per direction.
+ *   Cell T = (i0,i1,i2), canonical id c = (i0 N1 + i1) N2 + i2; local DOF J = j0 + n j1 + n^2 j2
+ *   (vec convention, j0 fastest); global DOF g = c n^3 + J (reading R10).
+ *   mu_T(xi) = o_T + J_T xi, o_T = (i0/N0, i1/N1, i2/N2) (reading R11).
+ *   Interior face F between T- (lower index along d, periodic) and T+ = T- + e_d; n_F points
+ *   from T- to T+ (P:L765). [v] = v|T- - v|T+ , {v} = (v|T- + v|T+)/2 (reading R4).
+ *   Face geometry (normal, surface element, quadrature points, c_F) from T- (reading R11, R12).
+ *
+ * Parity pins (tests/test_oracle_pins.py): Gauss rule closed forms + numpy leggauss + monomial
+ * exactness; Q1 table closed forms; independent Kronecker-sum SIPG matrix (oracle/brute.py,
+ * exact polynomial integration) on tiny meshes; symmetry, A.1 = 0, PSD; linear and quadratic
+ * consistency (exact special cases); c(x) reduction u = x2; uniform-shear affine consistency.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OMAX 16 /* max n and m */
+
+static const double PI = 3.14159265358979323846264338327950288;
+
+/* -------------------------------------------------------------------------------------- */
+/* 1D Gauss-Legendre rule on [0,1] ("1D quadrature rules with maximum order").  */
+/* Newton iteration on the Legendre polynomial P_m(t), t in [-1,1], evaluated with the      */
+/* three-term recurrence (k+1) P_{k+1} = (2k+1) t P_k - k P_{k-1}; derivative                */
+/* P_m'(t) = m (t P_m - P_{m-1}) / (t^2 - 1). Weights w = 2 / ((1 - t^2) P_m'(t)^2),        */
+/* mapped to [0,1]: xi = (1 + t)/2, w01 = w/2.                                              */
+/* -------------------------------------------------------------------------------------- */
+int oracle_gauss_legendre(int m, double* xi, double* w)
+{
+    if (m < 1 || m > OMAX) return -1;
+    for (int i = 0; i < m; ++i) {
+        /* initial guess: Chebyshev-like (roots in descending t order, i-th largest) */
+        double t = cos(PI * (i + 0.75) / (m + 0.5));
+        double dp = 1.0;
+        for (int it = 0; it < 100; ++it) {
+            double pm1 = 1.0, pm = t; /* P_0 = 1, P_1 = t */
+            for (int k = 1; k < m; ++k) {
+                double pn = ((2.0 * k + 1.0) * t * pm - k * pm1) / (k + 1.0);
+                pm1 = pm; pm = pn;
+            }
+            /* now pm = P_m(t), pm1 = P_{m-1}(t) */
+            dp = m * (t * pm - pm1) / (t * t - 1.0);
+            double dt = pm / dp;
+            t -= dt;
+            if (fabs(dt) < 1e-17) break;
+        }
+        /* recompute derivative at the converged root */
+        {
+            double pm1 = 1.0, pm = t;
+            for (int k = 1; k < m; ++k) {
+                double pn = ((2.0 * k + 1.0) * t * pm - k * pm1) / (k + 1.0);
+                pm1 = pm; pm = pn;
+            }
+            dp = m * (t * pm - pm1) / (t * t - 1.0);
+        }
+        /* store ascending on [0,1]: t descending -> index m-1-i */
+        xi[m - 1 - i] = 0.5 * (1.0 + t);
+        w[m - 1 - i] = 0.5 * 2.0 / ((1.0 - t * t) * dp * dp);
+    }
+    return 0;
+}
+
+/* Lagrange polynomial l_j on nodes[0..n-1] at s (product formula) and its derivative     */
+/* (product rule: l_j'(s) = sum_{a != j} 1/(x_j - x_a) prod_{b != j, a} (s - x_b)/(x_j - x_b)). */
+static void lagrange_1d(int n, const double* nodes, int j, double s, double* val, double* der)
+{
+    double v = 1.0;
+    for (int a = 0; a < n; ++a)
+        if (a != j) v *= (s - nodes[a]) / (nodes[j] - nodes[a]);
+    double d = 0.0;
+    for (int a = 0; a < n; ++a) {
+        if (a == j) continue;
+        double t = 1.0 / (nodes[j] - nodes[a]);
+        for (int b = 0; b < n; ++b)
+            if (b != j && b != a) t *= (s - nodes[b]) / (nodes[j] - nodes[b]);
+        d += t;
+    }
+    *val = v;
+    *der = d;
+}
+
+/* Exported for pins: 1D tables of the basis (n GL nodes) evaluated at arbitrary points.    */
+int oracle_basis_1d(int n, int npts, const double* pts, double* val, double* der)
+{
+    double xi[OMAX], w[OMAX];
+    if (oracle_gauss_legendre(n, xi, w)) return -1;
+    for (int q = 0; q < npts; ++q)
+        for (int j = 0; j < n; ++j)
+            lagrange_1d(n, xi, j, pts[q], &val[q * n + j], &der[q * n + j]);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- 3x3 helpers (row-major) */
+static double det3(const double* A)
+{
+    return A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+           A[2] * (A[3] * A[7] - A[4] * A[6]);
+}
+static void inv3(const double* A, double* B)
+{
+    double d = det3(A);
+    B[0] = (A[4] * A[8] - A[5] * A[7]) / d;
+    B[1] = (A[2] * A[7] - A[1] * A[8]) / d;
+    B[2] = (A[1] * A[5] - A[2] * A[4]) / d;
+    B[3] = (A[5] * A[6] - A[3] * A[8]) / d;
+    B[4] = (A[0] * A[8] - A[2] * A[6]) / d;
+    B[5] = (A[2] * A[3] - A[0] * A[5]) / d;
+    B[6] = (A[3] * A[7] - A[4] * A[6]) / d;
+    B[7] = (A[1] * A[6] - A[0] * A[7]) / d;
+    B[8] = (A[0] * A[4] - A[1] * A[3]) / d;
+}
+/* y = A^T x  (used as grad = J^{-T} grad_hat) */
+static void mat_t_vec(const double* A, const double* x, double* y)
+{
+    for (int a = 0; a < 3; ++a) y[a] = A[0 + a] * x[0] + A[3 + a] * x[1] + A[6 + a] * x[2];
+}
+
+/* Coefficient c(x): kind 0 -> 1; kind 1 -> 1 + 0.5 sin(2 pi x0) cos(2 pi x1) (BASELINE.json cfg2). */
+static double coeff(int kind, const double* x)
+{
+    if (kind == 0) return 1.0;
+    return 1.0 + 0.5 * sin(2.0 * PI * x[0]) * cos(2.0 * PI * x[1]);
+}
+
+/* -------------------------------------------------------------------------------------- */
+typedef struct {
+    int n, m, k;
+    int N[3];
+    int coeff_kind;
+    double penalty_scale;
+    double bnodes[OMAX];           /* basis nodes: n-point GL nodes */
+    double qx[OMAX], qw[OMAX];     /* quadrature rule, m points */
+    /* volume tables at all M = m^3 points for all n^3 basis functions: phi, dphi/dxi_0..2 */
+    double* vphi;                  /* [M][n^3][4] */
+    /* face tables: for d, side (0: xi_d = 0, 1: xi_d = 1), points (a,b) over m^2, [n^3][4] */
+    double* fphi[3][2];
+} otab;
+
+static int point_index3(int m, int q0, int q1, int q2) { return q0 + m * (q1 + m * q2); }
+
+/* Direct evaluation of phi_J and grad_hat phi_J at a reference point p (product of 1D values). */
+static void eval_basis_point(const otab* T, const double p[3], double* out /* [n^3][4] */)
+{
+    const int n = T->n;
+    double v[3][OMAX], d[3][OMAX];
+    for (int dim = 0; dim < 3; ++dim)
+        for (int j = 0; j < n; ++j) lagrange_1d(n, T->bnodes, j, p[dim], &v[dim][j], &d[dim][j]);
+    for (int j2 = 0; j2 < n; ++j2)
+        for (int j1 = 0; j1 < n; ++j1)
+            for (int j0 = 0; j0 < n; ++j0) {
+                int J = j0 + n * (j1 + n * j2);
+                out[4 * J + 0] = v[0][j0] * v[1][j1] * v[2][j2];
+                out[4 * J + 1] = d[0][j0] * v[1][j1] * v[2][j2];
+                out[4 * J + 2] = v[0][j0] * d[1][j1] * v[2][j2];
+                out[4 * J + 3] = v[0][j0] * v[1][j1] * d[2][j2];
+            }
+}
+
+/* Tangential directions of a face with normal d (increasing order). */
+static void tangential(int d, int* t1, int* t2)
+{
+    if (d == 0) { *t1 = 1; *t2 = 2; }
+    else if (d == 1) { *t1 = 0; *t2 = 2; }
+    else { *t1 = 0; *t2 = 1; }
+}
+
+static int otab_init(otab* T, int N0, int N1, int N2, int k, int m, int coeff_kind, double penalty_scale)
+{
+    memset(T, 0, sizeof(*T));
+    T->k = k; T->n = k + 1; T->m = m;
+    T->N[0] = N0; T->N[1] = N1; T->N[2] = N2;
+    T->coeff_kind = coeff_kind;
+    T->penalty_scale = penalty_scale;
+    if (T->n > OMAX || m > OMAX || k < 1 || m < 1) return -1;
+    double w[OMAX];
+    if (oracle_gauss_legendre(T->n, T->bnodes, w)) return -1;
+    if (oracle_gauss_legendre(m, T->qx, T->qw)) return -1;
+    const int n3 = T->n * T->n * T->n, M = m * m * m;
+    T->vphi = (double*)malloc(sizeof(double) * (size_t)M * n3 * 4);
+    if (!T->vphi) return -1;
+    for (int q2 = 0; q2 < m; ++q2)
+        for (int q1 = 0; q1 < m; ++q1)
+            for (int q0 = 0; q0 < m; ++q0) {
+                double p[3] = {T->qx[q0], T->qx[q1], T->qx[q2]};
+                eval_basis_point(T, p, T->vphi + (size_t)point_index3(m, q0, q1, q2) * n3 * 4);
+            }
+    for (int d = 0; d < 3; ++d) {
+        int t1, t2;
+        tangential(d, &t1, &t2);
+        for (int side = 0; side < 2; ++side) {
+            T->fphi[d][side] = (double*)malloc(sizeof(double) * (size_t)m * m * n3 * 4);
+            if (!T->fphi[d][side]) return -1;
+            for (int b = 0; b < m; ++b)
+                for (int a = 0; a < m; ++a) {
+                    double p[3];
+                    p[d] = (double)side;
+                    p[t1] = T->qx[a];
+                    p[t2] = T->qx[b];
+                    eval_basis_point(T, p, T->fphi[d][side] + (size_t)(a + m * b) * n3 * 4);
+                }
+        }
+    }
+    return 0;
+}
+
+static void otab_free(otab* T)
+{
+    free(T->vphi);
+    for (int d = 0; d < 3; ++d)
+        for (int s = 0; s < 2; ++s) free(T->fphi[d][s]);
+}
+
+/* u and grad_hat u at a point from a DOF block and the point's basis table row. */
+static void eval_u(int n3, const double* x, const double* tab, double* u, double gh[3])
+{
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    for (int J = 0; J < n3; ++J) {
+        s0 += x[J] * tab[4 * J + 0];
+        s1 += x[J] * tab[4 * J + 1];
+        s2 += x[J] * tab[4 * J + 2];
+        s3 += x[J] * tab[4 * J + 3];
+    }
+    *u = s0; gh[0] = s1; gh[1] = s2; gh[2] = s3;
+}
+
+/*
+ * Residual rows of ONE cell T = (i0,i1,i2).
+ *   xs[0] = x block of T, xs[1+2d] = block of T - e_d, xs[2+2d] = block of T + e_d (periodic)
+ *   Js[.] = the matching row-major 3x3 Jacobians J_T of the affine maps mu_T.
+ *   r    = n^3 output values (overwritten).
+ */
+static void cell_residual(const otab* T, int i0, int i1, int i2, const double* const xs[7],
+                          const double* const Js[7], double* r)
+{
+    const int n = T->n, m = T->m, n3 = n * n * n;
+    const int ic[3] = {i0, i1, i2};
+    for (int I = 0; I < n3; ++I) r[I] = 0.0;
+
+    /* ---------------- volume term (k grad u, grad v)_{0,T}, P:L982 ---------------- */
+    {
+        const double* J = Js[0];
+        double Jinv[9];
+        inv3(J, Jinv);
+        const double adet = fabs(det3(J));
+        double o[3];
+        for (int a = 0; a < 3; ++a) o[a] = (double)ic[a] / T->N[a];
+        for (int q2 = 0; q2 < m; ++q2)
+            for (int q1 = 0; q1 < m; ++q1)
+                for (int q0 = 0; q0 < m; ++q0) {
+                    const double* tab = T->vphi + (size_t)point_index3(m, q0, q1, q2) * n3 * 4;
+                    double u, gh[3], g[3];
+                    eval_u(n3, xs[0], tab, &u, gh);
+                    mat_t_vec(Jinv, gh, g);                 /* grad u = J^{-T} grad_hat u */
+                    const double xi[3] = {T->qx[q0], T->qx[q1], T->qx[q2]};
+                    double xp[3];
+                    for (int a = 0; a < 3; ++a) xp[a] = o[a] + J[3 * a] * xi[0] + J[3 * a + 1] * xi[1] + J[3 * a + 2] * xi[2];
+                    const double W = T->qw[q0] * T->qw[q1] * T->qw[q2] * adet;
+                    const double cW = W * coeff(T->coeff_kind, xp);
+                    for (int I = 0; I < n3; ++I) {
+                        double gp[3];
+                        mat_t_vec(Jinv, tab + 4 * I + 1, gp);  /* grad phi_I */
+                        r[I] += cW * (g[0] * gp[0] + g[1] * gp[1] + g[2] * gp[2]);
+                    }
+                }
+    }
+
+    /* ---------------- face terms, P:L986-989 with theta = -1 ---------------- */
+    for (int d = 0; d < 3; ++d) {
+        int t1, t2;
+        tangential(d, &t1, &t2);
+        const double gamma = T->penalty_scale * T->k * (T->k + 1) * (double)T->N[d]; /* / h_d */
+        for (int side = 0; side < 2; ++side) {
+            /* side 1: face at xi_d = 1 of T; T is T-, neighbour T + e_d is T+.
+               side 0: face at xi_d = 0 of T; T is T+, neighbour T - e_d is T-. */
+            const int self_is_minus = (side == 1);
+            const int im = self_is_minus ? 0 : 1 + 2 * d;
+            const int ip = self_is_minus ? 2 + 2 * d : 0;
+            int icm[3] = {ic[0], ic[1], ic[2]};
+            if (!self_is_minus) icm[d] = (ic[d] - 1 + T->N[d]) % T->N[d];
+            const double* Jm = Js[im];
+            const double* Jp = Js[ip];
+            double Jminv[9], Jpinv[9];
+            inv3(Jm, Jminv);
+            inv3(Jp, Jpinv);
+            const double adetm = fabs(det3(Jm));
+            /* nu = J_-^{-T} e_d (Nanson), n_F = nu/|nu|, dS = |det J_-| |nu| dS_hat */
+            double ed[3] = {0, 0, 0}, nu[3];
+            ed[d] = 1.0;
+            mat_t_vec(Jminv, ed, nu);
+            const double nnu = sqrt(nu[0] * nu[0] + nu[1] * nu[1] + nu[2] * nu[2]);
+            const double nF[3] = {nu[0] / nnu, nu[1] / nnu, nu[2] / nnu};
+            const double sF = adetm * nnu;
+            double om[3];
+            for (int a = 0; a < 3; ++a) om[a] = (double)icm[a] / T->N[a];
+            const double* tabm = T->fphi[d][1]; /* T- evaluated at xi_d = 1 */
+            const double* tabp = T->fphi[d][0]; /* T+ evaluated at xi_d = 0 */
+            const double* tabself = self_is_minus ? tabm : tabp;
+            const double* Jselfinv = self_is_minus ? Jminv : Jpinv;
+            for (int b = 0; b < m; ++b)
+                for (int a = 0; a < m; ++a) {
+                    const size_t off = (size_t)(a + m * b) * n3 * 4;
+                    double um, up, ghm[3], ghp[3], gm[3], gp[3];
+                    eval_u(n3, xs[im], tabm + off, &um, ghm);
+                    eval_u(n3, xs[ip], tabp + off, &up, ghp);
+                    mat_t_vec(Jminv, ghm, gm);
+                    mat_t_vec(Jpinv, ghp, gp);
+                    double xim[3];
+                    xim[d] = 1.0; xim[t1] = T->qx[a]; xim[t2] = T->qx[b];
+                    double xF[3];
+                    for (int c = 0; c < 3; ++c)
+                        xF[c] = om[c] + Jm[3 * c] * xim[0] + Jm[3 * c + 1] * xim[1] + Jm[3 * c + 2] * xim[2];
+                    const double cF = coeff(T->coeff_kind, xF);
+                    const double W = T->qw[a] * T->qw[b] * sF;
+                    const double jump = um - up;                                   /* [u] */
+                    const double avg = 0.5 * cF * ((gm[0] + gp[0]) * nF[0] + (gm[1] + gp[1]) * nF[1] +
+                                                   (gm[2] + gp[2]) * nF[2]);      /* n.{c grad u} */
+                    /* test side: [v] = +phi (T-) or -phi (T+); n.{c grad v} = cF/2 grad phi . n */
+                    const double sv = self_is_minus ? 1.0 : -1.0;
+                    for (int I = 0; I < n3; ++I) {
+                        const double phi = tabself[off + 4 * I];
+                        double gphi[3];
+                        mat_t_vec(Jselfinv, tabself + off + 4 * I + 1, gphi);
+                        const double dphin = 0.5 * cF * (gphi[0] * nF[0] + gphi[1] * nF[1] + gphi[2] * nF[2]);
+                        /* -(n.{c grad u}, [v]) + theta([u], n.{c grad v}) + gamma([u],[v]), theta = -1 */
+                        r[I] += W * (-avg * sv * phi - jump * dphin + gamma * jump * sv * phi);
+                    }
+                }
+        }
+    }
+}
+
+/* Geometry of a canonical cell: row-major J_T. geom_kind 0: diag(1/N); 1: from jac[9 c ..]. */
+static void cell_jac(int geom_kind, const int N[3], const double* jac, int64_t c, double* J)
+{
+    if (geom_kind == 0) {
+        memset(J, 0, 9 * sizeof(double));
+        J[0] = 1.0 / N[0]; J[4] = 1.0 / N[1]; J[8] = 1.0 / N[2];
+    } else {
+        memcpy(J, jac + 9 * c, 9 * sizeof(double));
+    }
+}
+
+/*
+ * Full (or sampled) operator application on a global vector.
+ *   x, r: host arrays of N0 N1 N2 n^3 doubles in canonical order (r rows of unlisted cells untouched)
+ *   jac : host array of 9 doubles per canonical cell (geom_kind 1), else NULL
+ *   cells: list of canonical cell ids to compute (NULL => all cells)
+ * Returns 0, or -1 on invalid arguments.
+ */
+int oracle_apply(int N0, int N1, int N2, int k, int m, int geom_kind, const double* jac, int coeff_kind,
+                 double penalty_scale, const double* x, double* r, const int64_t* cells, int64_t ncells)
+{
+    otab T;
+    if (N0 < 1 || N1 < 1 || N2 < 1 || (geom_kind == 1 && !jac)) return -1;
+    if (otab_init(&T, N0, N1, N2, k, m, coeff_kind, penalty_scale)) { otab_free(&T); return -1; }
+    const int n = k + 1;
+    const int64_t n3 = (int64_t)n * n * n;
+    const int64_t total = (int64_t)N0 * N1 * N2;
+    const int64_t cnt = cells ? ncells : total;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t s = 0; s < cnt; ++s) {
+        const int64_t c = cells ? cells[s] : s;
+        const int i2 = (int)(c % N2), i1 = (int)((c / N2) % N1), i0 = (int)(c / ((int64_t)N1 * N2));
+        const int ic[3] = {i0, i1, i2};
+        int64_t nb[7];
+        nb[0] = c;
+        for (int d = 0; d < 3; ++d)
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                int jc[3] = {ic[0], ic[1], ic[2]};
+                jc[d] = (ic[d] + (sgn ? 1 : -1) + T.N[d]) % T.N[d];
+                nb[1 + 2 * d + sgn] = ((int64_t)jc[0] * N1 + jc[1]) * N2 + jc[2];
+            }
+        const double* xs[7];
+        double Jbuf[7][9];
+        const double* Js[7];
+        for (int t = 0; t < 7; ++t) {
+            xs[t] = x + nb[t] * n3;
+            cell_jac(geom_kind, T.N, jac, nb[t], Jbuf[t]);
+            Js[t] = Jbuf[t];
+        }
+        cell_residual(&T, i0, i1, i2, xs, Js, r + c * n3);
+    }
+    otab_free(&T);
+    return 0;
+}
+
+/*
+ * Cell-local form used for sampled verification of meshes too large to hold on the host:
+ *   cells[s]       canonical id of target cell s
+ *   x7[s][7][n^3]  blocks of the target and its 6 face neighbours (order: self, -e0, +e0, -e1, +e1, -e2, +e2)
+ *   j7[s][7][9]    matching Jacobians (ignored for geom_kind 0)
+ *   r[s][n^3]      output rows
+ */
+int oracle_apply_cells_local(int N0, int N1, int N2, int k, int m, int geom_kind, int coeff_kind,
+                             double penalty_scale, const int64_t* cells, int64_t ncells, const double* x7,
+                             const double* j7, double* r)
+{
+    otab T;
+    if (otab_init(&T, N0, N1, N2, k, m, coeff_kind, penalty_scale)) { otab_free(&T); return -1; }
+    const int n = k + 1;
+    const int64_t n3 = (int64_t)n * n * n;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t s = 0; s < ncells; ++s) {
+        const int64_t c = cells[s];
+        const int i2 = (int)(c % N2), i1 = (int)((c / N2) % N1), i0 = (int)(c / ((int64_t)N1 * N2));
+        const double* xs[7];
+        double Jbuf[7][9];
+        const double* Js[7];
+        for (int t = 0; t < 7; ++t) {
+            xs[t] = x7 + (s * 7 + t) * n3;
+            if (geom_kind == 0) cell_jac(0, T.N, NULL, 0, Jbuf[t]);
+            else memcpy(Jbuf[t], j7 + (s * 7 + t) * 9, 9 * sizeof(double));
+            Js[t] = Jbuf[t];
+        }
+        cell_residual(&T, i0, i1, i2, xs, Js, r + s * n3);
+    }
+    otab_free(&T);
+    return 0;
+}
+
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
