@@ -1,0 +1,135 @@
+/*
+ * dg.h — C-ABI of libdg: matrix-free application of the symmetric interior penalty DG
+ * operator (SIPG, theta = -1) for -div(c grad u) on a structured periodic hexahedral mesh,
+ * Q_k tensor-product Lagrange elements on Gauss-Legendre nodes, evaluated with sum
+ * factorisation on sm_100a (B200).
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, line numbers P:Lnnn):
+ *   r = A x,  (A x)_I = R_I(x) = r_h(sum_J x_J phi_J, phi_I)
+ *   r_h = sum_T (c grad u, grad v)_T
+ *       + sum_F [ -(n_F.{c grad u}, [v])_F - ([u], n_F.{c grad v})_F + gamma_F([u],[v])_F ]
+ *                                                         Eq. diffreac_weak, theta=-1 P:L995
+ *   evaluated per cell with Alg. assembly (gradients by sum factorisation,
+ *   pointwise flux, transposed contractions) and per facet with the normal-direction
+ *   1-point tables.
+ * Readings fixed in DESIGN.md §2 (R1-R20): periodic unit cube, no boundary facets, f = 0;
+ * gamma_F = penalty_scale * k (k+1) / h_d with h_d = 1/N_d (BASELINE.json configs);
+ * [v] = v|T- - v|T+, T- the lower cell along the face normal d (periodic wrap: cell N_d-1 is
+ * T- of the face it shares with cell 0), n_F oriented T- -> T+ (P:L765); face geometry
+ * (normal, surface element, quadrature points, c_F) taken from T-.
+ *
+ * Data layout (all fp64):
+ *   cell (i0,i1,i2), canonical id c = (i0 N1 + i1) N2 + i2   (i0 slowest => x0-slabs contiguous)
+ *   DOF  g = c n^3 + j0 + n j1 + n^2 j2, n = k+1 (vec convention, j0 fastest)
+ *   A context owns the x0-planes [plane_begin, plane_begin + nplanes) (a "slab"); its local
+ *   vectors hold those planes' blocks contiguously (local offset = plane_begin N1 N2 n^3).
+ *
+ * Error behaviour: every function returns DG_OK (0) or a negative DG_ERR_* code and never
+ * aborts; dg_last_error() returns a thread-local message for the last failure. No function
+ * falls back to a CPU path: without a usable CUDA device dg_setup returns DG_ERR_CUDA.
+ * Thread safety: a context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef DG_H
+#define DG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_OK 0
+#define DG_ERR_INVALID (-1)     /* bad argument (sizes, pointers, aliasing, unsupported k) */
+#define DG_ERR_UNSUPPORTED (-2) /* valid request this build does not implement (quad != k+1) */
+#define DG_ERR_CUDA (-3)        /* CUDA runtime failure (no device, launch error, ...) */
+#define DG_ERR_OOM (-5)         /* device or pinned-host allocation failed */
+
+#define DG_GEOM_AXIS 0   /* J_T = diag(1/N0, 1/N1, 1/N2) */
+#define DG_GEOM_AFFINE 1 /* per-cell affine map x = o_T + J_T xi, J_T given per cell */
+#define DG_COEFF_ONE 0   /* c = 1 (Poisson) */
+#define DG_COEFF_SINCOS 1 /* c(x) = 1 + 0.5 sin(2 pi x0) cos(2 pi x1), at the mapped quadrature points */
+
+typedef struct dg_ctx dg_ctx;
+
+typedef struct dg_mesh {
+    int32_t N[3];          /* global cells per direction; the unit cube is periodic in all three; N[d] >= 2 */
+    int32_t plane_begin;   /* first global x0-plane owned by this context, 0 <= plane_begin < N[0] */
+    int32_t nplanes;       /* number of owned x0-planes L, 1 <= L <= N[0] (L == N[0]: whole mesh) */
+    int32_t geom_kind;     /* DG_GEOM_AXIS or DG_GEOM_AFFINE */
+    const double* jac;     /* HOST pointer, read during dg_setup only (caller keeps ownership).
+                              DG_GEOM_AFFINE: row-major 3x3 J_T (9 doubles) for every cell of the
+                              L+2 x0-planes plane_begin-1 .. plane_begin+L (global indices mod N0),
+                              each plane in canonical (i1, i2) order. det J_T must be nonzero.
+                              DG_GEOM_AXIS: must be NULL. */
+    int32_t coeff_kind;    /* DG_COEFF_ONE or DG_COEFF_SINCOS */
+    double penalty_scale;  /* gamma_F = penalty_scale * k (k+1) * N[d] on faces with normal d (> 0) */
+    int32_t device;        /* CUDA device ordinal */
+    void* stream;          /* cudaStream_t on which dg_apply* enqueue work (NULL: legacy default stream) */
+} dg_mesh;
+
+/* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,
+ * boundary vectors e0,e1,d0,d1), device copy of the slab's
+ * geometry, kernel selection. k in [1,7]; quad = Gauss points per direction, must equal k+1
+ * (collocation; other values -> DG_ERR_UNSUPPORTED). Allocates device memory (geometry:
+ * 72 B per cell of L+2 planes for DG_GEOM_AFFINE, nothing for DG_GEOM_AXIS). *out owned by the
+ * caller, release with dg_destroy. Synchronous. */
+int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out);
+
+/* r = A x for a context owning the WHOLE mesh (nplanes == N[0]).
+ * x, r: caller-owned DEVICE pointers to dg_local_ndofs() doubles each, 8-byte aligned, not
+ * overlapping (else DG_ERR_INVALID). r is overwritten (every entry written exactly once).
+ * Asynchronous on the context stream; the caller synchronises. */
+int dg_apply(dg_ctx* ctx, const double* x, double* r);
+
+/* Slab form used for x0 domain decomposition: overwrite the rows of r belonging to local
+ * x0-planes [p_begin, p_end) (0 <= p_begin <= p_end <= L).
+ *   x        DEVICE, the L owned planes (dg_local_ndofs() doubles)
+ *   x_below  DEVICE, the DOF blocks of global plane plane_begin-1 (mod N0): N1 N2 n^3 doubles
+ *            (the halo received from the lower neighbour; for a whole-mesh context this is
+ *            x + (L-1) N1 N2 n^3)
+ *   x_above  DEVICE, the blocks of global plane plane_begin+L (mod N0)
+ *   r        DEVICE, dg_local_ndofs() doubles; rows outside [p_begin, p_end) are untouched.
+ * Asynchronous on the context stream. */
+int dg_apply_planes(dg_ctx* ctx, const double* x, const double* x_below, const double* x_above, double* r,
+                    int p_begin, int p_end);
+
+/* End-to-end form with HOST buffers (whole-mesh context): copies x host->device, applies A,
+ * copies r device->host, pipelined over x0-plane chunks on three streams (H2D, compute, D2H)
+ * so the PCIe transfers overlap the kernels. x_host, r_host: dg_local_ndofs() doubles
+ * (page-locked memory gives full overlap; pageable memory works but serialises). Device
+ * staging buffers are allocated on first use and kept in the context. Synchronous: returns
+ * after r_host is complete. */
+int dg_apply_host(dg_ctx* ctx, const double* x_host, double* r_host);
+
+/* Release all device memory, streams and events of the context. NULL is accepted. */
+int dg_destroy(dg_ctx* ctx);
+
+int dg_set_stream(dg_ctx* ctx, void* stream);
+
+int64_t dg_local_ndofs(const dg_ctx* ctx);  /* L N1 N2 n^3 */
+int64_t dg_local_offset(const dg_ctx* ctx); /* plane_begin N1 N2 n^3: offset of the slab in the global vector */
+int64_t dg_plane_ndofs(const dg_ctx* ctx);  /* N1 N2 n^3: size of one x0-plane (halo message) */
+
+/* Algorithmic work of one application over the local slab:
+ * flops = F_alg(n) * local DOFs, with F_alg the collocated sum-factorisation count with
+ * each face once; bytes = 16 B per DOF (read x, write r) + geometry bytes. */
+double dg_alg_flops(const dg_ctx* ctx);
+double dg_alg_bytes(const dg_ctx* ctx);
+
+/* Kernel launches enqueued by one dg_apply / dg_apply_planes call, and the name of the kernel. */
+int dg_launches_per_apply(const dg_ctx* ctx);
+const char* dg_kernel_name(const dg_ctx* ctx);
+
+/* FP64 peak microbenchmark (measurement utility, not part of the operator): runs 8 independent
+ * DFMA chains per thread on every SM for `iters` x 128 DFMAs per thread and returns the achieved
+ * FP64 TFLOP/s (2 flops per DFMA) and the kernel time. Synchronous. */
+int dg_bench_fp64(int device, int iters, double* tflops, double* ms);
+
+/* Thread-local description of the last error ("" if none). */
+const char* dg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DG_H */

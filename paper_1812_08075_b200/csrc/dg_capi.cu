@@ -1,0 +1,324 @@
+// libdg C-ABI (include/dg.h): context setup, kernel dispatch, slab / host-pipelined apply.
+#include "../../include/dg.h"
+#include "common.cuh"
+#include "kernel_cell.cuh"
+#include "tables.h"
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                                    \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(e_ == cudaErrorMemoryAllocation ? DG_ERR_OOM : DG_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+    } while (0)
+
+using LaunchFn = cudaError_t (*)(const void* tab, const dg::MeshArgs& M, const double* x, const double* xb,
+                                 const double* xa, double* r, long long c0, long long c1, cudaStream_t st);
+
+template <int N, bool AFF, bool COEF>
+cudaError_t launch_cell(const void* tab, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
+                        double* r, long long c0, long long c1, cudaStream_t st)
+{
+    constexpr int CPB = dg::CellCfg<N>::CPB;
+    const long long ncell = c1 - c0;
+    if (ncell <= 0) return cudaSuccess;
+    const long long grid = (ncell + CPB - 1) / CPB;
+    dg::k_cell_general<N, AFF, COEF><<<(unsigned)grid, dg::CellCfg<N>::THREADS, 0, st>>>(
+        x, xb, xa, r, c0, c1, *static_cast<const dg::Tab<N>*>(tab), M);
+    return cudaGetLastError();
+}
+
+template <int N>
+LaunchFn pick_cell(bool aff, bool coef)
+{
+    if (aff) return coef ? launch_cell<N, true, true> : launch_cell<N, true, false>;
+    return coef ? launch_cell<N, false, true> : launch_cell<N, false, false>;
+}
+
+LaunchFn pick(int n, bool aff, bool coef)
+{
+    switch (n) {
+    case 2: return pick_cell<2>(aff, coef);
+    case 3: return pick_cell<3>(aff, coef);
+    case 4: return pick_cell<4>(aff, coef);
+    case 5: return pick_cell<5>(aff, coef);
+    case 6: return pick_cell<6>(aff, coef);
+    case 7: return pick_cell<7>(aff, coef);
+    case 8: return pick_cell<8>(aff, coef);
+    default: return nullptr;
+    }
+}
+
+template <int N>
+void fill_tab(const dg::HostTables& H, void* out)
+{
+    dg::Tab<N>* T = static_cast<dg::Tab<N>*>(out);
+    for (int i = 0; i < N * N; ++i) T->D[i] = H.D[i];
+    for (int i = 0; i < N; ++i) {
+        T->w[i] = H.w[i];
+        T->xi[i] = H.xi[i];
+        T->e0[i] = H.e0[i];
+        T->e1[i] = H.e1[i];
+        T->d0[i] = H.d0[i];
+        T->d1[i] = H.d1[i];
+    }
+}
+
+} // namespace
+
+struct dg_ctx {
+    dg_mesh mesh;
+    int k, n;
+    int device;
+    cudaStream_t stream;
+    dg::MeshArgs M;
+    alignas(16) unsigned char tab[sizeof(dg::Tab<dg::kMaxN>)];
+    LaunchFn launch;
+    const char* kname;
+    double* d_jac;
+    // host-pipeline state (dg_apply_host)
+    double* hx_d;
+    double* hr_d;
+    cudaStream_t s_h2d, s_d2h, s_cmp;
+    int64_t plane_dofs, local_dofs;
+};
+
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+
+int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
+{
+    g_err.clear();
+    if (!mesh || !out) return fail(DG_ERR_INVALID, "dg_setup: NULL argument");
+    *out = nullptr;
+    if (k < 1 || k > 7) return fail(DG_ERR_INVALID, "dg_setup: k=%d outside [1,7]", k);
+    if (quad != k + 1) return fail(DG_ERR_UNSUPPORTED, "dg_setup: quad=%d != k+1 (collocation only)", quad);
+    for (int d = 0; d < 3; ++d)
+        if (mesh->N[d] < 2) return fail(DG_ERR_INVALID, "dg_setup: N[%d]=%d < 2", d, mesh->N[d]);
+    if (mesh->plane_begin < 0 || mesh->plane_begin >= mesh->N[0] || mesh->nplanes < 1 || mesh->nplanes > mesh->N[0])
+        return fail(DG_ERR_INVALID, "dg_setup: bad slab [%d, +%d) for N0=%d", mesh->plane_begin, mesh->nplanes,
+                    mesh->N[0]);
+    if (mesh->geom_kind != DG_GEOM_AXIS && mesh->geom_kind != DG_GEOM_AFFINE)
+        return fail(DG_ERR_INVALID, "dg_setup: geom_kind=%d", mesh->geom_kind);
+    if ((mesh->geom_kind == DG_GEOM_AFFINE) != (mesh->jac != nullptr))
+        return fail(DG_ERR_INVALID, "dg_setup: jac must be given iff geom_kind == DG_GEOM_AFFINE");
+    if (mesh->coeff_kind != DG_COEFF_ONE && mesh->coeff_kind != DG_COEFF_SINCOS)
+        return fail(DG_ERR_INVALID, "dg_setup: coeff_kind=%d", mesh->coeff_kind);
+    if (!(mesh->penalty_scale > 0.0)) return fail(DG_ERR_INVALID, "dg_setup: penalty_scale must be > 0");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(DG_ERR_CUDA, "dg_setup: no CUDA device (libdg has no CPU path)");
+    if (mesh->device < 0 || mesh->device >= ndev) return fail(DG_ERR_INVALID, "dg_setup: device %d", mesh->device);
+    CU(cudaSetDevice(mesh->device));
+
+    dg_ctx* c = (dg_ctx*)calloc(1, sizeof(dg_ctx));
+    if (!c) return fail(DG_ERR_OOM, "dg_setup: host allocation");
+    c->mesh = *mesh;
+    c->mesh.jac = nullptr;
+    c->k = k;
+    c->n = k + 1;
+    c->device = mesh->device;
+    c->stream = (cudaStream_t)mesh->stream;
+    const int n = c->n;
+
+    dg::HostTables H;
+    if (dg::build_tables(n, &H)) { free(c); return fail(DG_ERR_INVALID, "tables n=%d", n); }
+    switch (n) {
+    case 2: fill_tab<2>(H, c->tab); break;
+    case 3: fill_tab<3>(H, c->tab); break;
+    case 4: fill_tab<4>(H, c->tab); break;
+    case 5: fill_tab<5>(H, c->tab); break;
+    case 6: fill_tab<6>(H, c->tab); break;
+    case 7: fill_tab<7>(H, c->tab); break;
+    case 8: fill_tab<8>(H, c->tab); break;
+    }
+
+    dg::MeshArgs& M = c->M;
+    M.N0 = mesh->N[0]; M.N1 = mesh->N[1]; M.N2 = mesh->N[2];
+    M.plane_begin = mesh->plane_begin;
+    M.L = mesh->nplanes;
+    M.plane_cells = mesh->N[1] * mesh->N[2];
+    for (int d = 0; d < 3; ++d) {
+        M.h[d] = 1.0 / mesh->N[d];
+        M.gamma[d] = mesh->penalty_scale * k * (k + 1) * (double)mesh->N[d];
+    }
+    M.jac = nullptr;
+    const int64_t n3 = (int64_t)n * n * n;
+    c->plane_dofs = (int64_t)M.plane_cells * n3;
+    c->local_dofs = c->plane_dofs * M.L;
+
+    if (mesh->geom_kind == DG_GEOM_AFFINE) {
+        const size_t bytes = sizeof(double) * 9 * (size_t)M.plane_cells * (size_t)(M.L + 2);
+        cudaError_t e = cudaMalloc(&c->d_jac, bytes);
+        if (e != cudaSuccess) { free(c); return fail(DG_ERR_OOM, "dg_setup: jac alloc %zu B: %s", bytes, cudaGetErrorString(e)); }
+        e = cudaMemcpy(c->d_jac, mesh->jac, bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { cudaFree(c->d_jac); free(c); return fail(DG_ERR_CUDA, "dg_setup: jac copy: %s", cudaGetErrorString(e)); }
+        M.jac = c->d_jac;
+    }
+    c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
+    c->kname = "k_cell_general";
+    *out = c;
+    return DG_OK;
+}
+
+int dg_destroy(dg_ctx* c)
+{
+    if (!c) return DG_OK;
+    cudaSetDevice(c->device);
+    if (c->d_jac) cudaFree(c->d_jac);
+    if (c->hx_d) cudaFree(c->hx_d);
+    if (c->hr_d) cudaFree(c->hr_d);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
+    free(c);
+    return DG_OK;
+}
+
+int dg_set_stream(dg_ctx* c, void* stream)
+{
+    if (!c) return fail(DG_ERR_INVALID, "dg_set_stream: NULL ctx");
+    c->stream = (cudaStream_t)stream;
+    return DG_OK;
+}
+
+int64_t dg_local_ndofs(const dg_ctx* c) { return c ? c->local_dofs : -1; }
+int64_t dg_local_offset(const dg_ctx* c) { return c ? (int64_t)c->mesh.plane_begin * c->plane_dofs : -1; }
+int64_t dg_plane_ndofs(const dg_ctx* c) { return c ? c->plane_dofs : -1; }
+int dg_launches_per_apply(const dg_ctx* c) { return c ? 1 : -1; }
+const char* dg_kernel_name(const dg_ctx* c) { return c ? c->kname : ""; }
+
+double dg_alg_flops(const dg_ctx* c)
+{
+    // collocated sum factorisation, each face once, multiply-add = 2 flops.
+    //   axis-aligned Poisson : F = 12 n + 51 + 30/n              per DOF
+    //   affine diffusion     : F = 12 n + 117 + Cc + 3 (32 + Cc)/n, Cc = 16 (nominal c(x) cost)
+    if (!c) return -1.0;
+    const double n = c->n;
+    double F;
+    if (c->mesh.geom_kind == DG_GEOM_AXIS && c->mesh.coeff_kind == DG_COEFF_ONE)
+        F = 12.0 * n + 51.0 + 30.0 / n;
+    else {
+        const double Cc = (c->mesh.coeff_kind == DG_COEFF_SINCOS) ? 16.0 : 0.0;
+        if (c->mesh.geom_kind == DG_GEOM_AXIS)
+            F = 12.0 * n + 51.0 + 30.0 / n + Cc * (1.0 + 3.0 / n); // c(x) at volume + face points
+        else
+            F = 12.0 * n + 117.0 + Cc + 3.0 * (32.0 + Cc) / n;
+    }
+    return F * (double)c->local_dofs;
+}
+
+double dg_alg_bytes(const dg_ctx* c)
+{
+    if (!c) return -1.0;
+    double b = 16.0 * (double)c->local_dofs;
+    if (c->mesh.geom_kind == DG_GEOM_AFFINE) b += 72.0 * (double)c->M.plane_cells * c->M.L;
+    return b;
+}
+
+int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1)
+{
+    if (!c || !x || !xb || !xa || !r) return fail(DG_ERR_INVALID, "dg_apply_planes: NULL argument");
+    if (p0 < 0 || p1 > c->M.L || p0 > p1) return fail(DG_ERR_INVALID, "dg_apply_planes: planes [%d,%d) of %d", p0, p1, c->M.L);
+    const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
+    const char *xs = (const char*)x, *rs = (const char*)r;
+    if (xs < rs + bytes && rs < xs + bytes) return fail(DG_ERR_INVALID, "dg_apply: x and r overlap");
+    if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 7)
+        return fail(DG_ERR_INVALID, "dg_apply: pointers must be 8-byte aligned");
+    const long long pc = c->M.plane_cells;
+    cudaError_t e = c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, c->stream);
+    if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
+    return DG_OK;
+}
+
+int dg_apply(dg_ctx* c, const double* x, double* r)
+{
+    if (!c) return fail(DG_ERR_INVALID, "dg_apply: NULL ctx");
+    if (c->M.L != c->M.N0)
+        return fail(DG_ERR_INVALID, "dg_apply: context owns %d of %d planes; use dg_apply_planes with halos", c->M.L,
+                    c->M.N0);
+    if (!x || !r) return fail(DG_ERR_INVALID, "dg_apply: NULL vector");
+    return dg_apply_planes(c, x, x + (size_t)(c->M.L - 1) * c->plane_dofs, x, r, 0, c->M.L);
+}
+
+int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
+{
+    if (!c || !xh || !rh) return fail(DG_ERR_INVALID, "dg_apply_host: NULL argument");
+    if (c->M.L != c->M.N0) return fail(DG_ERR_INVALID, "dg_apply_host: whole-mesh context required");
+    CU(cudaSetDevice(c->device));
+    const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
+    if (!c->hx_d) {
+        CU(cudaMalloc(&c->hx_d, bytes));
+        CU(cudaMalloc(&c->hr_d, bytes));
+        CU(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking));
+    }
+    const int L = c->M.L;
+    const int64_t pd = c->plane_dofs;
+    const size_t pbytes = sizeof(double) * (size_t)pd;
+    // chunks of planes; chunk i computes planes [b_i, e_i) once planes [b_i-1, e_i] are resident
+    const int nch = L >= 8 ? 8 : L;
+    int bnd[9];
+    for (int i = 0; i <= nch; ++i) bnd[i] = (int)((int64_t)L * i / nch);
+    cudaEvent_t ev_in[9], ev_cmp[9];
+    for (int i = 0; i < nch; ++i) {
+        CU(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ev_cmp[i], cudaEventDisableTiming));
+    }
+    // H2D: the last plane first (wrap halo of chunk 0), then chunks in order
+    CU(cudaMemcpyAsync(c->hx_d + (size_t)(L - 1) * pd, xh + (size_t)(L - 1) * pd, pbytes, cudaMemcpyHostToDevice,
+                       c->s_h2d));
+    for (int i = 0; i < nch; ++i) {
+        int b = bnd[i], e = bnd[i + 1];
+        if (i == nch - 1) e = L - 1; // last plane already sent
+        if (e > b)
+            CU(cudaMemcpyAsync(c->hx_d + (size_t)b * pd, xh + (size_t)b * pd, pbytes * (size_t)(e - b),
+                               cudaMemcpyHostToDevice, c->s_h2d));
+        CU(cudaEventRecord(ev_in[i], c->s_h2d));
+    }
+    // compute chunk i after chunk i+1 arrived (needs plane e_i); the last chunk needs plane 0 (chunk 0)
+    for (int i = 0; i < nch; ++i) {
+        const int need = (i + 1 < nch) ? i + 1 : nch - 1;
+        CU(cudaStreamWaitEvent(c->s_cmp, ev_in[need], 0));
+        cudaError_t e = c->launch(c->tab, c->M, c->hx_d, c->hx_d + (size_t)(L - 1) * pd, c->hx_d, c->hr_d,
+                                  (long long)bnd[i] * c->M.plane_cells, (long long)bnd[i + 1] * c->M.plane_cells,
+                                  c->s_cmp);
+        if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply_host: launch: %s", cudaGetErrorString(e));
+        CU(cudaEventRecord(ev_cmp[i], c->s_cmp));
+        CU(cudaStreamWaitEvent(c->s_d2h, ev_cmp[i], 0));
+        CU(cudaMemcpyAsync(rh + (size_t)bnd[i] * pd, c->hr_d + (size_t)bnd[i] * pd,
+                           pbytes * (size_t)(bnd[i + 1] - bnd[i]), cudaMemcpyDeviceToHost, c->s_d2h));
+    }
+    CU(cudaStreamSynchronize(c->s_d2h));
+    for (int i = 0; i < nch; ++i) {
+        cudaEventDestroy(ev_in[i]);
+        cudaEventDestroy(ev_cmp[i]);
+    }
+    return DG_OK;
+}
+
+} // extern "C"

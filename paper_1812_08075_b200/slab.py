@@ -1,0 +1,181 @@
+"""x0-slab domain decomposition with a nearest-neighbour halo exchange.
+
+Rank q of P owns the x0-planes [q N0 / P, (q+1) N0 / P). Because cells are ordered with i0
+slowest, a slab is a contiguous range of the canonical vector and so are its first and last
+planes: the halo messages are plain contiguous slices of x, sent without any packing kernel.
+Per application (the only exchange step of the method):
+
+    comm stream (high priority)           compute stream
+    ---------------------------           --------------
+    wait x ready                          planes [1, L-1)   (interior: x0-neighbours local)
+    send plane 0     -> rank q-1
+    send plane L-1   -> rank q+1
+    recv halo_above  <- rank q+1
+    recv halo_below  <- rank q-1
+    record done  ───────────────────────> wait done; planes 0 and L-1 (use the halos)
+
+The periodic wrap makes the ranks a ring (neighbours q +- 1 mod P). With P = 2 both
+neighbours are the same rank: the two messages are distinguished by tag (gloo) and by posting
+order (NCCL matches point-to-point operations between a pair in order: the sender posts
+[plane 0, plane L-1], the receiver posts [halo_above, halo_below], which pair up).
+P = 1 needs no exchange: the halos are x's own wrap planes.
+
+The exchange uses torch.distributed point-to-point ops (NCCL over NVLink on GPUs, gloo on
+CPU for the tests); the compute is libdg (dg_apply_planes).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class SlabPlan:
+    rank: int
+    world: int
+    N0: int
+    plane_begin: int
+    nplanes: int
+
+    @property
+    def below(self) -> int:
+        return (self.rank - 1) % self.world
+
+    @property
+    def above(self) -> int:
+        return (self.rank + 1) % self.world
+
+    @property
+    def interior(self):
+        """Local planes whose x0-neighbours are both local."""
+        return (1, max(1, self.nplanes - 1))
+
+    @property
+    def boundary(self):
+        """Local plane ranges that read a halo (computed after the exchange)."""
+        L = self.nplanes
+        if L == 1:
+            return [(0, 1)]
+        return [(0, 1), (L - 1, L)]
+
+
+def plan(N0: int, rank: int, world: int) -> SlabPlan:
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    if N0 < world:
+        raise ValueError(f"N0={N0} planes cannot be split over {world} ranks")
+    b = (rank * N0) // world
+    e = ((rank + 1) * N0) // world
+    return SlabPlan(rank, world, N0, b, e - b)
+
+
+def exchange_halos(x, halo_below, halo_above, plane_ndofs: int, p: SlabPlan, group=None):
+    """Post the two sends and two receives of one halo exchange and wait for them.
+    x: this rank's slab (1D, contiguous); halo_*: plane_ndofs-sized receive buffers."""
+    import torch.distributed as dist
+    if p.world == 1:
+        halo_below.copy_(x[-plane_ndofs:])
+        halo_above.copy_(x[:plane_ndofs])
+        return
+    ops = [
+        dist.P2POp(dist.isend, x[:plane_ndofs], p.below, group, tag=0),      # my plane 0 -> their halo_above
+        dist.P2POp(dist.isend, x[-plane_ndofs:], p.above, group, tag=1),     # my plane L-1 -> their halo_below
+        dist.P2POp(dist.irecv, halo_above, p.above, group, tag=0),
+        dist.P2POp(dist.irecv, halo_below, p.below, group, tag=1),
+    ]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+class SlabApply:
+    """One rank's share of r = A x with the halo exchange overlapped with interior planes.
+
+    planes_fn(x, x_below, x_above, r, p_begin, p_end) computes the rows of local planes
+    [p_begin, p_end) — libdg's dg_apply_planes on GPUs (see SlabOperator)."""
+
+    def __init__(self, p: SlabPlan, plane_ndofs: int, planes_fn, group=None, device=None):
+        import torch
+        self.p = p
+        self.plane_ndofs = plane_ndofs
+        self.fn = planes_fn
+        self.group = group
+        self.device = device
+        self.cuda = device is not None and torch.device(device).type == "cuda"
+        self.halo_below = torch.empty(plane_ndofs, dtype=torch.float64, device=device)
+        self.halo_above = torch.empty(plane_ndofs, dtype=torch.float64, device=device)
+        if self.cuda:
+            self.comm_stream = torch.cuda.Stream(device=device, priority=-1)
+            self.ev_x = torch.cuda.Event()
+            self.ev_halo = torch.cuda.Event()
+        # kernel launches per application: whole mesh 1; slab with L <= 2 planes 1 (after the
+        # exchange); otherwise interior + 2 boundary planes
+        self.launches_per_apply = 1 if (p.world == 1 or p.nplanes <= 2) else 3
+
+    def __call__(self, x, r):
+        import torch
+        p = self.p
+        if p.world == 1:
+            # whole mesh on one rank: halos are the wrap planes of x itself, one launch
+            L = p.nplanes
+            self.fn(x, x[(L - 1) * self.plane_ndofs:], x[:self.plane_ndofs], r, 0, L)
+            return r
+        if not self.cuda:
+            exchange_halos(x, self.halo_below, self.halo_above, self.plane_ndofs, p, self.group)
+            a, b = p.interior
+            if b > a:
+                self.fn(x, self.halo_below, self.halo_above, r, a, b)
+            for a, b in p.boundary:
+                self.fn(x, self.halo_below, self.halo_above, r, a, b)
+            return r
+        cur = torch.cuda.current_stream(self.device)
+        self.ev_x.record(cur)
+        with torch.cuda.stream(self.comm_stream):
+            self.comm_stream.wait_event(self.ev_x)
+            exchange_halos(x, self.halo_below, self.halo_above, self.plane_ndofs, p, self.group)
+            self.ev_halo.record(self.comm_stream)
+        a, b = p.interior
+        if b > a:
+            self.fn(x, self.halo_below, self.halo_above, r, a, b)
+        cur.wait_event(self.ev_halo)
+        if p.nplanes <= 2:
+            self.fn(x, self.halo_below, self.halo_above, r, 0, p.nplanes)
+        else:
+            for a, b in p.boundary:
+                self.fn(x, self.halo_below, self.halo_above, r, a, b)
+        # keep the halo buffers alive until the compute stream is done with them
+        self.halo_below.record_stream(cur)
+        self.halo_above.record_stream(cur)
+        return r
+
+
+class SlabOperator:
+    """libdg context for one rank's slab + the overlapped halo exchange (GPU, NCCL)."""
+
+    def __init__(self, N, k: int, rank: int, world: int, *, geom_kind=0, coeff_kind=0, penalty_scale=10.0,
+                 jac_fn=None, group=None, device=0):
+        """jac_fn(plane_begin, nplanes) -> host float64 [(nplanes) N1 N2, 9] (affine only); called for the
+        L+2 planes plane_begin-1 .. plane_begin+L."""
+        from .dg import Operator
+        self.plan = plan(int(N[0]), rank, world)
+        jac = None
+        if geom_kind == 1:
+            jac = jac_fn(self.plan.plane_begin - 1, self.plan.nplanes + 2)
+        self.op = Operator(N, k, geom_kind=geom_kind, coeff_kind=coeff_kind, penalty_scale=penalty_scale, jac=jac,
+                           plane_begin=self.plan.plane_begin, nplanes=self.plan.nplanes, device=device)
+        self.ndofs = self.op.ndofs
+        self.offset = self.op.offset
+        self.plane_ndofs = self.op.plane_ndofs
+        self._apply = SlabApply(self.plan, self.plane_ndofs, self.op.apply_planes, group=group,
+                                device=f"cuda:{device}")
+
+    @property
+    def launches_per_apply(self) -> int:
+        return self._apply.launches_per_apply
+
+    def apply(self, x, r=None):
+        import torch
+        if r is None:
+            r = torch.empty_like(x)
+        return self._apply(x, r)
+
+    def close(self):
+        self.op.close()

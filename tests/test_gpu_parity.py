@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): max|r_gpu - r_oracle| / max|r_oracle| <= 1e-11 in fp64.
+Full vectors where the oracle finishes in seconds (small meshes spanning several CTAs with
+ragged tails, cfg0, cfg1); at the full sizes of cfg2/cfg3/cfg4, in the launch configuration
+bench.py times, a deterministic sample of cells (slab-boundary planes, wrap planes, random)
+computed by the oracle one by one, plus size-independent properties (symmetry, A.1 = 0).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+def _op(w, **kw):
+    from paper_1812_08075_b200 import Operator
+    jac = synth.jac_planes_torch(w, -1, w.N[0] + 2, device="cuda").cpu().numpy() if w.geom_kind else None
+    return Operator(w.N, w.k, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind, penalty_scale=w.penalty_scale,
+                    jac=jac, **kw)
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+def _full_check(w):
+    op = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    r = op.apply(x)
+    torch.cuda.synchronize()
+    jac = synth.jac_cells_np(w, np.arange(w.ncells)) if w.geom_kind else None
+    ref = oracle.apply(w, x.cpu().numpy(), jac)
+    err = _rel(r.cpu().numpy(), ref)
+    op.close()
+    return err
+
+
+def _sampled_check(w, cells):
+    op = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    r = op.apply(x)
+    torch.cuda.synchronize()
+    n3 = w.n ** 3
+    xv = x.view(w.ncells, n3)
+    fetch = lambda ids: xv[torch.from_numpy(ids).cuda()].cpu().numpy()
+    jf = (lambda ids: synth.jac_cells_np(w, ids)) if w.geom_kind else None
+    ref = oracle.apply_sampled(w, cells, fetch, jf)
+    got = r.view(w.ncells, n3)[torch.from_numpy(cells).cuda()].cpu().numpy()
+    # the generator is shared: the sampled x blocks equal a fresh host draw
+    assert np.array_equal(fetch(cells[:4]), synth.x_cells_np(w, cells[:4]))
+    op.close()
+    del x, r
+    torch.cuda.empty_cache()
+    return _rel(got, ref)
+
+
+@pytest.mark.parametrize("k", range(1, 8))
+@pytest.mark.parametrize("geom,coeff", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_small_all_degrees(k, geom, coeff):
+    """Every degree, every geometry/coefficient combination; anisotropic N so that the cell count
+    is not a multiple of the cells-per-CTA (ragged last CTA)."""
+    N = (3, 5, 7) if k <= 3 else (3, 2, 5)
+    w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=100 + k)
+    assert _full_check(w) <= TOL
+
+
+def test_minimum_mesh():
+    for k in (1, 4, 7):
+        assert _full_check(synth.small(k, (2, 2, 2), geom_kind=1, coeff_kind=1, seed=5)) <= TOL
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_config_full_vector(cfg):
+    assert _full_check(synth.CONFIGS[cfg]) <= TOL
+
+
+@pytest.mark.parametrize("cfg,nrand", [(2, 3000), (3, 1500), (4, 3000)])
+def test_config_sampled(cfg, nrand):
+    w = synth.CONFIGS[cfg]
+    cells = synth.sample_cells(w, nrandom=nrand, plane_cap=96, wrap_plane_cells=128)
+    assert _sampled_check(w, cells) <= TOL
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_properties_full_size(cfg):
+    """Symmetry y.Ax = x.Ay and A.1 = 0 at full size (north_star invariants)."""
+    w = synth.CONFIGS[cfg]
+    op = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    import dataclasses
+    y = synth.x_torch(dataclasses.replace(w, seed=w.seed + 1000), device="cuda")
+    Ax = op.apply(x)
+    Ay = op.apply(y)
+    lhs = torch.dot(y, Ax).item()
+    rhs = torch.dot(x, Ay).item()
+    scale = max(torch.linalg.norm(y).item() * torch.linalg.norm(Ax).item(),
+                torch.linalg.norm(x).item() * torch.linalg.norm(Ay).item())
+    assert abs(lhs - rhs) <= 1e-12 * scale
+    one = torch.ones_like(x)
+    A1 = op.apply(one)
+    assert A1.abs().max().item() <= 1e-12 * Ax.abs().max().item()
+    op.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("wi", [0, 1])
+def test_slab_loopback_bitwise(world, wi):
+    """World-size-P slab decomposition emulated on one GPU: P contexts, halos copied from the
+    neighbours' planes, interior/boundary plane split — bitwise equal to the whole-mesh apply."""
+    from paper_1812_08075_b200 import Operator, slab
+    w = [synth.CONFIGS[1], synth.small(2, (6, 4, 5), geom_kind=1, coeff_kind=1, seed=3)][wi]
+    full = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    ref = full.apply(x)
+    pd = full.plane_ndofs
+    got = torch.full_like(x, float("nan"))
+    for q in range(world):
+        p = slab.plan(w.N[0], q, world)
+        jac = synth.jac_planes_torch(w, p.plane_begin - 1, p.nplanes + 2).numpy() if w.geom_kind else None
+        op = Operator(w.N, w.k, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind, penalty_scale=w.penalty_scale,
+                      jac=jac, plane_begin=p.plane_begin, nplanes=p.nplanes)
+        xs = x[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        rs = got[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        hb = x[((p.plane_begin - 1) % w.N[0]) * pd:][:pd].clone()
+        ha = x[((p.plane_begin + p.nplanes) % w.N[0]) * pd:][:pd].clone()
+        a, b = p.interior
+        if b > a:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        for a, b in p.boundary:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        torch.cuda.synchronize()
+        op.close()
+    assert torch.equal(got, ref)
+    full.close()
+
+
+def test_host_pipeline_bitwise():
+    """dg_apply_host (H2D / compute / D2H pipelined over plane chunks) == dg_apply."""
+    w = synth.CONFIGS[1]
+    op = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    ref = op.apply(x).cpu()
+    xh = x.cpu().pin_memory()
+    rh = torch.empty_like(xh).pin_memory()
+    op.apply_host(xh, rh)
+    assert torch.equal(rh, ref)
+    op.close()
+
+
+def test_apply_rejects_bad_arguments():
+    from paper_1812_08075_b200 import DgError, dg
+    w = synth.CONFIGS[0]
+    op = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    with pytest.raises(DgError):
+        dg.dg_apply(op.ctx, x, x)                        # aliasing
+    with pytest.raises(DgError):
+        op.apply_planes(x, x[:op.plane_ndofs], x[:op.plane_ndofs], torch.empty_like(x), 0, w.N[0] + 1)
+    with pytest.raises(DgError):
+        op.apply(x.float())
+    op.close()
