@@ -121,13 +121,15 @@ def oracle_sample_rate(w, budget_s: float, seed: int = 2024):
         return time.perf_counter() - t0
 
     th = oracle.num_threads()
-    probe = max(th, 8)
-    t1 = run(probe)
-    t4 = run(4 * probe)
-    per_cell = max((t4 - t1) / (3 * probe), 1e-9)   # t(n) = setup + per_cell n
-    setup = max(t1 - per_cell * probe, 0.0)
-    ncell = int(min(w.ncells, max(probe, (budget_s - setup) / per_cell)))
+    ncell = max(th, 8)
     t = run(ncell)
+    while t < 0.2 * budget_s and ncell < w.ncells:      # grow the probe until it costs ~20% of the budget
+        ncell = min(w.ncells, ncell * 4)
+        t = run(ncell)
+    target = int(min(w.ncells, max(ncell, ncell * budget_s / max(t, 1e-9))))
+    if target > ncell * 1.2:
+        ncell = target
+        t = run(ncell)
     return ncell * n3 / t, ncell, t, th
 
 
