@@ -1,8 +1,11 @@
 // libdg C-ABI (include/dg.h): context setup, kernel dispatch, slab / host-pipelined apply.
 #include "../../include/dg.h"
 #include "common.cuh"
+#include "kernel_axis8.cuh"
 #include "kernel_cell.cuh"
 #include "tables.h"
+
+#include <cudaTypedefs.h>
 
 #include <cstdarg>
 #include <cstdio>
@@ -85,6 +88,64 @@ void fill_tab(const dg::HostTables& H, void* out)
     }
 }
 
+// B^ = D^T W D + 1/2 (e0 d0^T + d0 e0^T - e1 d1^T - d1 e1^T) + P (e0 e0^T + e1 e1^T)  (see kernel_axis8.cuh)
+void build_axis8(const dg::HostTables& H, double P, const double h[3], dg::AxisTab8* A)
+{
+    const int n = 8, m = 4;
+    double B[8][8];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (int q = 0; q < n; ++q) s += H.D[q * n + i] * H.w[q] * H.D[q * n + j];
+            s += 0.5 * (H.e0[i] * H.d0[j] + H.d0[i] * H.e0[j] - H.e1[i] * H.d1[j] - H.d1[i] * H.e1[j]);
+            s += P * (H.e0[i] * H.e0[j] + H.e1[i] * H.e1[j]);
+            B[i][j] = s;
+        }
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+            A->Ee[i][j] = 0.5 * (B[i][j] + B[i][n - 1 - j]);
+            A->Oo[i][j] = 0.5 * (B[i][j] - B[i][n - 1 - j]);
+        }
+    double aL[8], bL[8], aR[8], bR[8];
+    for (int i = 0; i < n; ++i) {
+        aL[i] = -0.5 * H.d0[i] - P * H.e0[i];
+        bL[i] = 0.5 * H.e0[i];
+        aR[i] = 0.5 * H.d1[i] - P * H.e1[i];
+        bR[i] = -0.5 * H.e1[i];
+    }
+    for (int i = 0; i < m; ++i) {
+        A->te[i] = 0.5 * (H.e0[i] + H.e0[n - 1 - i]);
+        A->to[i] = 0.5 * (H.e0[i] - H.e0[n - 1 - i]);
+        A->qe[i] = 0.5 * (H.d0[i] + H.d0[n - 1 - i]);
+        A->qo[i] = 0.5 * (H.d0[i] - H.d0[n - 1 - i]);
+        A->aue[i] = 0.5 * (aL[i] + aR[i]);
+        A->age[i] = 0.5 * (bL[i] - bR[i]);
+        A->auo[i] = 0.5 * (aL[i] - aR[i]);
+        A->ago[i] = 0.5 * (bL[i] + bR[i]);
+    }
+    for (int i = 0; i < n; ++i) {
+        A->e0[i] = H.e0[i];
+        A->d0[i] = H.d0[i];
+        A->w[i] = H.w[i];
+    }
+    A->c[0] = h[1] * h[2] / h[0];
+    A->c[1] = h[0] * h[2] / h[1];
+    A->c[2] = h[0] * h[1] / h[2];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
 } // namespace
 
 struct dg_ctx {
@@ -96,6 +157,11 @@ struct dg_ctx {
     alignas(16) unsigned char tab[sizeof(dg::Tab<dg::kMaxN>)];
     LaunchFn launch;
     const char* kname;
+    // axis-aligned n = 8 fast path (k_axis8)
+    bool ax8;
+    dg::AxisTab8 atab;
+    CUtensorMap tmap;
+    const double* tmap_ptr;
     double* d_jac;
     // host-pipeline state (dg_apply_host)
     double* hx_d;
@@ -103,6 +169,30 @@ struct dg_ctx {
     cudaStream_t s_h2d, s_d2h, s_cmp;
     int64_t plane_dofs, local_dofs;
 };
+
+static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0,
+                                 int p1, cudaStream_t st)
+{
+    if (p1 <= p0) return cudaSuccess;
+    if (c->ax8) {
+        if (c->tmap_ptr != x) {
+            cuuint64_t dims[2] = {16, (cuuint64_t)(c->local_dofs / 16)};
+            cuuint64_t strides[1] = {128};
+            cuuint32_t box[2] = {16, (cuuint32_t)(dg::ax8::T * 32)};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult rc = get_encode()(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)x, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (rc != CUDA_SUCCESS) return cudaErrorInvalidValue;
+            c->tmap_ptr = x;
+        }
+        const unsigned grid = (unsigned)((c->M.N1 / dg::ax8::T) * (c->M.N2 / dg::ax8::T));
+        dg::k_axis8<<<grid, dg::ax8::NT, dg::ax8::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, c->atab, c->M);
+        return cudaGetLastError();
+    }
+    const long long pc = c->M.plane_cells;
+    return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st);
+}
 
 extern "C" {
 
@@ -180,6 +270,14 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     }
     c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
     c->kname = "k_cell_general";
+    c->ax8 = (n == 8 && mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE &&
+              mesh->N[1] % dg::ax8::T == 0 && mesh->N[2] % dg::ax8::T == 0 && getenv("DG_FORCE_GENERAL") == nullptr);
+    if (c->ax8) {
+        build_axis8(H, mesh->penalty_scale * k * (k + 1), M.h, &c->atab);
+        cudaError_t e = cudaFuncSetAttribute(dg::k_axis8, cudaFuncAttributeMaxDynamicSharedMemorySize, dg::ax8::SMEM_BYTES);
+        if (e != cudaSuccess || !get_encode()) c->ax8 = false;
+        else c->kname = "k_axis8";
+    }
     *out = c;
     return DG_OK;
 }
@@ -248,8 +346,8 @@ int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* 
     if (xs < rs + bytes && rs < xs + bytes) return fail(DG_ERR_INVALID, "dg_apply: x and r overlap");
     if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 7)
         return fail(DG_ERR_INVALID, "dg_apply: pointers must be 8-byte aligned");
-    const long long pc = c->M.plane_cells;
-    cudaError_t e = c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, c->stream);
+    if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned");
+    cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
     return DG_OK;
 }
@@ -304,9 +402,8 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
     for (int i = 0; i < nch; ++i) {
         const int need = (i + 1 < nch) ? i + 1 : nch - 1;
         CU(cudaStreamWaitEvent(c->s_cmp, ev_in[need], 0));
-        cudaError_t e = c->launch(c->tab, c->M, c->hx_d, c->hx_d + (size_t)(L - 1) * pd, c->hx_d, c->hr_d,
-                                  (long long)bnd[i] * c->M.plane_cells, (long long)bnd[i + 1] * c->M.plane_cells,
-                                  c->s_cmp);
+        cudaError_t e = launch_planes(c, c->hx_d, c->hx_d + (size_t)(L - 1) * pd, c->hx_d, c->hr_d, bnd[i],
+                                      bnd[i + 1], c->s_cmp);
         if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply_host: launch: %s", cudaGetErrorString(e));
         CU(cudaEventRecord(ev_cmp[i], c->s_cmp));
         CU(cudaStreamWaitEvent(c->s_d2h, ev_cmp[i], 0));

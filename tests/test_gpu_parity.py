@@ -165,3 +165,60 @@ def test_apply_rejects_bad_arguments():
     with pytest.raises(DgError):
         op.apply(x.float())
     op.close()
+
+
+@pytest.mark.parametrize("N", [(3, 4, 8), (2, 4, 4), (5, 8, 12), (4, 12, 4)])
+def test_axis8_fast_path_small(N):
+    """k_axis8 (axis-aligned, n = 8, 4x4 tiles marching along x0) on meshes with 1-3 tiles per
+    direction (ring cells that wrap onto the tile itself) against the oracle."""
+    from paper_1812_08075_b200 import Operator
+    w = synth.small(7, N, seed=31)
+    op = _op(w)
+    assert op.kernel_name == "k_axis8"
+    op.close()
+    assert _full_check(w) <= TOL
+
+
+def test_axis8_matches_general_kernel():
+    import os
+    w = synth.small(7, (4, 8, 8), seed=8)
+    x = synth.x_torch(w, device="cuda")
+    fast = _op(w)
+    os.environ["DG_FORCE_GENERAL"] = "1"
+    try:
+        gen = _op(w)
+    finally:
+        del os.environ["DG_FORCE_GENERAL"]
+    assert fast.kernel_name == "k_axis8" and gen.kernel_name == "k_cell_general"
+    a = fast.apply(x)
+    b = gen.apply(x)
+    assert (a - b).abs().max().item() <= 1e-13 * b.abs().max().item()
+    fast.close()
+    gen.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_axis8_slab_loopback_bitwise(world):
+    from paper_1812_08075_b200 import Operator, slab
+    w = synth.small(7, (10, 8, 4), seed=12)
+    full = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    ref = full.apply(x)
+    pd = full.plane_ndofs
+    got = torch.full_like(x, float("nan"))
+    for q in range(world):
+        p = slab.plan(w.N[0], q, world)
+        op = Operator(w.N, w.k, plane_begin=p.plane_begin, nplanes=p.nplanes)
+        xs = x[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        rs = got[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        hb = x[((p.plane_begin - 1) % w.N[0]) * pd:][:pd].clone()
+        ha = x[((p.plane_begin + p.nplanes) % w.N[0]) * pd:][:pd].clone()
+        a, b = p.interior
+        if b > a:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        for a, b in p.boundary:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        torch.cuda.synchronize()
+        op.close()
+    assert torch.equal(got, ref)
+    full.close()
