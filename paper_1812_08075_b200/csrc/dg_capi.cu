@@ -159,9 +159,11 @@ struct dg_ctx {
     const char* kname;
     // axis-aligned n = 8 fast path (k_axis8)
     bool ax8;
+    int ax8_tile, ax8_T1, ax8_T2;
     dg::AxisTab8 atab;
     CUtensorMap tmap;
     const double* tmap_ptr;
+    long long* dbg; // DG_TRACE: device buffer of per-phase clock64 stamps (k_axis8)
     double* d_jac;
     // host-pipeline state (dg_apply_host)
     double* hx_d;
@@ -178,7 +180,7 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         if (c->tmap_ptr != x) {
             cuuint64_t dims[2] = {16, (cuuint64_t)(c->local_dofs / 16)};
             cuuint64_t strides[1] = {128};
-            cuuint32_t box[2] = {16, (cuuint32_t)(dg::ax8::T * 32)};
+            cuuint32_t box[2] = {16, (cuuint32_t)(c->ax8_T2 * 32)};
             cuuint32_t estr[2] = {1, 1};
             CUresult rc = get_encode()(&c->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)x, dims, strides, box, estr,
                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -186,8 +188,16 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
             if (rc != CUDA_SUCCESS) return cudaErrorInvalidValue;
             c->tmap_ptr = x;
         }
-        const unsigned grid = (unsigned)((c->M.N1 / dg::ax8::T) * (c->M.N2 / dg::ax8::T));
-        dg::k_axis8<<<grid, dg::ax8::NT, dg::ax8::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, c->atab, c->M);
+        const unsigned grid = (unsigned)((c->M.N1 / c->ax8_T1) * (c->M.N2 / c->ax8_T2));
+        if (c->ax8_tile == 0)
+            dg::k_axis8<2, 4, 256><<<grid, 256, dg::ax8::Cfg<2, 4, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1,
+                                                                                          c->atab, c->M, c->dbg);
+        else if (c->ax8_tile == 1)
+            dg::k_axis8<4, 4, 512><<<grid, 512, dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1,
+                                                                                          c->atab, c->M, c->dbg);
+        else
+            dg::k_axis8<4, 2, 256><<<grid, 256, dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1,
+                                                                                          c->atab, c->M, c->dbg);
         return cudaGetLastError();
     }
     const long long pc = c->M.plane_cells;
@@ -270,13 +280,37 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     }
     c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
     c->kname = "k_cell_general";
-    c->ax8 = (n == 8 && mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE &&
-              mesh->N[1] % dg::ax8::T == 0 && mesh->N[2] % dg::ax8::T == 0 && getenv("DG_FORCE_GENERAL") == nullptr);
+    // axis-aligned Q7 fast path: tile T1 x T2 (env DG_AX8_TILE = 2x4 | 4x4 | 4x2 for experiments)
+    {
+        const char* tv = getenv("DG_AX8_TILE");
+        c->ax8_tile = 0;
+        if (tv && !strcmp(tv, "4x4")) c->ax8_tile = 1;
+        if (tv && !strcmp(tv, "4x2")) c->ax8_tile = 2;
+        const int T1 = (c->ax8_tile == 1 || c->ax8_tile == 2) ? 4 : 2;
+        const int T2 = (c->ax8_tile == 2) ? 2 : 4;
+        c->ax8_T1 = T1;
+        c->ax8_T2 = T2;
+        c->ax8 = (n == 8 && mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE &&
+                  mesh->N[1] % T1 == 0 && mesh->N[2] % T2 == 0 && getenv("DG_FORCE_GENERAL") == nullptr);
+    }
     if (c->ax8) {
         build_axis8(H, mesh->penalty_scale * k * (k + 1), M.h, &c->atab);
-        cudaError_t e = cudaFuncSetAttribute(dg::k_axis8, cudaFuncAttributeMaxDynamicSharedMemorySize, dg::ax8::SMEM_BYTES);
+        cudaError_t e = cudaSuccess;
+        if (c->ax8_tile == 0)
+            e = cudaFuncSetAttribute(dg::k_axis8<2, 4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     dg::ax8::Cfg<2, 4, 256>::SMEM_BYTES);
+        else if (c->ax8_tile == 1)
+            e = cudaFuncSetAttribute(dg::k_axis8<4, 4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES);
+        else
+            e = cudaFuncSetAttribute(dg::k_axis8<4, 2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES);
         if (e != cudaSuccess || !get_encode()) c->ax8 = false;
         else c->kname = "k_axis8";
+        if (c->ax8 && getenv("DG_TRACE")) {
+            if (cudaMalloc(&c->dbg, sizeof(long long) * 1024 * 16 * 8) != cudaSuccess) c->dbg = nullptr;
+            else cudaMemset(c->dbg, 0, sizeof(long long) * 1024 * 16 * 8);
+        }
     }
     *out = c;
     return DG_OK;
@@ -287,6 +321,15 @@ int dg_destroy(dg_ctx* c)
     if (!c) return DG_OK;
     cudaSetDevice(c->device);
     if (c->d_jac) cudaFree(c->d_jac);
+    if (c->dbg) {
+        // DG_TRACE: dump the stamps of the last launch
+        static long long h[1024 * 16 * 8];
+        if (cudaMemcpy(h, c->dbg, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            FILE* f = fopen(getenv("DG_TRACE"), "wb");
+            if (f) { fwrite(h, sizeof h, 1, f); fclose(f); }
+        }
+        cudaFree(c->dbg);
+    }
     if (c->hx_d) cudaFree(c->hx_d);
     if (c->hr_d) cudaFree(c->hr_d);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);

@@ -15,13 +15,15 @@
 // direction. B^ is centro-symmetric (symmetric Gauss nodes), so every line product
 // runs in even/odd form: 2 (4x4) products instead of one 8x8.
 //
-// Mapping (B200): one CTA (256 threads, 1 per SM, 192 KB smem) owns a 4x4 tile of cells in
-// (i1, i2) and MARCHES along i0 through the planes [p_begin, p_end):
+// Mapping (B200): one CTA owns a T1 x T2 tile of cells in (i1, i2) (2x4 with 256 threads and
+// 97 KB smem, 2 CTAs per SM; or 4x4 / 512 threads / 193 KB) and MARCHES along i0 through the
+// planes [p_begin, p_end):
 //   * each plane's 16 blocks (64 KB) arrive by TMA (cp.async.bulk.tensor, 128B swizzle) into a
 //     double buffer one plane ahead of use;
-//   * pass d=1 and pass d=2: a thread owns one line position across the 4 cells of a tile row,
-//     so neighbour traces inside the tile stay in registers; the ring cells outside the tile are
-//     read from L2 (their owner CTAs stream them concurrently);
+//   * pass d=1 and pass d=2: a thread owns one line position across up to 2 cells of a tile row
+//     (and its partner lane, lane ^ 16, the other 2 of a 4-cell row), so the neighbour traces
+//     inside the tile stay in registers (one shuffle pair per pass); the ring cells outside the
+//     tile are read from L2 (their owner CTAs stream them concurrently);
 //   * pass d=0 (the marching direction): the lower neighbour's traces are carried in registers
 //     from the previous plane, the upper neighbour's come from the prefetched next plane;
 //   * partial sums of the three passes meet in a swizzled smem buffer; the d=0 pass adds them
@@ -45,10 +47,19 @@ struct AxisTab8 {
 
 namespace ax8 {
 
-constexpr int N = 8, T = 4, NT = 256;
-constexpr int CELL_BYTES = N * N * N * 8;        // 4096
-constexpr int BUF_BYTES = T * T * CELL_BYTES;    // 65536
-constexpr int SMEM_BYTES = 3 * BUF_BYTES + 1024; // X0, X1, R (+ barriers, alignment slack)
+constexpr int N = 8;
+constexpr int CELL_BYTES = N * N * N * 8; // 4096
+
+// tile T1 x T2 cells in (i1, i2), NT threads
+template <int T1, int T2, int NT>
+struct Cfg {
+    static constexpr int CELLS = T1 * T2;
+    static constexpr int BUF_BYTES = CELLS * CELL_BYTES;
+    static constexpr int SMEM_BYTES = 3 * BUF_BYTES + 1024; // X0, X1, R (+ barriers, alignment slack)
+    static constexpr int WARPS = NT / 32;
+    static_assert(WARPS == CELLS, "pass d=0 maps one warp per cell");
+    static constexpr int MINB = (SMEM_BYTES <= 113 * 1024) ? 2 : 1;
+};
 
 __device__ __forceinline__ uint32_t swz(uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
 
@@ -57,18 +68,29 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p)
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+__device__ __forceinline__ double lds(uint32_t a)
 {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds2(uint32_t a, double& x, double& y)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ void sts(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
 {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
     asm volatile(
         "{\n"
@@ -76,17 +98,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
+        "}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar)
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar)
 {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
 
@@ -127,23 +149,138 @@ __device__ __forceinline__ void traces_eo(const AxisTab8& A, const double xe[4],
     g1 = d - c;
 }
 
+
+
+// In-plane pass (pd = 1: lines along j1 / neighbours along i1; pd = 2: along j2 / i2).
+// TL = tile cells along the pass direction, TW = across. G = threads per tile row (1 or 2).
+template <int pd, int TL, int TW, int NT>
+__device__ __forceinline__ void inplane_pass(const AxisTab8& A, const MeshArgs& M, const double* __restrict__ x, uint32_t X,
+                                             uint32_t R, int lp, int ti1, int ti2, int tid, double S)
+{
+    constexpr int G = (64 * TW * TL / NT == TL) ? 1 : 2; // cells per thread == TL -> one thread per row
+    constexpr int CPT = TL / G;
+    static_assert(G * CPT == TL && 64 * TW * G == NT, "pass mapping");
+    constexpr int T1 = (pd == 1) ? TL : TW, T2 = (pd == 1) ? TW : TL;
+    const int j0 = tid & 7, jb = (tid >> 3) & 1, hb = (tid >> 4) & 1, rest = tid >> 5;
+    int half, jt, tw;
+    if (G == 2) { half = hb; jt = jb + 2 * (rest & 3); tw = rest >> 2; }
+    else        { half = 0;  jt = jb + 2 * hb + 4 * (rest & 1); tw = rest >> 1; }
+    auto eoff = [&](int j) { return pd == 1 ? j0 + 8 * j + 64 * jt : j0 + 8 * jt + 64 * j; };
+    auto bcell = [&](int cc) { const int a = half * CPT + cc; return pd == 1 ? a * T2 + tw : tw * T2 + a; };
+    auto cidx = [&](int i1, int i2) -> long long { return (long long)lp * M.plane_cells + (long long)i1 * M.N2 + i2; };
+    // ring cells (tile neighbours along the pass direction)
+    long long rlo, rhi;
+    if (pd == 1) {
+        rlo = cidx((ti1 * T1 - 1 + M.N1) % M.N1, ti2 * T2 + tw);
+        rhi = cidx((ti1 * T1 + T1) % M.N1, ti2 * T2 + tw);
+    } else {
+        rlo = cidx(ti1 * T1 + tw, (ti2 * T2 - 1 + M.N2) % M.N2);
+        rhi = cidx(ti1 * T1 + tw, (ti2 * T2 + T2) % M.N2);
+    }
+    constexpr int NR = (G == 1) ? 2 : 1;
+    double rv[NR][8];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        const double* g = x + ((G == 1 ? (k ? rhi : rlo) : (half ? rhi : rlo))) * 512;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) rv[k][j] = __ldg(g + eoff(j));
+    }
+    double xe[CPT][4], xo[CPT][4], u0[CPT], u1[CPT], g0[CPT], g1[CPT];
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+        const uint32_t cb = X + bcell(cc) * CELL_BYTES;
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = lds(cb + swz(8 * eoff(j)));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { xe[cc][j] = v[j] + v[7 - j]; xo[cc][j] = v[j] - v[7 - j]; }
+        traces_eo(A, xe[cc], xo[cc], u0[cc], u1[cc], g0[cc], g1[cc]);
+    }
+    // ring traces: lower ring cell -> (e1.x, d1.x); upper -> (e0.x, d0.x)
+    double loU = 0, loG = 0, hiU = 0, hiG = 0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        const bool up = (G == 1) ? (k == 1) : (half == 1);
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            a = fma(up ? A.e0[j] : A.e0[7 - j], rv[k][j], a);
+            b = fma(up ? A.d0[j] : -A.d0[7 - j], rv[k][j], b);
+        }
+        if (G == 1) { if (k) { hiU = a; hiG = b; } else { loU = a; loG = b; } }
+        else { loU = hiU = a; loG = hiG = b; }
+    }
+    double recvU = 0.0, recvG = 0.0;
+    if (G == 2) {
+        const double sendU = half ? u0[0] : u1[CPT - 1];
+        const double sendG = half ? g0[0] : g1[CPT - 1];
+        recvU = __shfl_xor_sync(0xffffffffu, sendU, 16);
+        recvG = __shfl_xor_sync(0xffffffffu, sendG, 16);
+    }
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) {
+        double uL, gL, uR, gR;
+        if (cc > 0) { uL = u1[cc - 1]; gL = g1[cc - 1]; }
+        else if (G == 2 && half) { uL = recvU; gL = recvG; }
+        else { uL = loU; gL = loG; }
+        if (cc < CPT - 1) { uR = u0[cc + 1]; gR = g0[cc + 1]; }
+        else if (G == 2 && !half) { uR = recvU; gR = recvG; }
+        else { uR = hiU; gR = hiG; }
+        double ye[4], yo[4];
+        line_eo(A, xe[cc], xo[cc], uL, gL, uR, gR, ye, yo);
+        const uint32_t rb = R + bcell(cc) * CELL_BYTES;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t p0 = rb + swz(8 * eoff(i));
+            const uint32_t p1 = rb + swz(8 * eoff(7 - i));
+            if (pd == 1) {
+                sts(p0, S * (ye[i] + yo[i]));
+                sts(p1, S * (ye[i] - yo[i]));
+            } else {
+                sts(p0, fma(S, ye[i] + yo[i], lds(p0)));
+                sts(p1, fma(S, ye[i] - yo[i], lds(p1)));
+            }
+        }
+    }
+}
+
+// thread's tangential weights product for the in-plane passes (same decomposition as above)
+template <int pd, int TL, int TW, int NT>
+__device__ __forceinline__ double inplane_scale(const AxisTab8& A, int tid)
+{
+    constexpr int G = (64 * TW * TL / NT == TL) ? 1 : 2;
+    const int j0 = tid & 7, jb = (tid >> 3) & 1, hb = (tid >> 4) & 1, rest = tid >> 5;
+    const int jt = (G == 2) ? jb + 2 * (rest & 3) : jb + 2 * hb + 4 * (rest & 1);
+    double wj0 = 0.0, wjt = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { // uniform-index table reads (no divergent constant loads)
+        wj0 = (i == j0) ? A.w[i] : wj0;
+        wjt = (i == jt) ? A.w[i] : wjt;
+    }
+    return wj0 * wjt * A.c[pd];
+}
+
 } // namespace ax8
 
-// grid: (N1/4) * (N2/4) CTAs, block 256, dynamic smem ax8::SMEM_BYTES
-__global__ void __launch_bounds__(ax8::NT, 1)
+// grid: (N1/T1) * (N2/T2) CTAs, block NT, dynamic smem Cfg::SMEM_BYTES
+template <int T1, int T2, int NT>
+__global__ void __launch_bounds__(NT, ax8::Cfg<T1, T2, NT>::MINB)
 k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, const double* __restrict__ xb,
         const double* __restrict__ xa, double* __restrict__ r, int p_begin, int p_end, const AxisTab8 A,
-        const MeshArgs M)
+        const MeshArgs M, long long* __restrict__ dbg)
 {
     using namespace ax8;
+    using C = Cfg<T1, T2, NT>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* bufX[2] = {smem, smem + BUF_BYTES};
-    unsigned char* bufR = smem + 2 * BUF_BYTES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * BUF_BYTES);
+    // 32-bit shared-window addresses (explicit ld/st.shared; 1024-aligned for the 128B swizzle)
+    const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    const uint32_t bufX[2] = {sbase, sbase + C::BUF_BYTES};
+    const uint32_t bufR = sbase + 2 * C::BUF_BYTES;
+    const uint32_t bar0 = sbase + 3 * C::BUF_BYTES;
+    auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int ntile2 = M.N2 / T;
+    const int ntile2 = M.N2 / T2;
     const int ti1 = blockIdx.x / ntile2, ti2 = blockIdx.x % ntile2;
     const int PC = M.plane_cells;
     const int nsteps = p_end - p_begin;
@@ -151,40 +288,56 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
 
     auto cell_index = [&](int lp, int i1, int i2) -> long long { return (long long)lp * PC + (long long)i1 * M.N2 + i2; };
 
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+    // the TMA producer is lane 0 of the last warp (warp 0 carries the trace stamps)
+    const bool producer = (tid == NT - 32);
+    if (producer) {
+        mbar_init(bar(0), 1);
+        mbar_init(bar(1), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
     }
     __syncthreads();
 
     auto issue = [&](int step) {
-        // TMA the 16 blocks of plane p_begin + step into buffer (step & 1): one 16 KB box per tile row
+        // TMA the T1 x T2 blocks of plane p_begin + step into buffer (step & 1): one box per tile row
         const int lp = p_begin + step;
-        uint64_t* b = &bar[step & 1];
-        mbar_expect_tx(b, BUF_BYTES);
+        const uint32_t b = bar(step & 1);
+        mbar_expect_tx(b, C::BUF_BYTES);
 #pragma unroll
-        for (int c1 = 0; c1 < T; ++c1) {
-            const long long cell = cell_index(lp, ti1 * T + c1, ti2 * T);
-            tma_load_2d(bufX[step & 1] + c1 * T * CELL_BYTES, &tmx, 0, (int)(cell * (CELL_BYTES / 128)), b);
+        for (int c1 = 0; c1 < T1; ++c1) {
+            const long long cell = cell_index(lp, ti1 * T1 + c1, ti2 * T2);
+            tma_load_2d(bufX[step & 1] + c1 * T2 * CELL_BYTES, &tmx, 0, (int)(cell * (CELL_BYTES / 128)), b);
         }
     };
-    if (tid == 0) {
+    if (producer) {
         issue(0);
         if (nsteps > 1) issue(1);
     }
 
-    // ---- d=0 mapping: warp w owns cells 2w, 2w+1 (buffer order c1*4+c2); lanes own lines L, L+32
-    const int dcell0 = 2 * warp;
-    double prevU[4], prevG[4]; // traces e1.x, d1.x of the lower x0-neighbour for the thread's 4 lines
-    {
-        // prologue: lower neighbour plane p_begin - 1 (halo x_below if p_begin == 0)
+    const double S1 = inplane_scale<1, T1, T2, NT>(A, tid);
+    const double S2 = inplane_scale<2, T2, T1, NT>(A, tid);
+    // d=0 mapping: warp w owns cell w (buffer order c1*T2+c2); lanes own lines L = lane, lane + 32
+    const int dc1 = warp / T2, dc2 = warp % T2;
+    const long long d0_inplane = (long long)(ti1 * T1 + dc1) * M.N2 + ti2 * T2 + dc2;
+    double S0[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int cb = dcell0 + (q >> 1), L = lane + 32 * (q & 1);
-            const int c1 = cb >> 2, c2 = cb & 3;
-            const long long inplane = (long long)(ti1 * T + c1) * M.N2 + ti2 * T + c2;
-            const double* src = (p_begin == 0) ? xb + inplane * 512 : x + (cell_index(p_begin - 1, 0, 0) + inplane) * 512;
+    for (int q = 0; q < 2; ++q) {
+        const int L = lane + 32 * q;
+        double wa = 0.0, wb = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            wa = ((L & 7) == i) ? A.w[i] : wa;
+            wb = ((L >> 3) == i) ? A.w[i] : wb;
+        }
+        S0[q] = wa * wb * A.c[0];
+    }
+
+    double prevU[2], prevG[2]; // traces e1.x, d1.x of the lower x0-neighbour, per d=0 line
+    {
+        const double* src = (p_begin == 0) ? xb + d0_inplane * 512 : x + (cell_index(p_begin - 1, 0, 0) + d0_inplane) * 512;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int L = lane + 32 * q;
             const double2* s2 = reinterpret_cast<const double2*>(src + 8 * L);
             double v[8];
 #pragma unroll
@@ -203,138 +356,47 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
         }
     }
 
+    // optional phase timestamps (DG_TRACE): dbg[block][step][phase], first 16 steps
+    const bool trace = dbg != nullptr && tid == 0 && blockIdx.x < 1024;
+    auto stamp = [&](int s, int ph) {
+        if (trace && s < 16) dbg[(blockIdx.x * 16 + s) * 8 + ph] = clock64();
+    };
     for (int s = 0; s < nsteps; ++s) {
         const int lp = p_begin + s;
-        const unsigned char* X = bufX[s & 1];
-        mbar_wait(&bar[s & 1], (s >> 1) & 1);
+        const uint32_t X = bufX[s & 1];
+        stamp(s, 0);
+        mbar_wait(bar(s & 1), (s >> 1) & 1);
+        stamp(s, 1);
 
-        // ================= pass d = 1 (lines along j1; neighbours along i1) =================
-        {
-            const int j0 = lane & 7, j2 = (lane >> 3) + 4 * (warp & 1), c2 = warp >> 1;
-            const int i2 = ti2 * T + c2;
-            const int i1L = (ti1 * T - 1 + M.N1) % M.N1, i1R = (ti1 * T + T) % M.N1;
-            const double* gl = x + cell_index(lp, i1L, i2) * 512 + j0 + 64 * j2;
-            const double* gr = x + cell_index(lp, i1R, i2) * 512 + j0 + 64 * j2;
-            double rl[8], rr[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { rl[j] = __ldg(gl + 8 * j); rr[j] = __ldg(gr + 8 * j); }
-            double xe[T][4], xo[T][4], u0[T], u1[T], g0[T], g1[T];
-#pragma unroll
-            for (int c1 = 0; c1 < T; ++c1) {
-                const unsigned char* cb = X + (c1 * T + c2) * CELL_BYTES;
-                double v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const double*>(cb + swz(8 * (j0 + 8 * j + 64 * j2)));
-#pragma unroll
-                for (int j = 0; j < 4; ++j) { xe[c1][j] = v[j] + v[7 - j]; xo[c1][j] = v[j] - v[7 - j]; }
-                ax8::traces_eo(A, xe[c1], xo[c1], u0[c1], u1[c1], g0[c1], g1[c1]);
-            }
-            double uLr, gLr, uRr, gRr;
-            {
-                double a = 0, b = 0, c = 0, d = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    a = fma(A.e0[7 - j], rl[j], a);  // e1.x_L (e1_j = e0_{7-j})
-                    b = fma(-A.d0[7 - j], rl[j], b); // d1.x_L (d1_j = -d0_{7-j})
-                    c = fma(A.e0[j], rr[j], c);
-                    d = fma(A.d0[j], rr[j], d);
-                }
-                uLr = a; gLr = b; uRr = c; gRr = d;
-            }
-            const double S = A.w[j0] * A.w[j2] * A.c[1];
-#pragma unroll
-            for (int c1 = 0; c1 < T; ++c1) {
-                const double uL = c1 > 0 ? u1[c1 - 1] : uLr, gL = c1 > 0 ? g1[c1 - 1] : gLr;
-                const double uR = c1 < T - 1 ? u0[c1 + 1] : uRr, gR = c1 < T - 1 ? g0[c1 + 1] : gRr;
-                double ye[4], yo[4];
-                ax8::line_eo(A, xe[c1], xo[c1], uL, gL, uR, gR, ye, yo);
-                unsigned char* rb = bufR + (c1 * T + c2) * CELL_BYTES;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    *reinterpret_cast<double*>(rb + swz(8 * (j0 + 8 * i + 64 * j2))) = S * (ye[i] + yo[i]);
-                    *reinterpret_cast<double*>(rb + swz(8 * (j0 + 8 * (7 - i) + 64 * j2))) = S * (ye[i] - yo[i]);
-                }
-            }
-        }
+        inplane_pass<1, T1, T2, NT>(A, M, x, X, bufR, lp, ti1, ti2, tid, S1);
+        stamp(s, 2);
         __syncthreads();
-
-        // ================= pass d = 2 (lines along j2; neighbours along i2) =================
-        {
-            const int j0 = lane & 7, j1 = (lane >> 3) + 4 * (warp & 1), c1 = warp >> 1;
-            const int i1 = ti1 * T + c1;
-            const int i2L = (ti2 * T - 1 + M.N2) % M.N2, i2R = (ti2 * T + T) % M.N2;
-            const double* gl = x + cell_index(lp, i1, i2L) * 512 + j0 + 8 * j1;
-            const double* gr = x + cell_index(lp, i1, i2R) * 512 + j0 + 8 * j1;
-            double rl[8], rr[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { rl[j] = __ldg(gl + 64 * j); rr[j] = __ldg(gr + 64 * j); }
-            double xe[T][4], xo[T][4], u0[T], u1[T], g0[T], g1[T];
-#pragma unroll
-            for (int c2 = 0; c2 < T; ++c2) {
-                const unsigned char* cb = X + (c1 * T + c2) * CELL_BYTES;
-                double v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const double*>(cb + swz(8 * (j0 + 8 * j1 + 64 * j)));
-#pragma unroll
-                for (int j = 0; j < 4; ++j) { xe[c2][j] = v[j] + v[7 - j]; xo[c2][j] = v[j] - v[7 - j]; }
-                ax8::traces_eo(A, xe[c2], xo[c2], u0[c2], u1[c2], g0[c2], g1[c2]);
-            }
-            double uLr, gLr, uRr, gRr;
-            {
-                double a = 0, b = 0, c = 0, d = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    a = fma(A.e0[7 - j], rl[j], a);
-                    b = fma(-A.d0[7 - j], rl[j], b);
-                    c = fma(A.e0[j], rr[j], c);
-                    d = fma(A.d0[j], rr[j], d);
-                }
-                uLr = a; gLr = b; uRr = c; gRr = d;
-            }
-            const double S = A.w[j0] * A.w[j1] * A.c[2];
-#pragma unroll
-            for (int c2 = 0; c2 < T; ++c2) {
-                const double uL = c2 > 0 ? u1[c2 - 1] : uLr, gL = c2 > 0 ? g1[c2 - 1] : gLr;
-                const double uR = c2 < T - 1 ? u0[c2 + 1] : uRr, gR = c2 < T - 1 ? g0[c2 + 1] : gRr;
-                double ye[4], yo[4];
-                ax8::line_eo(A, xe[c2], xo[c2], uL, gL, uR, gR, ye, yo);
-                unsigned char* rb = bufR + (c1 * T + c2) * CELL_BYTES;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    double* p0 = reinterpret_cast<double*>(rb + swz(8 * (j0 + 8 * j1 + 64 * i)));
-                    double* p1 = reinterpret_cast<double*>(rb + swz(8 * (j0 + 8 * j1 + 64 * (7 - i))));
-                    *p0 = fma(S, ye[i] + yo[i], *p0);
-                    *p1 = fma(S, ye[i] - yo[i], *p1);
-                }
-            }
-        }
+        stamp(s, 3);
+        inplane_pass<2, T2, T1, NT>(A, M, x, X, bufR, lp, ti1, ti2, tid, S2);
+        stamp(s, 4);
         __syncthreads();
+        stamp(s, 5);
 
         // ================= pass d = 0 (lines along j0; neighbours along i0: marching) =================
         {
             const bool last = (s == nsteps - 1);
-            if (!last) mbar_wait(&bar[(s + 1) & 1], ((s + 1) >> 1) & 1);
-            const unsigned char* XN = bufX[(s + 1) & 1];
+            if (!last) mbar_wait(bar((s + 1) & 1), ((s + 1) >> 1) & 1);
+            const uint32_t XN = bufX[(s + 1) & 1];
+            const int cb = warp;
+            const double* nsrc = (p_end == M.L) ? xa + d0_inplane * 512 : x + (cell_index(p_end, 0, 0) + d0_inplane) * 512;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int cb = dcell0 + (q >> 1), L = lane + 32 * (q & 1);
-                const int c1 = cb >> 2, c2 = cb & 3;
-                const long long inplane = (long long)(ti1 * T + c1) * M.N2 + ti2 * T + c2;
+            for (int q = 0; q < 2; ++q) {
+                const int L = lane + 32 * q;
                 // upper neighbour's traces e0.x, d0.x
                 double uR = 0.0, gR = 0.0;
                 {
                     double v[8];
                     if (!last) {
-                        const unsigned char* nb = XN + cb * CELL_BYTES;
+                        const uint32_t nb = XN + cb * CELL_BYTES;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            double2 t = *reinterpret_cast<const double2*>(nb + swz(8 * (8 * L + 2 * k)));
-                            v[2 * k] = t.x;
-                            v[2 * k + 1] = t.y;
-                        }
+                        for (int k = 0; k < 4; ++k) lds2(nb + swz(8 * (8 * L + 2 * k)), v[2 * k], v[2 * k + 1]);
                     } else {
-                        const double* src = (p_end == M.L) ? xa + inplane * 512 : x + (cell_index(p_end, 0, 0) + inplane) * 512;
-                        const double2* s2 = reinterpret_cast<const double2*>(src + 8 * L);
+                        const double2* s2 = reinterpret_cast<const double2*>(nsrc + 8 * L);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             double2 t = __ldg(s2 + k);
@@ -348,15 +410,10 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
                         gR = fma(A.d0[j], v[j], gR);
                     }
                 }
-                // own line
                 double v[8];
-                const unsigned char* xcb = X + cb * CELL_BYTES;
+                const uint32_t xcb = X + cb * CELL_BYTES;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    double2 t = *reinterpret_cast<const double2*>(xcb + swz(8 * (8 * L + 2 * k)));
-                    v[2 * k] = t.x;
-                    v[2 * k + 1] = t.y;
-                }
+                for (int k = 0; k < 4; ++k) lds2(xcb + swz(8 * (8 * L + 2 * k)), v[2 * k], v[2 * k + 1]);
                 double xe[4], xo[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
@@ -366,28 +423,24 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
                 ax8::line_eo(A, xe, xo, prevU[q], prevG[q], uR, gR, ye, yo);
                 prevU[q] = u1;
                 prevG[q] = g1;
-                const double S = A.w[L & 7] * A.w[L >> 3] * A.c[0];
-                // partial sums of passes 1, 2
-                const unsigned char* rb = bufR + cb * CELL_BYTES;
+                const uint32_t rb = bufR + cb * CELL_BYTES;
                 double o[8];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    double2 t = *reinterpret_cast<const double2*>(rb + swz(8 * (8 * L + 2 * k)));
-                    o[2 * k] = t.x;
-                    o[2 * k + 1] = t.y;
-                }
+                for (int k = 0; k < 4; ++k) lds2(rb + swz(8 * (8 * L + 2 * k)), o[2 * k], o[2 * k + 1]);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    o[i] = fma(S, ye[i] + yo[i], o[i]);
-                    o[7 - i] = fma(S, ye[i] - yo[i], o[7 - i]);
+                    o[i] = fma(S0[q], ye[i] + yo[i], o[i]);
+                    o[7 - i] = fma(S0[q], ye[i] - yo[i], o[7 - i]);
                 }
-                double2* dst = reinterpret_cast<double2*>(r + (cell_index(lp, 0, 0) + inplane) * 512 + 8 * L);
+                double2* dst = reinterpret_cast<double2*>(r + (cell_index(lp, 0, 0) + d0_inplane) * 512 + 8 * L);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) dst[k] = make_double2(o[2 * k], o[2 * k + 1]);
             }
         }
+        stamp(s, 6);
         __syncthreads();
-        if (tid == 0 && s + 2 < nsteps) issue(s + 2);
+        stamp(s, 7);
+        if (producer && s + 2 < nsteps) issue(s + 2);
     }
 }
 
