@@ -3,6 +3,7 @@
 #include "common.cuh"
 #include "kernel_axis8.cuh"
 #include "kernel_cell.cuh"
+#include "kernel_tile.cuh"
 #include "tables.h"
 
 #include <cudaTypedefs.h>
@@ -37,11 +38,12 @@ int fail(int code, const char* fmt, ...)
     } while (0)
 
 using LaunchFn = cudaError_t (*)(const void* tab, const dg::MeshArgs& M, const double* x, const double* xb,
-                                 const double* xa, double* r, long long c0, long long c1, cudaStream_t st);
+                                 const double* xa, double* r, long long c0, long long c1, cudaStream_t st,
+                                 const double* geo);
 
 template <int N, bool AFF, bool COEF>
 cudaError_t launch_cell(const void* tab, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                        double* r, long long c0, long long c1, cudaStream_t st)
+                        double* r, long long c0, long long c1, cudaStream_t st, const double*)
 {
     constexpr int CPB = dg::CellCfg<N>::CPB;
     const long long ncell = c1 - c0;
@@ -70,6 +72,74 @@ LaunchFn pick(int n, bool aff, bool coef)
     case 7: return pick_cell<7>(aff, coef);
     case 8: return pick_cell<8>(aff, coef);
     default: return nullptr;
+    }
+}
+
+// ---- marching-tile general kernel (k_tile): tile per degree
+template <int N> struct TileShape;
+template <> struct TileShape<2> { static constexpr int T1 = 4, T2 = 8, NT = 128; };
+template <> struct TileShape<3> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
+template <> struct TileShape<4> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
+template <> struct TileShape<5> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+template <> struct TileShape<6> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+template <> struct TileShape<7> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+template <> struct TileShape<8> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+
+struct TileInfo {
+    LaunchFn fn;
+    int T1, T2, smem;
+    cudaError_t (*attr)();
+};
+
+template <int N, bool AFF, bool COEF>
+cudaError_t launch_tile(const void* tab, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
+                        double* r, long long p0, long long p1, cudaStream_t st, const double* geo)
+{
+    constexpr int T1 = TileShape<N>::T1, T2 = TileShape<N>::T2, NT = TileShape<N>::NT;
+    using Y = dg::tl::Lay<N, T1, T2>;
+    if (p1 <= p0) return cudaSuccess;
+    const unsigned grid = (unsigned)((M.N1 / T1) * (M.N2 / T2));
+    dg::k_tile<N, AFF, COEF, T1, T2, NT><<<grid, NT, Y::BYTES, st>>>(
+        x, xb, xa, r, (int)p0, (int)p1, *static_cast<const dg::Tab<N>*>(tab), M, geo);
+    return cudaGetLastError();
+}
+
+template <int N, bool AFF, bool COEF>
+cudaError_t attr_tile()
+{
+    constexpr int T1 = TileShape<N>::T1, T2 = TileShape<N>::T2, NT = TileShape<N>::NT;
+    return cudaFuncSetAttribute(dg::k_tile<N, AFF, COEF, T1, T2, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dg::tl::Lay<N, T1, T2>::BYTES);
+}
+
+template <int N>
+TileInfo tile_info(bool aff, bool coef)
+{
+    constexpr int T1 = TileShape<N>::T1, T2 = TileShape<N>::T2;
+    TileInfo t;
+    t.T1 = T1;
+    t.T2 = T2;
+    t.smem = dg::tl::Lay<N, T1, T2>::BYTES;
+    if (aff) {
+        t.fn = coef ? launch_tile<N, true, true> : launch_tile<N, true, false>;
+        t.attr = coef ? attr_tile<N, true, true> : attr_tile<N, true, false>;
+    } else {
+        t.fn = coef ? launch_tile<N, false, true> : launch_tile<N, false, false>;
+        t.attr = coef ? attr_tile<N, false, true> : attr_tile<N, false, false>;
+    }
+    return t;
+}
+
+TileInfo pick_tile(int n, bool aff, bool coef)
+{
+    switch (n) {
+    case 2: return tile_info<2>(aff, coef);
+    case 3: return tile_info<3>(aff, coef);
+    case 4: return tile_info<4>(aff, coef);
+    case 5: return tile_info<5>(aff, coef);
+    case 6: return tile_info<6>(aff, coef);
+    case 7: return tile_info<7>(aff, coef);
+    default: return tile_info<8>(aff, coef);
     }
 }
 
@@ -159,12 +229,15 @@ struct dg_ctx {
     const char* kname;
     // axis-aligned n = 8 fast path (k_axis8)
     bool ax8;
+    bool tile;
+    TileInfo tinfo;
     int ax8_tile, ax8_T1, ax8_T2;
     dg::AxisTab8 atab;
     CUtensorMap tmap;
     const double* tmap_ptr;
     long long* dbg; // DG_TRACE: device buffer of per-phase clock64 stamps (k_axis8)
     double* d_jac;
+    double* d_geo; // k_tile geometry records (affine)
     // host-pipeline state (dg_apply_host)
     double* hx_d;
     double* hr_d;
@@ -200,8 +273,9 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
                                                                                           c->atab, c->M, c->dbg);
         return cudaGetLastError();
     }
+    if (c->tile) return c->tinfo.fn(c->tab, c->M, x, xb, xa, r, p0, p1, st, c->d_geo);
     const long long pc = c->M.plane_cells;
-    return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st);
+    return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
 }
 
 extern "C" {
@@ -280,6 +354,26 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     }
     c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
     c->kname = "k_cell_general";
+    // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
+    {
+        c->tinfo = pick_tile(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
+        const int64_t rowb = (int64_t)c->tinfo.T2 * n3 * 8;
+        const bool rows_aligned = (rowb % 16 == 0) && ((n3 * 8) % 16 == 0 || (mesh->N[2] % 2 == 0 && c->tinfo.T2 % 2 == 0));
+        c->tile = mesh->N[1] % c->tinfo.T1 == 0 && mesh->N[2] % c->tinfo.T2 == 0 && rows_aligned &&
+                  getenv("DG_FORCE_GENERAL") == nullptr && c->tinfo.attr() == cudaSuccess;
+        if (c->tile && mesh->geom_kind == DG_GEOM_AFFINE) {
+            // per-cell geometry records for the tile kernel (k_geom, once)
+            const long long nc = (long long)M.plane_cells * (M.L + 2);
+            cudaError_t e = cudaMalloc(&c->d_geo, sizeof(double) * dg::GREC * (size_t)nc);
+            if (e != cudaSuccess) {
+                c->tile = false;
+            } else {
+                dg::k_geom<<<(unsigned)((nc + 255) / 256), 256>>>(c->d_jac, c->d_geo, nc, M.plane_cells, M.N1, M.N2, M.L + 2);
+                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_geo); c->d_geo = nullptr; c->tile = false; }
+            }
+        }
+        if (c->tile) c->kname = "k_tile";
+    }
     // axis-aligned Q7 fast path: tile T1 x T2 (env DG_AX8_TILE = 2x4 | 4x4 | 4x2 for experiments)
     {
         const char* tv = getenv("DG_AX8_TILE");
@@ -321,6 +415,7 @@ int dg_destroy(dg_ctx* c)
     if (!c) return DG_OK;
     cudaSetDevice(c->device);
     if (c->d_jac) cudaFree(c->d_jac);
+    if (c->d_geo) cudaFree(c->d_geo);
     if (c->dbg) {
         // DG_TRACE: dump the stamps of the last launch
         static long long h[1024 * 16 * 8];
@@ -390,6 +485,7 @@ int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* 
     if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 7)
         return fail(DG_ERR_INVALID, "dg_apply: pointers must be 8-byte aligned");
     if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned");
+    if (((uintptr_t)x & 15) && c->tile) return fail(DG_ERR_INVALID, "dg_apply: x must be 16-byte aligned");
     cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
     return DG_OK;
