@@ -79,9 +79,9 @@ LaunchFn pick(int n, bool aff, bool coef)
 template <int N> struct TileShape;
 template <> struct TileShape<2> { static constexpr int T1 = 4, T2 = 8, NT = 128; };
 template <> struct TileShape<3> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
-template <> struct TileShape<4> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
-template <> struct TileShape<5> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
-template <> struct TileShape<6> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+template <> struct TileShape<4> { static constexpr int T1 = 2, T2 = 4, NT = 256; };
+template <> struct TileShape<5> { static constexpr int T1 = 2, T2 = 2, NT = 256; };
+template <> struct TileShape<6> { static constexpr int T1 = 2, T2 = 2, NT = 256; };
 template <> struct TileShape<7> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
 template <> struct TileShape<8> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
 
@@ -231,7 +231,7 @@ struct dg_ctx {
     bool ax8;
     bool tile;
     TileInfo tinfo;
-    int ax8_tile, ax8_T1, ax8_T2;
+    int ax8_tile, ax8_T1, ax8_T2, ax8_chunk;
     dg::AxisTab8 atab;
     CUtensorMap tmap;
     const double* tmap_ptr;
@@ -261,15 +261,21 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
             if (rc != CUDA_SUCCESS) return cudaErrorInvalidValue;
             c->tmap_ptr = x;
         }
-        const unsigned grid = (unsigned)((c->M.N1 / c->ax8_T1) * (c->M.N2 / c->ax8_T2));
+        const int ntiles = (c->M.N1 / c->ax8_T1) * (c->M.N2 / c->ax8_T2);
+        const int np = p1 - p0;
+        const int CL = c->ax8_chunk > 0 ? (c->ax8_chunk < np ? c->ax8_chunk : np) : np;
+        const unsigned grid = (unsigned)(ntiles * ((np + CL - 1) / CL));
         if (c->ax8_tile == 0)
-            dg::k_axis8<2, 4, 256><<<grid, 256, dg::ax8::Cfg<2, 4, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1,
+            dg::k_axis8<2, 4, 256><<<grid, 256, dg::ax8::Cfg<2, 4, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
                                                                                           c->atab, c->M, c->dbg);
         else if (c->ax8_tile == 1)
-            dg::k_axis8<4, 4, 512><<<grid, 512, dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1,
+            dg::k_axis8<4, 4, 512><<<grid, 512, dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
+                                                                                          c->atab, c->M, c->dbg);
+        else if (c->ax8_tile == 2)
+            dg::k_axis8<4, 2, 256><<<grid, 256, dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
                                                                                           c->atab, c->M, c->dbg);
         else
-            dg::k_axis8<4, 2, 256><<<grid, 256, dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1,
+            dg::k_axis8<2, 2, 256><<<grid, 256, dg::ax8::Cfg<2, 2, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
                                                                                           c->atab, c->M, c->dbg);
         return cudaGetLastError();
     }
@@ -380,10 +386,13 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         c->ax8_tile = 0;
         if (tv && !strcmp(tv, "4x4")) c->ax8_tile = 1;
         if (tv && !strcmp(tv, "4x2")) c->ax8_tile = 2;
+        if (tv && !strcmp(tv, "2x2")) c->ax8_tile = 3;
         const int T1 = (c->ax8_tile == 1 || c->ax8_tile == 2) ? 4 : 2;
-        const int T2 = (c->ax8_tile == 2) ? 2 : 4;
+        const int T2 = (c->ax8_tile == 2 || c->ax8_tile == 3) ? 2 : 4;
         c->ax8_T1 = T1;
         c->ax8_T2 = T2;
+        const char* cl = getenv("DG_AX8_CHUNK");
+        c->ax8_chunk = cl ? atoi(cl) : 12; // planes per work item (0: whole slab)
         c->ax8 = (n == 8 && mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE &&
                   mesh->N[1] % T1 == 0 && mesh->N[2] % T2 == 0 && getenv("DG_FORCE_GENERAL") == nullptr);
     }
@@ -396,9 +405,12 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         else if (c->ax8_tile == 1)
             e = cudaFuncSetAttribute(dg::k_axis8<4, 4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES);
-        else
+        else if (c->ax8_tile == 2)
             e = cudaFuncSetAttribute(dg::k_axis8<4, 2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES);
+        else
+            e = cudaFuncSetAttribute(dg::k_axis8<2, 2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     dg::ax8::Cfg<2, 2, 256>::SMEM_BYTES);
         if (e != cudaSuccess || !get_encode()) c->ax8 = false;
         else c->kname = "k_axis8";
         if (c->ax8 && getenv("DG_TRACE")) {

@@ -57,8 +57,10 @@ struct Cfg {
     static constexpr int BUF_BYTES = CELLS * CELL_BYTES;
     static constexpr int SMEM_BYTES = 3 * BUF_BYTES + 1024; // X0, X1, R (+ barriers, alignment slack)
     static constexpr int WARPS = NT / 32;
-    static_assert(WARPS == CELLS, "pass d=0 maps one warp per cell");
-    static constexpr int MINB = (SMEM_BYTES <= 113 * 1024) ? 2 : 1;
+    static constexpr int LPT = 64 * CELLS / NT; // pass d=0: lines per thread (1 or 2)
+    static constexpr int WPC = 2 / LPT;         // pass d=0: warps per cell
+    static_assert(LPT * NT == 64 * CELLS && (LPT == 1 || LPT == 2), "pass d=0 mapping");
+    static constexpr int MINB = (SMEM_BYTES <= 56 * 1024) ? 4 : (SMEM_BYTES <= 113 * 1024) ? 2 : 1;
 };
 
 __device__ __forceinline__ uint32_t swz(uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
@@ -266,8 +268,8 @@ __device__ __forceinline__ double inplane_scale(const AxisTab8& A, int tid)
 template <int T1, int T2, int NT>
 __global__ void __launch_bounds__(NT, ax8::Cfg<T1, T2, NT>::MINB)
 k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, const double* __restrict__ xb,
-        const double* __restrict__ xa, double* __restrict__ r, int p_begin, int p_end, const AxisTab8 A,
-        const MeshArgs M, long long* __restrict__ dbg)
+        const double* __restrict__ xa, double* __restrict__ r, int p_begin, int p_end, int chunk_len,
+        const AxisTab8 A, const MeshArgs M, long long* __restrict__ dbg)
 {
     using namespace ax8;
     using C = Cfg<T1, T2, NT>;
@@ -281,7 +283,16 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ntile2 = M.N2 / T2;
-    const int ti1 = blockIdx.x / ntile2, ti2 = blockIdx.x % ntile2;
+    const int ntiles = (M.N1 / T1) * ntile2;
+    // work item = (plane chunk, tile), chunk-major: concurrently resident CTAs march the same
+    // planes, so their ring cells (each other's own cells) are L2 hits
+    const int chunk = blockIdx.x / ntiles, tile = blockIdx.x % ntiles;
+    const int ti1 = tile / ntile2, ti2 = tile % ntile2;
+    {
+        const int b = p_begin + chunk * chunk_len;
+        p_end = min(p_end, b + chunk_len);
+        p_begin = b;
+    }
     const int PC = M.plane_cells;
     const int nsteps = p_end - p_begin;
     if (nsteps <= 0) return;
@@ -316,13 +327,16 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
 
     const double S1 = inplane_scale<1, T1, T2, NT>(A, tid);
     const double S2 = inplane_scale<2, T2, T1, NT>(A, tid);
-    // d=0 mapping: warp w owns cell w (buffer order c1*T2+c2); lanes own lines L = lane, lane + 32
-    const int dc1 = warp / T2, dc2 = warp % T2;
+    // d=0 mapping: warp w owns (part of) cell w / WPC (buffer order c1*T2+c2); lane owns lines
+    // L = lane + 32 (q + LPT (w % WPC)), q < LPT
+    constexpr int LPT = C::LPT, WPC = C::WPC;
+    const int dcell = warp / WPC, lbase = 32 * LPT * (warp % WPC);
+    const int dc1 = dcell / T2, dc2 = dcell % T2;
     const long long d0_inplane = (long long)(ti1 * T1 + dc1) * M.N2 + ti2 * T2 + dc2;
-    double S0[2];
+    double S0[LPT];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int L = lane + 32 * q;
+    for (int q = 0; q < LPT; ++q) {
+        const int L = lane + 32 * q + lbase;
         double wa = 0.0, wb = 0.0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -332,12 +346,12 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
         S0[q] = wa * wb * A.c[0];
     }
 
-    double prevU[2], prevG[2]; // traces e1.x, d1.x of the lower x0-neighbour, per d=0 line
+    double prevU[LPT], prevG[LPT]; // traces e1.x, d1.x of the lower x0-neighbour, per d=0 line
     {
         const double* src = (p_begin == 0) ? xb + d0_inplane * 512 : x + (cell_index(p_begin - 1, 0, 0) + d0_inplane) * 512;
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int L = lane + 32 * q;
+        for (int q = 0; q < LPT; ++q) {
+            const int L = lane + 32 * q + lbase;
             const double2* s2 = reinterpret_cast<const double2*>(src + 8 * L);
             double v[8];
 #pragma unroll
@@ -359,7 +373,11 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
     // optional phase timestamps (DG_TRACE): dbg[block][step][phase], first 16 steps
     const bool trace = dbg != nullptr && tid == 0 && blockIdx.x < 1024;
     auto stamp = [&](int s, int ph) {
+#ifdef DG_AX8_TRACE
         if (trace && s < 16) dbg[(blockIdx.x * 16 + s) * 8 + ph] = clock64();
+#else
+        (void)s; (void)ph; (void)trace;
+#endif
     };
     for (int s = 0; s < nsteps; ++s) {
         const int lp = p_begin + s;
@@ -382,11 +400,11 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
             const bool last = (s == nsteps - 1);
             if (!last) mbar_wait(bar((s + 1) & 1), ((s + 1) >> 1) & 1);
             const uint32_t XN = bufX[(s + 1) & 1];
-            const int cb = warp;
+            const int cb = dcell;
             const double* nsrc = (p_end == M.L) ? xa + d0_inplane * 512 : x + (cell_index(p_end, 0, 0) + d0_inplane) * 512;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int L = lane + 32 * q;
+            for (int q = 0; q < LPT; ++q) {
+                const int L = lane + 32 * q + lbase;
                 // upper neighbour's traces e0.x, d0.x
                 double uR = 0.0, gR = 0.0;
                 {
