@@ -77,13 +77,14 @@ LaunchFn pick(int n, bool aff, bool coef)
 
 // ---- marching-tile general kernel (k_tile): tile per degree
 template <int N> struct TileShape;
+// NT = T1 T2 N^2 rounded up to a warp multiple (one thread per cell line position)
 template <> struct TileShape<2> { static constexpr int T1 = 4, T2 = 8, NT = 128; };
-template <> struct TileShape<3> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
-template <> struct TileShape<4> { static constexpr int T1 = 2, T2 = 4, NT = 256; };
-template <> struct TileShape<5> { static constexpr int T1 = 2, T2 = 2, NT = 256; };
-template <> struct TileShape<6> { static constexpr int T1 = 2, T2 = 2, NT = 256; };
-template <> struct TileShape<7> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
-template <> struct TileShape<8> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+template <> struct TileShape<3> { static constexpr int T1 = 2, T2 = 4, NT = 96; };
+template <> struct TileShape<4> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
+template <> struct TileShape<5> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
+template <> struct TileShape<6> { static constexpr int T1 = 2, T2 = 2, NT = 160; };
+template <> struct TileShape<7> { static constexpr int T1 = 2, T2 = 2, NT = 224; };
+template <> struct TileShape<8> { static constexpr int T1 = 2, T2 = 2, NT = 256; };
 
 struct TileInfo {
     LaunchFn fn;

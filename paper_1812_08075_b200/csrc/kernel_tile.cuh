@@ -113,8 +113,9 @@ __device__ __forceinline__ void cmul(double ar, double ai, double br, double bi,
 template <int N, int T1, int T2>
 struct Lay {
     static constexpr int N2 = N * N, N3 = N * N * N, NC = T1 * T2;
+    static constexpr int NACT = NC * N2;     // threads with a fixed (cell, a, b)
     static constexpr int NR = 2 * (T1 + T2); // ring cells: d=1 low[T2] high[T2], d=2 low[T1] high[T1]
-    // trace / coefficient slots (each N2 points, 5 quantity arrays):
+    // face slots (N2 points each, 4 quantity arrays):
     //   own cells: slot c*6 + 2*d + side   (side 0: lower face, 1: upper face)
     //   ring:      slot 6 NC + r           (the ring cell's side facing the tile)
     //   next:      slot 6 NC + NR + c      (the lower face of the next-plane cell above c)
@@ -122,12 +123,10 @@ struct Lay {
     static constexpr int QSZ = NS * N2;
     static constexpr int CXSZ = 2 * 3 * (N + 1) * 2; // c(x) tables per cell: [coord k][axis b][q = 0..N] complex
     // offsets in doubles
-    static constexpr int XB0 = 0;
-    static constexpr int XB1 = XB0 + NC * N3;
-    static constexpr int G = XB1 + NC * N3;            // 3 arrays: grad_hat U -> flux Q
-    static constexpr int RR = G + 3 * NC * N3;         // partial residual (passes d = 1, 2)
-    static constexpr int TQ = RR + NC * N3;            // 5 arrays: u|Cv, gn|G, gt1|Ct1, gt2|Ct2, V
-    static constexpr int PEND = TQ + 5 * QSZ;          // 2 (ping-pong) x {V+, G+} x [NC][N2]
+    static constexpr int XB = 0;                       // current plane (TMA)
+    static constexpr int G = XB + NC * N3;             // 3 arrays: grad_hat U -> flux Q -> partial residuals
+    static constexpr int TQ = G + 3 * NC * N3;         // 4 arrays: u|Cv|V, gn|G, gt1|Ct1, gt2|Ct2
+    static constexpr int PEND = TQ + 4 * QSZ;          // 2 (ping-pong) x {V+, G+} x [NC][N2]
     static constexpr int GEO = PEND + 2 * 2 * NC * N2; // geometry records of own [NC] and ring [NR] cells
     static constexpr int CX = GEO + (NC + NR) * GREC;
     static constexpr int CO = CX + (NC + NR) * CXSZ;  // origin phases e^{2 pi i o_k}, k = 0, 1
@@ -137,6 +136,9 @@ struct Lay {
 
 } // namespace tl
 
+// Thread mapping: thread t < NC N2 owns cell c = t / N2 of the tile and the position (a, b) = (t % N, t / N % N)
+// of the cell's lines in every direction and of every face of the cell; all per-thread loops below run
+// over compile-time directions / quadrature indices (no per-task index arithmetic).
 template <int N, bool AFFINE, bool COEFF, int T1, int T2, int NT>
 __global__ void __launch_bounds__(NT)
 k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa,
@@ -145,11 +147,10 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
     using Y = tl::Lay<N, T1, T2>;
     constexpr int N2 = Y::N2, N3 = Y::N3, NC = Y::NC, NR = Y::NR, QSZ = Y::QSZ;
     constexpr int SNEXT = 6 * NC + NR; // first "next" slot
+    static_assert(Y::NACT <= NT, "one thread per (cell, line position)");
     extern __shared__ __align__(16) double sm[];
-    double* const XB0 = sm + Y::XB0;
-    double* const XB1 = sm + Y::XB1;
+    double* const XB = sm + Y::XB;
     double* const G = sm + Y::G;
-    double* const RR = sm + Y::RR;
     double* const TQ = sm + Y::TQ;
     double* const GEO = sm + Y::GEO;
     double* const CX = sm + Y::CX;
@@ -168,27 +169,28 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
     auto wrap = [](int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); };
     auto Q = [&](int q, int slot) { return TQ + q * QSZ + slot * N2; };
 
+    // fixed thread coordinates
+    const bool act = tid < Y::NACT;
+    const int mc = act ? tid / N2 : 0, mab = act ? tid % N2 : 0, ma = mab % N, mb = mab / N;
+    const int mc1 = mc / T2, mc2 = mc % T2;
+    const long long minpl = (long long)(ti1 * T1 + mc1) * M.N2 + ti2 * T2 + mc2; // in-plane index of cell mc
+
     for (int i = tid; i < N * N; i += NT) sD[i] = T.D[i];
     for (int i = tid; i < N; i += NT) { sW[i] = T.w[i]; sXi[i] = T.xi[i]; }
     if (tid == 0) {
         sXi[N] = 1.0;
         tl::mbar_init(&bar[0], 1);
-        tl::mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     auto issue = [&](int step) {
         const int lp = p_begin + step;
-        uint64_t* b = &bar[step & 1];
-        tl::mbar_expect_tx(b, NC * N3 * 8);
+        tl::mbar_expect_tx(&bar[0], NC * N3 * 8);
 #pragma unroll
         for (int c1 = 0; c1 < T1; ++c1)
-            tl::bulk_g2s(((step & 1) ? XB1 : XB0) + c1 * T2 * N3, x + cidx(lp, ti1 * T1 + c1, ti2 * T2) * N3, T2 * N3 * 8, b);
+            tl::bulk_g2s(XB + c1 * T2 * N3, x + cidx(lp, ti1 * T1 + c1, ti2 * T2) * N3, T2 * N3 * 8, &bar[0]);
     };
-    if (tid == 0) {
-        issue(0);
-        if (nsteps > 1) issue(1);
-    }
+    if (tid == 0) issue(0);
 
     // ring cell rr -> in-plane (i1, i2), the face direction it borders, and whether it is below the tile
     auto ring_cell = [&](int rr, int& i1, int& i2, int& d, bool& low) {
@@ -224,7 +226,6 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
         }
         return 1.0 + 0.5 * z[0][1] * z[1][0]; // 1 + 0.5 sin(2 pi x0) cos(2 pi x1)  (reading R13)
     };
-    // fill the c(x) tables of cell slot cc (origin plane index g0, row i1) — one task per entry
     constexpr int NE = 2 * 3 * (N + 1);
     auto ctab_task = [&](int cc, int rem, int g0, int i1) {
         double sv, cv;
@@ -243,6 +244,111 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
             CO[cc * 4 + 2 * k + 1] = sv;
         }
     };
+    // tangential derivatives (D on the face) of the u-trace of slot `slot` at point (a, b)
+    auto tangential = [&](int slot, int a, int b) {
+        const double* U = Q(0, slot);
+        double v1 = 0.0, v2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            v1 = fma(sD[a * N + j], U[j + N * b], v1);
+            v2 = fma(sD[b * N + j], U[a + N * j], v2);
+        }
+        Q(2, slot)[a + N * b] = v1;
+        Q(3, slot)[a + N * b] = v2;
+    };
+    // same with the thread's D rows in registers (Da = D[a][.], Db = D[b][.])
+    auto tangential_r = [&](int slot, int a, int b, const double* Da, const double* Db) {
+        const double* U = Q(0, slot);
+        double v1 = 0.0, v2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            v1 = fma(Da[j], U[j + N * b], v1);
+            v2 = fma(Db[j], U[a + N * j], v2);
+        }
+        Q(2, slot)[a + N * b] = v1;
+        Q(3, slot)[a + N * b] = v2;
+    };
+    // V with the thread's D columns in registers (Ca = D[.][a], Cb = D[.][b])
+    auto vface_r = [&](int slot, int a, int b, const double* Ca, const double* Cb) -> double {
+        double v = Q(0, slot)[a + N * b];
+        if (AFFINE) {
+            const double* C1 = Q(2, slot);
+            const double* C2 = Q(3, slot);
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                v = fma(Ca[j], C1[j + N * b], v);
+                v = fma(Cb[j], C2[a + N * j], v);
+            }
+        }
+        return v;
+    };
+    // V = Cv + D^T_t1 Ct1 + D^T_t2 Ct2 at point (a, b) of a slot
+    auto vface = [&](int slot, int a, int b) -> double {
+        double v = Q(0, slot)[a + N * b];
+        if (AFFINE) {
+            const double* C1 = Q(2, slot);
+            const double* C2 = Q(3, slot);
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                v = fma(sD[j * N + a], C1[j + N * b], v);
+                v = fma(sD[j * N + b], C2[a + N * j], v);
+            }
+        }
+        return v;
+    };
+    // SIPG flux at point (a, b) of the face with normal d between slots sMinus (T-) and sPlus (T+);
+    // geometry / c tables from cell-record slot gs (= T-). Writes the coefficients (Cv, G, Ct1, Ct2)
+    // of the requested sides into their own slots (read-before-write of the same point only).
+    auto face = [&](int d, int a, int b, int sMinus, int sPlus, int gs, bool wMinus, bool wPlus) {
+        const int ab = a + N * b;
+        const double jump = Q(0, sMinus)[ab] - Q(0, sPlus)[ab];
+        const double gmd = Q(1, sMinus)[ab], gpd = Q(1, sPlus)[ab];
+        double cF = 1.0;
+        if (COEFF) {
+            const int q0 = (d == 0) ? N : a, q1 = (d == 1) ? N : (d == 0 ? a : b), q2 = (d == 2) ? N : b;
+            cF = cval(gs, q0, q1, q2); // x_F on the T- cell at xi_d = 1
+        }
+        const double gam = d == 0 ? M.gamma[0] : (d == 1 ? M.gamma[1] : M.gamma[2]);
+        double Cvm, Cvp, Cg, am_d, am_t1, am_t2, ap_d, ap_t1, ap_t2;
+        if (!AFFINE) {
+            const double hd = d == 0 ? M.h[0] : (d == 1 ? M.h[1] : M.h[2]);
+            const double W = sW[a] * sW[b] * (M.h[0] * M.h[1] * M.h[2] / hd);
+            const double avg = 0.5 * cF * (gmd + gpd) / hd;
+            Cvm = W * (-avg + gam * jump);
+            Cvp = W * (avg - gam * jump);
+            Cg = -0.5 * W * jump * cF;
+            am_d = ap_d = 1.0 / hd;
+            am_t1 = am_t2 = ap_t1 = ap_t2 = 0.0;
+        } else {
+            const double* f = GEO + gs * GREC + 12 + 7 * d;
+            // components (d, t1, t2) of a- = f[1..3], a+ = f[4..6]
+            am_d = d == 0 ? f[1] : (d == 1 ? f[2] : f[3]);
+            am_t1 = d == 0 ? f[2] : f[1];
+            am_t2 = d == 2 ? f[2] : f[3];
+            ap_d = d == 0 ? f[4] : (d == 1 ? f[5] : f[6]);
+            ap_t1 = d == 0 ? f[5] : f[4];
+            ap_t2 = d == 2 ? f[5] : f[6];
+            const double gm = cF * (am_d * gmd + am_t1 * Q(2, sMinus)[ab] + am_t2 * Q(3, sMinus)[ab]);
+            const double gp = cF * (ap_d * gpd + ap_t1 * Q(2, sPlus)[ab] + ap_t2 * Q(3, sPlus)[ab]);
+            const double avg = 0.5 * (gm + gp);
+            const double W = sW[a] * sW[b] * f[0];
+            Cvm = W * (-avg + gam * jump);
+            Cvp = W * (avg - gam * jump);
+            Cg = -0.5 * W * jump * cF;
+        }
+        if (wMinus) {
+            Q(0, sMinus)[ab] = Cvm;
+            Q(1, sMinus)[ab] = am_d * Cg;
+            Q(2, sMinus)[ab] = am_t1 * Cg;
+            Q(3, sMinus)[ab] = am_t2 * Cg;
+        }
+        if (wPlus) {
+            Q(0, sPlus)[ab] = Cvp;
+            Q(1, sPlus)[ab] = ap_d * Cg;
+            Q(2, sPlus)[ab] = ap_t1 * Cg;
+            Q(3, sPlus)[ab] = ap_t2 * Cg;
+        }
+    };
 
     // ---------------- prologue: the lower d=0 face of plane p_begin (T- = plane p_begin - 1) ----------------
     // Evaluated once here; its T+ half (V+, G+) is left in PEND[0] exactly as a regular step leaves it.
@@ -252,22 +358,22 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
     {
         const int lpm = p_begin - 1;
         const int g0m = wrap(M.plane_begin + lpm, M.N0);
-        for (int t = tid; t < 2 * NC * N2; t += NT) {
-            const int which = t / (NC * N2), rem = t % (NC * N2), c = rem / N2, ab = rem % N2, a = ab % N, b = ab / N;
-            const int c1 = c / T2, c2 = c % T2;
-            const long long inpl = (long long)(ti1 * T1 + c1) * M.N2 + ti2 * T2 + c2;
-            const double* src = which ? x + (cidx(p_begin, 0, 0) + inpl) * N3
-                                      : ((p_begin == 0) ? xb + inpl * N3 : x + (cidx(lpm, 0, 0) + inpl) * N3);
-            double u = 0.0, g = 0.0;
+        if (act) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const double v = __ldg(src + pidx<N>(0, j, a, b));
-                u = fma(which ? T.e0[j] : T.e1[j], v, u);
-                g = fma(which ? T.d0[j] : T.d1[j], v, g);
+            for (int which = 0; which < 2; ++which) {
+                const double* src = which ? x + (cidx(p_begin, 0, 0) + minpl) * N3
+                                          : ((p_begin == 0) ? xb + minpl * N3 : x + (cidx(lpm, 0, 0) + minpl) * N3);
+                double u = 0.0, g = 0.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const double v = __ldg(src + pidx<N>(0, j, ma, mb));
+                    u = fma(which ? T.e0[j] : T.e1[j], v, u);
+                    g = fma(which ? T.d0[j] : T.d1[j], v, g);
+                }
+                const int slot = which ? mc * 6 + 0 : SNEXT + mc;
+                Q(0, slot)[mab] = u;
+                Q(1, slot)[mab] = g;
             }
-            const int slot = which ? c * 6 + 0 : SNEXT + c;
-            Q(0, slot)[ab] = u;
-            Q(1, slot)[ab] = g;
         }
         if (AFFINE) {
             for (int t = tid; t < NC * GREC; t += NT) {
@@ -278,69 +384,20 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
         __syncthreads();
         if (COEFF)
             for (int t = tid; t < NC * (NE + 2); t += NT) ctab_task(t / (NE + 2), t % (NE + 2), g0m, ti1 * T1 + (t / (NE + 2)) / T2);
-        if (AFFINE) {
-            for (int t = tid; t < 2 * NC * N2; t += NT) {
-                const int which = t / (NC * N2), rem = t % (NC * N2), c = rem / N2, ab = rem % N2, a = ab % N, b = ab / N;
-                const int slot = which ? c * 6 + 0 : SNEXT + c;
-                const double* U = Q(0, slot);
-                double v1 = 0.0, v2 = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    v1 = fma(sD[a * N + j], U[j + N * b], v1);
-                    v2 = fma(sD[b * N + j], U[a + N * j], v2);
-                }
-                Q(2, slot)[ab] = v1;
-                Q(3, slot)[ab] = v2;
-            }
+        if (AFFINE && act) {
+            tangential(mc * 6 + 0, ma, mb);
+            tangential(SNEXT + mc, ma, mb);
         }
         __syncthreads();
-        for (int t = tid; t < NC * N2; t += NT) {
-            const int c = t / N2, ab = t % N2, a = ab % N, b = ab / N;
-            const int sM = SNEXT + c, sP = c * 6 + 0;
-            const double jump = Q(0, sM)[ab] - Q(0, sP)[ab];
-            const double gmd = Q(1, sM)[ab], gpd = Q(1, sP)[ab];
-            const double cF = COEFF ? cval(c, N, a, b) : 1.0;
-            double Cv, Gp, C1 = 0.0, C2 = 0.0;
-            if (!AFFINE) {
-                const double hd = M.h[0];
-                const double W = sW[a] * sW[b] * (M.h[0] * M.h[1] * M.h[2] / hd);
-                const double avg = 0.5 * cF * (gmd + gpd) / hd;
-                Cv = W * (avg - M.gamma[0] * jump);
-                Gp = -0.5 * W * jump * cF / hd;
-            } else {
-                const double* f = GEO + c * GREC + 12; // the cell below: its upper face d = 0
-                const double gm = cF * (f[1] * gmd + f[2] * Q(2, sM)[ab] + f[3] * Q(3, sM)[ab]);
-                const double gp = cF * (f[4] * gpd + f[5] * Q(2, sP)[ab] + f[6] * Q(3, sP)[ab]);
-                const double W = sW[a] * sW[b] * f[0];
-                Cv = W * (0.5 * (gm + gp) - M.gamma[0] * jump);
-                const double Cg = -0.5 * W * jump * cF;
-                Gp = f[4] * Cg;
-                C1 = f[5] * Cg;
-                C2 = f[6] * Cg;
-            }
-            // Cv, C1, C2 into the (T-, unused now) next slot arrays; G+ into quantity 1 of the same slot
-            Q(0, sM)[ab] = Cv;
-            Q(4, sM)[ab] = Gp;
-            Q(2, sP)[ab] = C1; // own lower slot's tangential arrays are free: reuse for Ct
-            Q(3, sP)[ab] = C2;
+        if (act) {
+            // face below cell mc; T- = cell below (record / c tables in own slot mc), T+ = mc
+            face(0, ma, mb, SNEXT + mc, mc * 6 + 0, mc, false, true);
         }
         __syncthreads();
         double* P = sm + Y::PEND;
-        for (int t = tid; t < NC * N2; t += NT) {
-            const int c = t / N2, ab = t % N2, a = ab % N, b = ab / N;
-            const int sM = SNEXT + c, sP = c * 6 + 0;
-            double v = Q(0, sM)[ab];
-            if (AFFINE) {
-                const double* C1 = Q(2, sP);
-                const double* C2 = Q(3, sP);
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    v = fma(sD[j * N + a], C1[j + N * b], v);
-                    v = fma(sD[j * N + b], C2[a + N * j], v);
-                }
-            }
-            P[c * N2 + ab] = v;
-            P[NC * N2 + c * N2 + ab] = Q(4, sM)[ab];
+        if (act) {
+            P[mc * N2 + mab] = vface(mc * 6 + 0, ma, mb);
+            P[NC * N2 + mc * N2 + mab] = Q(1, mc * 6 + 0)[mab];
         }
         __syncthreads();
     }
@@ -349,8 +406,6 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
         const int lp = p_begin + s;
         const int ig0 = wrap(M.plane_begin + lp, M.N0);
         const bool lastp = (s == nsteps - 1);
-        double* X = (s & 1) ? XB1 : XB0;
-        double* XN = (s & 1) ? XB0 : XB1;
         const double* Pin = sm + Y::PEND + pend * 2 * NC * N2;  // lower d=0 face of this plane (from last step)
         double* Pout = sm + Y::PEND + (pend ^ 1) * 2 * NC * N2; // lower d=0 face of the next plane
 
@@ -374,19 +429,18 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
                 ctab_task(cc, t % (NE + 2), ig0, i1);
             }
         }
-        tl::mbar_wait(&bar[s & 1], (s >> 1) & 1);
-        if (!lastp) tl::mbar_wait(&bar[(s + 1) & 1], ((s + 1) >> 1) & 1);
+        tl::mbar_wait(&bar[0], s & 1);
         __syncthreads();
 
-        // ---------------- P1: stage 1 + own traces; ring traces; next-plane traces ----------------
-        for (int t = tid; t < 3 * NC * N2 + NR * N2 + NC * N2; t += NT) {
-            if (t < 3 * NC * N2) {
-                const int d = t / (NC * N2), rem = t % (NC * N2), c = rem / N2, ab = rem % N2, a = ab % N, b = ab / N;
-                const double* xc = X + c * N3;
+        // ---------------- P1: stage 1 + own traces (fixed mapping); next-plane traces; ring traces ----------------
+        if (act) {
+            const double* xc = XB + mc * N3;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
                 double v[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) v[j] = xc[pidx<N>(d, j, a, b)];
-                double* gd = G + (d * NC + c) * N3;
+                for (int j = 0; j < N; ++j) v[j] = xc[pidx<N>(d, j, ma, mb)];
+                double* gd = G + (d * NC + mc) * N3;
                 double u0 = 0, u1 = 0, g0 = 0, g1 = 0;
 #pragma unroll
                 for (int j = 0; j < N; ++j) {
@@ -400,255 +454,173 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
                     double acc = 0.0;
 #pragma unroll
                     for (int j = 0; j < N; ++j) acc = fma(T.D[q * N + j], v[j], acc);
-                    gd[pidx<N>(d, q, a, b)] = acc;
+                    gd[pidx<N>(d, q, ma, mb)] = acc;
                 }
-                Q(0, c * 6 + 2 * d + 0)[ab] = u0;
-                Q(0, c * 6 + 2 * d + 1)[ab] = u1;
-                Q(1, c * 6 + 2 * d + 0)[ab] = g0;
-                Q(1, c * 6 + 2 * d + 1)[ab] = g1;
-            } else if (t < 3 * NC * N2 + NR * N2) {
-                const int tt = t - 3 * NC * N2, rr = tt / N2, ab = tt % N2, a = ab % N, b = ab / N;
-                int i1, i2, d;
-                bool low;
-                ring_cell(rr, i1, i2, d, low);
-                const double* src = x + cidx(lp, i1, i2) * N3;
-                double u = 0, g = 0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    const double v = __ldg(src + pidx<N>(d, j, a, b));
-                    u = fma(low ? T.e1[j] : T.e0[j], v, u); // a ring cell below the tile faces it with its upper end
-                    g = fma(low ? T.d1[j] : T.d0[j], v, g);
-                }
-                Q(0, 6 * NC + rr)[ab] = u;
-                Q(1, 6 * NC + rr)[ab] = g;
-            } else {
-                const int tt = t - 3 * NC * N2 - NR * N2, c = tt / N2, ab = tt % N2, a = ab % N, b = ab / N;
-                double u = 0, g = 0;
-                if (!lastp) {
-                    const double* src = XN + c * N3;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        const double v = src[pidx<N>(0, j, a, b)];
-                        u = fma(T.e0[j], v, u);
-                        g = fma(T.d0[j], v, g);
-                    }
-                } else {
-                    const int c1 = c / T2, c2 = c % T2;
-                    const long long inpl = (long long)(ti1 * T1 + c1) * M.N2 + ti2 * T2 + c2;
-                    const double* src = (p_end == M.L) ? xa + inpl * N3 : x + (cidx(p_end, 0, 0) + inpl) * N3;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        const double v = __ldg(src + pidx<N>(0, j, a, b));
-                        u = fma(T.e0[j], v, u);
-                        g = fma(T.d0[j], v, g);
-                    }
-                }
-                Q(0, SNEXT + c)[ab] = u;
-                Q(1, SNEXT + c)[ab] = g;
+                Q(0, mc * 6 + 2 * d + 0)[mab] = u0;
+                Q(0, mc * 6 + 2 * d + 1)[mab] = u1;
+                Q(1, mc * 6 + 2 * d + 0)[mab] = g0;
+                Q(1, mc * 6 + 2 * d + 1)[mab] = g1;
             }
+            // the lower end of the line above (next plane; halo x_above at the slab's last plane)
+            const double* src = !lastp ? x + (cidx(lp + 1, 0, 0) + minpl) * N3
+                                       : ((p_end == M.L) ? xa + minpl * N3 : x + (cidx(p_end, 0, 0) + minpl) * N3);
+            double u = 0, g = 0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double v = __ldg(src + pidx<N>(0, j, ma, mb));
+                u = fma(T.e0[j], v, u);
+                g = fma(T.d0[j], v, g);
+            }
+            Q(0, SNEXT + mc)[mab] = u;
+            Q(1, SNEXT + mc)[mab] = g;
+        }
+        for (int t = tid; t < NR * N2; t += NT) {
+            const int rr = t / N2, ab = t % N2, a = ab % N, b = ab / N;
+            int i1, i2, d;
+            bool low;
+            ring_cell(rr, i1, i2, d, low);
+            const double* src = x + cidx(lp, i1, i2) * N3;
+            double u = 0, g = 0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double v = __ldg(src + pidx<N>(d == 1 ? 1 : 2, j, a, b));
+                u = fma(low ? T.e1[j] : T.e0[j], v, u); // a ring cell below the tile faces it with its upper end
+                g = fma(low ? T.d1[j] : T.d0[j], v, g);
+            }
+            Q(0, 6 * NC + rr)[ab] = u;
+            Q(1, 6 * NC + rr)[ab] = g;
         }
         __syncthreads();
+        // the plane buffer is no longer read this step: stream the next plane in behind the compute
+        if (tid == 0 && s + 1 < nsteps) issue(s + 1);
 
-        // ---------------- P2: flux transform; tangential derivatives of the face u-traces ----------------
-        for (int t = tid; t < NC * N3 + (AFFINE ? Y::NS * N2 : 0); t += NT) {
-            if (t < NC * N3) {
-                const int c = t / N3, P = t % N3, q0 = P % N, q1 = (P / N) % N, q2 = P / N2;
-                double cW = sW[q0] * sW[q1] * sW[q2];
-                if (COEFF) cW *= cval(c, q0, q1, q2);
-                double* g0 = G + (0 * NC + c) * N3;
-                double* g1 = G + (1 * NC + c) * N3;
-                double* g2 = G + (2 * NC + c) * N3;
+        // ---------------- P2: flux transform at (a, b, q); tangential derivatives ----------------
+        if (act) {
+            double gt[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) gt[i] = AFFINE ? GEO[mc * GREC + i] : 0.0;
+            // c(x) at (a, b, q) = 1 + 0.5 Im(z0 E02[q]) Re(z1 E12[q]) with z_k = e^{2 pi i o_k} E_k0[a] E_k1[b]
+            double z0r = 0, z0i = 0, z1r = 0, z1i = 0;
+            if (COEFF) {
+                const double* cx = CX + mc * Y::CXSZ;
+                double tr, ti;
+                tl::cmul(CO[mc * 4 + 0], CO[mc * 4 + 1], cx[((0 * 3 + 0) * (N + 1) + ma) * 2], cx[((0 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
+                tl::cmul(tr, ti, cx[((0 * 3 + 1) * (N + 1) + mb) * 2], cx[((0 * 3 + 1) * (N + 1) + mb) * 2 + 1], z0r, z0i);
+                tl::cmul(CO[mc * 4 + 2], CO[mc * 4 + 3], cx[((1 * 3 + 0) * (N + 1) + ma) * 2], cx[((1 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
+                tl::cmul(tr, ti, cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
+            }
+            const double wab = sW[ma] * sW[mb];
+            double* g0 = G + (0 * NC + mc) * N3;
+            double* g1 = G + (1 * NC + mc) * N3;
+            double* g2 = G + (2 * NC + mc) * N3;
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                const int P = mab + N2 * q;
+                double cW = wab * T.w[q];
+                if (COEFF) {
+                    const double* cx = CX + mc * Y::CXSZ;
+                    const double* e0 = cx + ((0 * 3 + 2) * (N + 1) + q) * 2;
+                    const double* e1 = cx + ((1 * 3 + 2) * (N + 1) + q) * 2;
+                    const double s0 = fma(z0r, e0[1], z0i * e0[0]);  // Im(z0 e0) = sin(2 pi x0)
+                    const double c1 = fma(z1r, e1[0], -z1i * e1[1]); // Re(z1 e1) = cos(2 pi x1)
+                    cW *= fma(0.5 * s0, c1, 1.0);
+                }
                 const double a0 = g0[P], a1 = g1[P], a2 = g2[P];
                 if (AFFINE) {
-                    const double* g = GEO + c * GREC;
-                    g0[P] = cW * (g[0] * a0 + g[3] * a1 + g[4] * a2);
-                    g1[P] = cW * (g[3] * a0 + g[1] * a1 + g[5] * a2);
-                    g2[P] = cW * (g[4] * a0 + g[5] * a1 + g[2] * a2);
+                    g0[P] = cW * (gt[0] * a0 + gt[3] * a1 + gt[4] * a2);
+                    g1[P] = cW * (gt[3] * a0 + gt[1] * a1 + gt[5] * a2);
+                    g2[P] = cW * (gt[4] * a0 + gt[5] * a1 + gt[2] * a2);
                 } else {
                     const double adet = M.h[0] * M.h[1] * M.h[2];
                     g0[P] = cW * (adet / (M.h[0] * M.h[0])) * a0;
                     g1[P] = cW * (adet / (M.h[1] * M.h[1])) * a1;
                     g2[P] = cW * (adet / (M.h[2] * M.h[2])) * a2;
                 }
-            } else {
-                const int tt = t - NC * N3, slot = tt / N2, ab = tt % N2, a = ab % N, b = ab / N;
-                const double* U = Q(0, slot);
-                double v1 = 0.0, v2 = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    v1 = fma(sD[a * N + j], U[j + N * b], v1);
-                    v2 = fma(sD[b * N + j], U[a + N * j], v2);
-                }
-                Q(2, slot)[ab] = v1;
-                Q(3, slot)[ab] = v2;
             }
-        }
-        __syncthreads();
-
-        // ---------------- P3: face fluxes ----------------
-        // tasks [0, 3 NC N2): the upper face d of own cell c (T- = c);
-        //       [3 NC N2, NF): the lower faces at the tile's low boundary (T- = ring cell below)
-        constexpr int NF = 3 * NC * N2 + (T2 + T1) * N2;
-        constexpr int MAXF = (NF + NT - 1) / NT;
-        double oCv[MAXF][2], oG[MAXF][2], oC1[MAXF][2], oC2[MAXF][2];
-        int oslot[MAXF][2];
-#pragma unroll
-        for (int k = 0; k < MAXF; ++k) {
-            const int t = tid + k * NT;
-            oslot[k][0] = oslot[k][1] = -1;
-            oCv[k][0] = oCv[k][1] = oG[k][0] = oG[k][1] = oC1[k][0] = oC1[k][1] = oC2[k][0] = oC2[k][1] = 0.0;
-            if (t >= NF) continue;
-            int d, ab, sMinus, sPlus, gslot;
-            int tMinus = -1, tPlus = -1; // receiving slots (-1: belongs to another CTA)
-            if (t < 3 * NC * N2) {
-                const int c = t / (3 * N2), rem = t % (3 * N2), c1 = c / T2, c2 = c % T2;
-                d = rem / N2;
-                ab = rem % N2;
-                sMinus = c * 6 + 2 * d + 1;
-                tMinus = sMinus;
-                gslot = c;
-                if (d == 0) { sPlus = SNEXT + c; tPlus = sPlus; } // T+ half carried to the next plane
-                else if (d == 1) {
-                    if (c1 + 1 < T1) { sPlus = ((c1 + 1) * T2 + c2) * 6 + 2; tPlus = sPlus; }
-                    else sPlus = 6 * NC + T2 + c2;
-                } else {
-                    if (c2 + 1 < T2) { sPlus = (c1 * T2 + c2 + 1) * 6 + 4; tPlus = sPlus; }
-                    else sPlus = 6 * NC + 2 * T2 + T1 + c1;
-                }
-            } else {
-                const int tt = t - 3 * NC * N2, f = tt / N2;
-                ab = tt % N2;
-                int c;
-                if (f < T2) { d = 1; c = f; sMinus = 6 * NC + f; gslot = NC + f; }
-                else { d = 2; const int c1 = f - T2; c = c1 * T2; sMinus = 6 * NC + 2 * T2 + c1; gslot = NC + 2 * T2 + c1; }
-                sPlus = c * 6 + 2 * d + 0;
-                tPlus = sPlus;
-            }
-            const int a = ab % N, b = ab / N;
-            const double jump = Q(0, sMinus)[ab] - Q(0, sPlus)[ab];
-            const double gmd = Q(1, sMinus)[ab], gpd = Q(1, sPlus)[ab];
-            double cF = 1.0;
-            if (COEFF) {
-                const int q0 = (d == 0) ? N : a, q1 = (d == 1) ? N : (d == 0 ? a : b), q2 = (d == 2) ? N : b;
-                cF = cval(gslot, q0, q1, q2); // x_F on the T- cell at xi_d = 1
-            }
-            const double gam = d == 0 ? M.gamma[0] : (d == 1 ? M.gamma[1] : M.gamma[2]);
-            double Cvm, Cvp, Cg, am_d, am_t1, am_t2, ap_d, ap_t1, ap_t2;
-            if (!AFFINE) {
-                const double hd = d == 0 ? M.h[0] : (d == 1 ? M.h[1] : M.h[2]);
-                const double W = sW[a] * sW[b] * (M.h[0] * M.h[1] * M.h[2] / hd);
-                const double avg = 0.5 * cF * (gmd + gpd) / hd;
-                Cvm = W * (-avg + gam * jump);
-                Cvp = W * (avg - gam * jump);
-                Cg = -0.5 * W * jump * cF;
-                am_d = ap_d = 1.0 / hd;
-                am_t1 = am_t2 = ap_t1 = ap_t2 = 0.0;
-            } else {
-                const int t1 = (d == 0) ? 1 : 0, t2 = (d == 2) ? 1 : 2;
-                const double* f = GEO + gslot * GREC + 12 + 7 * d;
-                auto comp = [&](const double* v, int e) { return e == 0 ? v[0] : (e == 1 ? v[1] : v[2]); };
-                am_d = comp(f + 1, d); am_t1 = comp(f + 1, t1); am_t2 = comp(f + 1, t2);
-                ap_d = comp(f + 4, d); ap_t1 = comp(f + 4, t1); ap_t2 = comp(f + 4, t2);
-                const double gm = cF * (am_d * gmd + am_t1 * Q(2, sMinus)[ab] + am_t2 * Q(3, sMinus)[ab]);
-                const double gp = cF * (ap_d * gpd + ap_t1 * Q(2, sPlus)[ab] + ap_t2 * Q(3, sPlus)[ab]);
-                const double avg = 0.5 * (gm + gp);
-                const double W = sW[a] * sW[b] * f[0];
-                Cvm = W * (-avg + gam * jump);
-                Cvp = W * (avg - gam * jump);
-                Cg = -0.5 * W * jump * cF;
-            }
-            if (tMinus >= 0) {
-                oslot[k][0] = tMinus * N2 + ab;
-                oCv[k][0] = Cvm; oG[k][0] = am_d * Cg; oC1[k][0] = am_t1 * Cg; oC2[k][0] = am_t2 * Cg;
-            }
-            if (tPlus >= 0) {
-                oslot[k][1] = tPlus * N2 + ab;
-                oCv[k][1] = Cvp; oG[k][1] = ap_d * Cg; oC1[k][1] = ap_t1 * Cg; oC2[k][1] = ap_t2 * Cg;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < MAXF; ++k) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int o = oslot[k][h];
-                if (o < 0) continue;
-                TQ[0 * QSZ + o] = oCv[k][h];
-                TQ[1 * QSZ + o] = oG[k][h];
-                TQ[2 * QSZ + o] = oC1[k][h];
-                TQ[3 * QSZ + o] = oC2[k][h];
-            }
-        }
-        // the lower d=0 side of each own cell was evaluated on the previous step: V+, G+
-        for (int t = tid; t < NC * N2; t += NT) {
-            const int c = t / N2, ab = t % N2;
-            TQ[4 * QSZ + (c * 6 + 0) * N2 + ab] = Pin[c * N2 + ab];
-            TQ[1 * QSZ + (c * 6 + 0) * N2 + ab] = Pin[NC * N2 + c * N2 + ab];
-        }
-        __syncthreads();
-
-        // ---------------- P4: V = Cv + D^T_t1 Ct1 + D^T_t2 Ct2 (own sides; the next plane's T+ half) ----------------
-        for (int t = tid; t < 7 * NC * N2; t += NT) {
-            const int f = t / N2, ab = t % N2, a = ab % N, b = ab / N;
-            int slot;
-            if (f < 6 * NC) {
-                if (f % 6 == 0) continue; // lower d=0 side: from the pending buffer
-                slot = f;
-            } else slot = SNEXT + (f - 6 * NC);
-            double v = TQ[0 * QSZ + slot * N2 + ab];
             if (AFFINE) {
-                const double* C1 = Q(2, slot);
-                const double* C2 = Q(3, slot);
+                double Da[N], Db[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    v = fma(sD[j * N + a], C1[j + N * b], v);
-                    v = fma(sD[j * N + b], C2[a + N * j], v);
-                }
+                for (int j = 0; j < N; ++j) { Da[j] = sD[ma * N + j]; Db[j] = sD[mb * N + j]; }
+#pragma unroll
+                for (int f = 1; f < 6; ++f) tangential_r(mc * 6 + f, ma, mb, Da, Db); // the lower d0 side is pending
+                tangential_r(SNEXT + mc, ma, mb, Da, Db);
             }
-            if (f < 6 * NC) TQ[4 * QSZ + slot * N2 + ab] = v;
-            else {
-                const int c = f - 6 * NC;
-                Pout[c * N2 + ab] = v;
-                Pout[NC * N2 + c * N2 + ab] = TQ[1 * QSZ + slot * N2 + ab];
+        }
+        if (AFFINE) {
+            for (int t = tid; t < NR * N2; t += NT) {
+                const int rr = t / N2, ab = t % N2;
+                tangential(6 * NC + rr, ab % N, ab / N);
             }
         }
         __syncthreads();
 
-        // ---------------- P5: stage 3 fused with the face back-projection; passes d = 1, 2, 0 ----------------
-#pragma unroll 1
+        // ---------------- P3: face fluxes (each face once on this CTA) ----------------
+        if (act) {
+            // upper faces of cell mc (T- = mc)
+            face(0, ma, mb, mc * 6 + 1, SNEXT + mc, mc, true, true);
+            {
+                const bool in = mc1 + 1 < T1;
+                const int sp = in ? ((mc1 + 1) * T2 + mc2) * 6 + 2 : 6 * NC + T2 + mc2;
+                face(1, ma, mb, mc * 6 + 3, sp, mc, true, in);
+            }
+            {
+                const bool in = mc2 + 1 < T2;
+                const int sp = in ? (mc1 * T2 + mc2 + 1) * 6 + 4 : 6 * NC + 2 * T2 + T1 + mc1;
+                face(2, ma, mb, mc * 6 + 5, sp, mc, true, in);
+            }
+            // lower faces on the tile's low boundary (T- = ring cell below)
+            if (mc1 == 0) face(1, ma, mb, 6 * NC + mc2, mc * 6 + 2, NC + mc2, false, true);
+            if (mc2 == 0) face(2, ma, mb, 6 * NC + 2 * T2 + mc1, mc * 6 + 4, NC + 2 * T2 + mc1, false, true);
+            // the lower d=0 side was evaluated on the previous step: V+, G+
+            Q(0, mc * 6 + 0)[mab] = Pin[mc * N2 + mab];
+            Q(1, mc * 6 + 0)[mab] = Pin[NC * N2 + mc * N2 + mab];
+        }
+        __syncthreads();
+
+        // ---------------- P4: V on every own side (in place of Cv) and on the next plane's T+ half ----------------
+        if (act) {
+            double Ca[N], Cb[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) { Ca[j] = sD[j * N + ma]; Cb[j] = sD[j * N + mb]; }
+            double v[6];
+#pragma unroll
+            for (int f = 1; f < 6; ++f) v[f] = vface_r(mc * 6 + f, ma, mb, Ca, Cb);
+            const double vn = vface_r(SNEXT + mc, ma, mb, Ca, Cb);
+            // (other threads read only Ct1 / Ct2 of these slots, never Cv: in-place update is safe)
+#pragma unroll
+            for (int f = 1; f < 6; ++f) Q(0, mc * 6 + f)[mab] = v[f];
+            Pout[mc * N2 + mab] = vn;
+            Pout[NC * N2 + mc * N2 + mab] = Q(1, SNEXT + mc)[mab];
+        }
+        __syncthreads();
+
+        // ---------------- P5: stage 3 + face back-projection; passes d = 1, 2 (in place), 0 (to r) ----------------
+#pragma unroll
         for (int pass = 0; pass < 3; ++pass) {
             const int d = (pass == 2) ? 0 : pass + 1;
-            for (int t = tid; t < NC * N2; t += NT) {
-                const int c = t / N2, ab = t % N2, a = ab % N, b = ab / N;
-                const double* qd = G + (d * NC + c) * N3;
+            if (act) {
+                double* qd = G + (d * NC + mc) * N3;
                 double q[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) q[j] = qd[pidx<N>(d, j, a, b)];
-                const double Vl = TQ[4 * QSZ + (c * 6 + 2 * d + 0) * N2 + ab];
-                const double Vh = TQ[4 * QSZ + (c * 6 + 2 * d + 1) * N2 + ab];
-                const double Gl = TQ[1 * QSZ + (c * 6 + 2 * d + 0) * N2 + ab];
-                const double Gh = TQ[1 * QSZ + (c * 6 + 2 * d + 1) * N2 + ab];
-                double* rc = RR + c * N3;
-                double* dst = nullptr;
-                if (pass == 2) {
-                    const int c1 = c / T2, c2 = c % T2;
-                    dst = r + cidx(lp, ti1 * T1 + c1, ti2 * T2 + c2) * N3;
-                }
+                for (int j = 0; j < N; ++j) q[j] = qd[pidx<N>(d, j, ma, mb)];
+                const double Vl = Q(0, mc * 6 + 2 * d + 0)[mab], Vh = Q(0, mc * 6 + 2 * d + 1)[mab];
+                const double Gl = Q(1, mc * 6 + 2 * d + 0)[mab], Gh = Q(1, mc * 6 + 2 * d + 1)[mab];
+                const double* prev = G + ((pass == 1 ? 1 : 2) * NC + mc) * N3; // partial sums of the earlier passes
+                double* dst = r + (cidx(lp, 0, 0) + minpl) * N3;
 #pragma unroll
                 for (int i = 0; i < N; ++i) {
                     double acc = fma(T.e0[i], Vl, fma(T.d0[i], Gl, fma(T.e1[i], Vh, T.d1[i] * Gh)));
 #pragma unroll
                     for (int j = 0; j < N; ++j) acc = fma(T.D[j * N + i], q[j], acc);
-                    const int P = pidx<N>(d, i, a, b);
-                    if (pass == 0) rc[P] = acc;
-                    else if (pass == 1) rc[P] += acc;
-                    else dst[P] = rc[P] + acc;
+                    const int P = pidx<N>(d, i, ma, mb);
+                    if (pass == 0) qd[P] = acc;                 // R1 in place of Q1
+                    else if (pass == 1) qd[P] = acc + prev[P];  // R1 + R2 in place of Q2
+                    else dst[P] = acc + prev[P];                // r = R1 + R2 + R0
                 }
             }
             __syncthreads();
         }
         pend ^= 1;
-        if (tid == 0 && s + 2 < nsteps) issue(s + 2);
     }
 }
 
