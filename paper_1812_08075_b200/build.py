@@ -31,7 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC] + ARCH + FLAGS + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+    extra = os.environ.get("DG_BUILD_FLAGS", "").split()  # experiments only (e.g. -DDG_AX8_TRACE)
+    cmd = [NVCC] + ARCH + FLAGS + extra + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(LIBDIR, "build.log")
     with open(log, "w") as f:

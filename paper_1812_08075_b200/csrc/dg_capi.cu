@@ -3,6 +3,7 @@
 #include "common.cuh"
 #include "kernel_axis8.cuh"
 #include "kernel_cell.cuh"
+#include "kernel_gen.cuh"
 #include "kernel_tile.cuh"
 #include "tables.h"
 
@@ -13,6 +14,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+
+// k_axis8 variants (DG_AX8_TILE=<T1>x<T2>m<minBlocks>; default = the first): ID, T1, T2, threads, min CTAs/SM
+#define AX8_VARIANTS(X) \
+    X(0, 2, 4, 256, 2)  \
+    X(1, 2, 4, 256, 1)  \
+    X(2, 4, 4, 512, 1)  \
+    X(3, 2, 2, 256, 3)  \
+    X(4, 2, 2, 256, 2)  \
+    X(5, 4, 2, 256, 2)
 
 namespace {
 
@@ -144,6 +154,125 @@ TileInfo pick_tile(int n, bool aff, bool coef)
     }
 }
 
+// ---- marching-tile general kernel v2 (k_gen): tile per degree (T1, T2 even for odd n: 16-B bulk rows)
+template <int N> struct GenShape;
+template <> struct GenShape<2> { static constexpr int T1 = 4, T2 = 4, MINB = 4; };
+template <> struct GenShape<3> { static constexpr int T1 = 2, T2 = 4, MINB = 4; };
+template <> struct GenShape<4> { static constexpr int T1 = 2, T2 = 4, MINB = 3; };
+template <> struct GenShape<5> { static constexpr int T1 = 2, T2 = 2, MINB = 3; };
+template <> struct GenShape<6> { static constexpr int T1 = 2, T2 = 2, MINB = 2; };
+template <> struct GenShape<7> { static constexpr int T1 = 2, T2 = 2, MINB = 1; };
+template <> struct GenShape<8> { static constexpr int T1 = 2, T2 = 2, MINB = 1; };
+
+using GenFn = cudaError_t (*)(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
+                              double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo);
+
+template <int N, bool AFF, bool COEF>
+cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
+                       double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo)
+{
+    constexpr int T1 = GenShape<N>::T1, T2 = GenShape<N>::T2, MB = GenShape<N>::MINB;
+    using Y = dg::gn::Lay<N, AFF, COEF, T1, T2>;
+    if (p1 <= p0) return cudaSuccess;
+    const int np = p1 - p0;
+    const int CL = chunk > 0 && chunk < np ? chunk : np;
+    const unsigned grid = (unsigned)((M.N1 / T1) * (M.N2 / T2) * ((np + CL - 1) / CL));
+    dg::k_gen<N, AFF, COEF, T1, T2, MB><<<grid, Y::NT, Y::BYTES, st>>>(
+        x, xb, xa, r, p0, p1, CL, *static_cast<const dg::EOTab<N>*>(eot), M, geo);
+    return cudaGetLastError();
+}
+
+template <int N, bool AFF, bool COEF>
+cudaError_t attr_gen()
+{
+    constexpr int T1 = GenShape<N>::T1, T2 = GenShape<N>::T2, MB = GenShape<N>::MINB;
+    return cudaFuncSetAttribute(dg::k_gen<N, AFF, COEF, T1, T2, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dg::gn::Lay<N, AFF, COEF, T1, T2>::BYTES);
+}
+
+struct GenInfo {
+    GenFn fn;
+    int T1, T2, smem;
+    cudaError_t (*attr)();
+};
+
+template <int N>
+GenInfo gen_info(bool aff, bool coef)
+{
+    GenInfo g;
+    g.T1 = GenShape<N>::T1;
+    g.T2 = GenShape<N>::T2;
+    if (aff) {
+        g.fn = coef ? launch_gen<N, true, true> : launch_gen<N, true, false>;
+        g.attr = coef ? attr_gen<N, true, true> : attr_gen<N, true, false>;
+        g.smem = coef ? dg::gn::Lay<N, true, true, GenShape<N>::T1, GenShape<N>::T2>::BYTES
+                      : dg::gn::Lay<N, true, false, GenShape<N>::T1, GenShape<N>::T2>::BYTES;
+    } else {
+        g.fn = coef ? launch_gen<N, false, true> : launch_gen<N, false, false>;
+        g.attr = coef ? attr_gen<N, false, true> : attr_gen<N, false, false>;
+        g.smem = coef ? dg::gn::Lay<N, false, true, GenShape<N>::T1, GenShape<N>::T2>::BYTES
+                      : dg::gn::Lay<N, false, false, GenShape<N>::T1, GenShape<N>::T2>::BYTES;
+    }
+    return g;
+}
+
+GenInfo pick_gen(int n, bool aff, bool coef)
+{
+    switch (n) {
+    case 2: return gen_info<2>(aff, coef);
+    case 3: return gen_info<3>(aff, coef);
+    case 4: return gen_info<4>(aff, coef);
+    case 5: return gen_info<5>(aff, coef);
+    case 6: return gen_info<6>(aff, coef);
+    case 7: return gen_info<7>(aff, coef);
+    default: return gen_info<8>(aff, coef);
+    }
+}
+
+// even/odd tables (kernel_gen.cuh, EOTab): D is centro-antisymmetric and e1, d1 are the mirrored
+// e0, -d0 on the symmetric Gauss nodes; the halves fold the factor 1/2 in.
+template <int N>
+void fill_eotab(const dg::HostTables& Ht, void* out)
+{
+    dg::EOTab<N>* E = static_cast<dg::EOTab<N>*>(out);
+    constexpr int H = N / 2;
+    auto D = [&](int q, int j) { return Ht.D[q * N + j]; };
+    for (int q = 0; q < H; ++q) {
+        for (int j = 0; j < H; ++j) {
+            E->Fm[q][j] = 0.5 * (D(q, j) - D(q, N - 1 - j));
+            E->Fp[q][j] = 0.5 * (D(q, j) + D(q, N - 1 - j));
+            E->Tm[q][j] = 0.5 * (D(j, q) - D(N - 1 - j, q));
+            E->Tp[q][j] = 0.5 * (D(j, q) + D(N - 1 - j, q));
+        }
+        if (N & 1) {
+            E->Fp[q][H] = D(q, H);
+            E->Tp[q][H] = D(H, q);
+        }
+        if (N & 1) {
+            E->Fmid[q] = D(H, q);
+            E->Tmid[q] = D(q, H);
+        } else {
+            E->Fmid[q] = 0.0;
+            E->Tmid[q] = 0.0;
+        }
+    }
+    for (int j = 0; j < H; ++j) {
+        E->Es[j] = 0.5 * (Ht.e0[j] + Ht.e0[N - 1 - j]);
+        E->Ea[j] = 0.5 * (Ht.e0[j] - Ht.e0[N - 1 - j]);
+        E->Ds[j] = 0.5 * (Ht.d0[j] + Ht.d0[N - 1 - j]);
+        E->Da[j] = 0.5 * (Ht.d0[j] - Ht.d0[N - 1 - j]);
+    }
+    if (N & 1) {
+        E->Es[H] = Ht.e0[H];
+        E->Ds[H] = Ht.d0[H];
+    }
+    for (int i = 0; i < N * N; ++i) E->D[i] = Ht.D[i];
+    for (int i = 0; i < N; ++i) {
+        E->w[i] = Ht.w[i];
+        E->xi[i] = Ht.xi[i];
+    }
+}
+
 template <int N>
 void fill_tab(const dg::HostTables& H, void* out)
 {
@@ -232,6 +361,10 @@ struct dg_ctx {
     bool ax8;
     bool tile;
     TileInfo tinfo;
+    bool gen;
+    GenInfo ginfo;
+    int gen_chunk;
+    alignas(16) unsigned char eotab[sizeof(dg::EOTab<dg::kMaxN>)];
     int ax8_tile, ax8_T1, ax8_T2, ax8_chunk;
     dg::AxisTab8 atab;
     CUtensorMap tmap;
@@ -266,20 +399,18 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         const int np = p1 - p0;
         const int CL = c->ax8_chunk > 0 ? (c->ax8_chunk < np ? c->ax8_chunk : np) : np;
         const unsigned grid = (unsigned)(ntiles * ((np + CL - 1) / CL));
-        if (c->ax8_tile == 0)
-            dg::k_axis8<2, 4, 256><<<grid, 256, dg::ax8::Cfg<2, 4, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
-                                                                                          c->atab, c->M, c->dbg);
-        else if (c->ax8_tile == 1)
-            dg::k_axis8<4, 4, 512><<<grid, 512, dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
-                                                                                          c->atab, c->M, c->dbg);
-        else if (c->ax8_tile == 2)
-            dg::k_axis8<4, 2, 256><<<grid, 256, dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
-                                                                                          c->atab, c->M, c->dbg);
-        else
-            dg::k_axis8<2, 2, 256><<<grid, 256, dg::ax8::Cfg<2, 2, 256>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, CL,
-                                                                                          c->atab, c->M, c->dbg);
+        switch (c->ax8_tile) {
+#define AX8_LAUNCH(ID, T1, T2, NT, MB)                                                                               \
+    case ID:                                                                                                         \
+        dg::k_axis8<T1, T2, NT, MB><<<grid, NT, dg::ax8::Cfg<T1, T2, NT>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, \
+                                                                                          CL, c->atab, c->M, c->dbg); \
+        break;
+            AX8_VARIANTS(AX8_LAUNCH)
+#undef AX8_LAUNCH
+        }
         return cudaGetLastError();
     }
+    if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo);
     if (c->tile) return c->tinfo.fn(c->tab, c->M, x, xb, xa, r, p0, p1, st, c->d_geo);
     const long long pc = c->M.plane_cells;
     return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
@@ -368,30 +499,51 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         const bool rows_aligned = (rowb % 16 == 0) && ((n3 * 8) % 16 == 0 || (mesh->N[2] % 2 == 0 && c->tinfo.T2 % 2 == 0));
         c->tile = mesh->N[1] % c->tinfo.T1 == 0 && mesh->N[2] % c->tinfo.T2 == 0 && rows_aligned &&
                   getenv("DG_FORCE_GENERAL") == nullptr && c->tinfo.attr() == cudaSuccess;
-        if (c->tile && mesh->geom_kind == DG_GEOM_AFFINE) {
+        // k_gen (preferred): tiles divide the mesh; odd n^3 needs even T2 and N2 for 16-B aligned bulk rows
+        c->ginfo = pick_gen(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
+        c->gen = mesh->N[1] % c->ginfo.T1 == 0 && mesh->N[2] % c->ginfo.T2 == 0 &&
+                 ((n3 % 2 == 0) || (mesh->N[2] % 2 == 0 && c->ginfo.T2 % 2 == 0)) && getenv("DG_FORCE_GENERAL") == nullptr &&
+                 getenv("DG_NO_GEN") == nullptr && c->ginfo.attr() == cudaSuccess;
+        {
+            const char* gc = getenv("DG_GEN_CHUNK");
+            c->gen_chunk = gc ? atoi(gc) : 16;
+        }
+        if (c->gen) {
+            switch (n) {
+            case 2: fill_eotab<2>(H, c->eotab); break;
+            case 3: fill_eotab<3>(H, c->eotab); break;
+            case 4: fill_eotab<4>(H, c->eotab); break;
+            case 5: fill_eotab<5>(H, c->eotab); break;
+            case 6: fill_eotab<6>(H, c->eotab); break;
+            case 7: fill_eotab<7>(H, c->eotab); break;
+            case 8: fill_eotab<8>(H, c->eotab); break;
+            }
+        }
+        if ((c->tile || c->gen) && mesh->geom_kind == DG_GEOM_AFFINE) {
             // per-cell geometry records for the tile kernel (k_geom, once)
             const long long nc = (long long)M.plane_cells * (M.L + 2);
             cudaError_t e = cudaMalloc(&c->d_geo, sizeof(double) * dg::GREC * (size_t)nc);
             if (e != cudaSuccess) {
-                c->tile = false;
+                c->tile = c->gen = false;
             } else {
                 dg::k_geom<<<(unsigned)((nc + 255) / 256), 256>>>(c->d_jac, c->d_geo, nc, M.plane_cells, M.N1, M.N2, M.L + 2);
-                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_geo); c->d_geo = nullptr; c->tile = false; }
+                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_geo); c->d_geo = nullptr; c->tile = c->gen = false; }
             }
         }
         if (c->tile) c->kname = "k_tile";
+        if (c->gen) c->kname = "k_gen";
     }
-    // axis-aligned Q7 fast path: tile T1 x T2 (env DG_AX8_TILE = 2x4 | 4x4 | 4x2 for experiments)
+    // axis-aligned Q7 fast path: tile T1 x T2 (env DG_AX8_TILE picks an AX8_VARIANTS entry for experiments)
     {
         const char* tv = getenv("DG_AX8_TILE");
         c->ax8_tile = 0;
-        if (tv && !strcmp(tv, "4x4")) c->ax8_tile = 1;
-        if (tv && !strcmp(tv, "4x2")) c->ax8_tile = 2;
-        if (tv && !strcmp(tv, "2x2")) c->ax8_tile = 3;
-        const int T1 = (c->ax8_tile == 1 || c->ax8_tile == 2) ? 4 : 2;
-        const int T2 = (c->ax8_tile == 2 || c->ax8_tile == 3) ? 2 : 4;
-        c->ax8_T1 = T1;
-        c->ax8_T2 = T2;
+        c->ax8_T1 = 2;
+        c->ax8_T2 = 4;
+#define AX8_PICK(ID, T1_, T2_, NT, MB)                                                                 \
+    if (tv && !strcmp(tv, #T1_ "x" #T2_ "m" #MB)) { c->ax8_tile = ID; c->ax8_T1 = T1_; c->ax8_T2 = T2_; }
+        AX8_VARIANTS(AX8_PICK)
+#undef AX8_PICK
+        const int T1 = c->ax8_T1, T2 = c->ax8_T2;
         const char* cl = getenv("DG_AX8_CHUNK");
         c->ax8_chunk = cl ? atoi(cl) : 12; // planes per work item (0: whole slab)
         c->ax8 = (n == 8 && mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE &&
@@ -400,18 +552,15 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (c->ax8) {
         build_axis8(H, mesh->penalty_scale * k * (k + 1), M.h, &c->atab);
         cudaError_t e = cudaSuccess;
-        if (c->ax8_tile == 0)
-            e = cudaFuncSetAttribute(dg::k_axis8<2, 4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     dg::ax8::Cfg<2, 4, 256>::SMEM_BYTES);
-        else if (c->ax8_tile == 1)
-            e = cudaFuncSetAttribute(dg::k_axis8<4, 4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     dg::ax8::Cfg<4, 4, 512>::SMEM_BYTES);
-        else if (c->ax8_tile == 2)
-            e = cudaFuncSetAttribute(dg::k_axis8<4, 2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     dg::ax8::Cfg<4, 2, 256>::SMEM_BYTES);
-        else
-            e = cudaFuncSetAttribute(dg::k_axis8<2, 2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     dg::ax8::Cfg<2, 2, 256>::SMEM_BYTES);
+        switch (c->ax8_tile) {
+#define AX8_ATTR(ID, T1, T2, NT, MB)                                                                                   \
+    case ID:                                                                                                           \
+        e = cudaFuncSetAttribute(dg::k_axis8<T1, T2, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                 dg::ax8::Cfg<T1, T2, NT>::SMEM_BYTES);                                                \
+        break;
+            AX8_VARIANTS(AX8_ATTR)
+#undef AX8_ATTR
+        }
         if (e != cudaSuccess || !get_encode()) c->ax8 = false;
         else c->kname = "k_axis8";
         if (c->ax8 && getenv("DG_TRACE")) {
@@ -499,6 +648,8 @@ int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* 
         return fail(DG_ERR_INVALID, "dg_apply: pointers must be 8-byte aligned");
     if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned");
     if (((uintptr_t)x & 15) && c->tile) return fail(DG_ERR_INVALID, "dg_apply: x must be 16-byte aligned");
+    if ((((uintptr_t)x | (uintptr_t)xb | (uintptr_t)xa) & 15) && c->gen)
+        return fail(DG_ERR_INVALID, "dg_apply: x and the halo planes must be 16-byte aligned");
     cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
     return DG_OK;

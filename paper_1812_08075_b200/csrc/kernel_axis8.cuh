@@ -265,8 +265,8 @@ __device__ __forceinline__ double inplane_scale(const AxisTab8& A, int tid)
 } // namespace ax8
 
 // grid: (N1/T1) * (N2/T2) CTAs, block NT, dynamic smem Cfg::SMEM_BYTES
-template <int T1, int T2, int NT>
-__global__ void __launch_bounds__(NT, ax8::Cfg<T1, T2, NT>::MINB)
+template <int T1, int T2, int NT, int MB = ax8::Cfg<T1, T2, NT>::MINB>
+__global__ void __launch_bounds__(NT, MB)
 k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, const double* __restrict__ xb,
         const double* __restrict__ xa, double* __restrict__ r, int p_begin, int p_end, int chunk_len,
         const AxisTab8 A, const MeshArgs M, long long* __restrict__ dbg)

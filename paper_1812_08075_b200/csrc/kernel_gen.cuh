@@ -1,0 +1,648 @@
+// K_gen: the general sum-factorised SIPG operator (any degree n = k+1 in 2..8, per-cell affine
+// geometry, c(x)) — the path of the affine configs (cfg2 Q5, cfg4 Q4) and of the axis-aligned
+// configs other than Q7. Successor of k_tile (kernel_tile.cuh) with the same mathematics:
+//
+//   Alg. assembly per cell, collocation (A = I, reading R8):
+//     stage 1  grad_hat U = (D along d) X,
+//     stage 2  Q = w_q c(x_q) |det J| J^{-1} J^{-T} grad_hat U,       P:L867-872 (Eq. diffreac_weak)
+//     stage 3  R = sum_d (D^T along d) Q_d,
+//   faces (P:L883-886, 1-point tables e0/e1/d0/d1 P:L143-146), SIPG flux of Eq. diffreac_weak
+//   (theta = -1), geometry of T- (reading R11), c_F at the T- mapped point (R12).
+//
+// What is new against k_tile (design notes):
+//  * every global input of a plane step (own blocks of the NEXT plane, ring blocks, geometry
+//    records) arrives asynchronously one step ahead (cp.async.bulk + mbarrier; cp.async for the
+//    odd-sized single ring cells): the compute phases touch only shared memory and registers;
+//  * line sweeps in even/odd form (D is centro-antisymmetric on the symmetric Gauss nodes): about
+//    half the FMAs of a plain n x n product and half-length dependency chains;
+//  * faces are evaluated once per face (T- side owner), with the tangential parts of both sides
+//    combined by linearity: {g} needs D_t (a-_t u- + a+_t u+), and the back-projection of the
+//    gradient test term needs D_t^T Cg once per face (a+- constant on an affine face);
+//  * the T+ half of the face to the next plane stays in the registers of the thread that owns the
+//    same line position on the next plane (no pending buffer);
+//  * stage-3 partial sums of directions 0 and 1 are written in place of Q_0 / Q_1 (one barrier
+//    fewer); direction 2 stays in registers from stage 1 to stage 3.
+#pragma once
+
+#include "common.cuh"
+#include "kernel_tile.cuh" // k_geom / GREC records, tl:: mbarrier + bulk-copy helpers
+
+namespace dg {
+
+// Even/odd (centro-(anti)symmetric) forms of the 1D tables, built on the host (dg_capi.cu).
+// With xe_j = x_j + x_{n-1-j}, xo_j = x_j - x_{n-1-j} (j < H), xe_H = x_H (odd n):
+//   y = D x      : S_q = sum_{j<H} Fm[q][j] xo_j, A_q = sum_{j<HE} Fp[q][j] xe_j, y_q = S_q + A_q,
+//                  y_{n-1-q} = S_q - A_q (q < H); odd n: y_H = sum_{j<H} Fmid[j] xo_j
+//   y = D^T x    : the same with Tm, Tp, Tmid
+//   traces       : u_lo = TE + TO, u_hi = TE - TO, gn_lo = QE + QO, gn_hi = QO - QE with
+//                  TE = sum Es xe, TO = sum Ea xo, QE = sum Ds xe, QO = sum Da xo
+//   face terms of stage 3: S_i += Es_i (Vl + Vh) + Ds_i (Gl - Gh), A_i += Ea_i (Vl - Vh) + Da_i (Gl + Gh)
+template <int N>
+struct EOTab {
+    static constexpr int H = N / 2, ODD = N & 1, HE = H + ODD;
+    double Fm[H][H], Fp[H][HE], Fmid[H];
+    double Tm[H][H], Tp[H][HE], Tmid[H];
+    double Es[HE], Ea[H], Ds[HE], Da[H];
+    double D[N * N];   // plain D[q*N + j] (tangential face derivatives)
+    double w[N], xi[N];
+};
+
+namespace gn {
+
+using tl::bulk_g2s;
+using tl::mbar_expect_tx;
+using tl::mbar_init;
+using tl::mbar_wait;
+using tl::s32;
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// split a line into even/odd halves
+template <int N>
+__device__ __forceinline__ void split(const double v[N], double xe[EOTab<N>::HE], double xo[EOTab<N>::H])
+{
+    constexpr int H = EOTab<N>::H;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        xe[j] = v[j] + v[N - 1 - j];
+        xo[j] = v[j] - v[N - 1 - j];
+    }
+    if (N & 1) xe[H] = v[H];
+}
+
+// y = D x (TR = false) or y = D^T x (TR = true), plus optional stage-3 face terms at both ends
+template <int N, bool TR, bool FACE>
+__device__ __forceinline__ void sweep(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
+                                      double y[N], double Vl = 0, double Gl = 0, double Vh = 0, double Gh = 0)
+{
+    constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
+    const double sV = Vl + Vh, dV = Vl - Vh, sG = Gl + Gh, dG = Gl - Gh;
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+        double S = FACE ? fma(E.Es[q], sV, E.Ds[q] * dG) : 0.0;
+        double A = FACE ? fma(E.Ea[q], dV, E.Da[q] * sG) : 0.0;
+#pragma unroll
+        for (int j = 0; j < H; ++j) S = fma(TR ? E.Tm[q][j] : E.Fm[q][j], xo[j], S);
+#pragma unroll
+        for (int j = 0; j < HE; ++j) A = fma(TR ? E.Tp[q][j] : E.Fp[q][j], xe[j], A);
+        y[q] = S + A;
+        y[N - 1 - q] = S - A;
+    }
+    if (N & 1) {
+        double m = FACE ? fma(E.Es[H], sV, E.Ds[H] * dG) : 0.0;
+#pragma unroll
+        for (int j = 0; j < H; ++j) m = fma(TR ? E.Tmid[j] : E.Fmid[j], xo[j], m);
+        y[H] = m;
+    }
+}
+
+// traces of a line at both ends: u_lo = e0.x, u_hi = e1.x, g_lo = d0.x, g_hi = d1.x
+template <int N>
+__device__ __forceinline__ void traces(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
+                                       double& ulo, double& glo, double& uhi, double& ghi)
+{
+    constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
+    double te = 0, to = 0, qe = 0, qo = 0;
+#pragma unroll
+    for (int j = 0; j < HE; ++j) {
+        te = fma(E.Es[j], xe[j], te);
+        qe = fma(E.Ds[j], xe[j], qe);
+    }
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        to = fma(E.Ea[j], xo[j], to);
+        qo = fma(E.Da[j], xo[j], qo);
+    }
+    ulo = te + to;
+    uhi = te - to;
+    glo = qe + qo;
+    ghi = qo - qe;
+}
+
+__device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double& cr, double& ci)
+{
+    cr = fma(ar, br, -ai * bi);
+    ci = fma(ar, bi, ai * br);
+}
+
+// shared-memory layout (in doubles) of k_gen<N, AFFINE, COEFF, T1, T2>
+template <int N, bool AFFINE, bool COEFF, int T1, int T2>
+struct Lay {
+    static constexpr int N2 = N * N, N3 = N * N * N, NC = T1 * T2;
+    static constexpr int NACT = NC * N2;
+    static constexpr int NT = (NACT + 31) / 32 * 32;
+    static constexpr int NRL = T1 + T2, NRH = T1 + T2; // ring cells below / above the tile
+    static constexpr int NF = 3 * NC + NRL;            // faces evaluated by the CTA per plane
+    static constexpr int CXSZ = 2 * 3 * (N + 1) * 2;   // per cell: [coord k][axis b][q = 0..N] complex
+    static constexpr int NE = 2 * 3 * (N + 1);
+    static constexpr int NCG = NC + NRL;               // cells with geometry / c tables (own + ring below)
+    // regions
+    static constexpr int XS = 0;                                        // [2][NC][N3] own planes
+    static constexpr int RXSZ = (NRL + NRH) * N3;                       // ring blocks: bd1[T2] bd2[T1] ad1[T2] ad2[T1]
+    static constexpr int WCSZ = AFFINE ? 3 * NF * N2 : 0;               // W (2 per face point) + CG (1)
+    static constexpr int RX = XS + 2 * NC * N3;                         // ring blocks, aliased by W / CG after P1
+    static constexpr int RXEND = RX + (RXSZ > WCSZ ? RXSZ : WCSZ);
+    static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
+    static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // [2][NC][N3] grad0/1 -> Q0/1 -> R0/1
+    static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][side][u|V, gn|G][N2]
+    static constexpr int CX = TRB + NF * 4 * N2;
+    static constexpr int CO = CX + (COEFF ? NCG * CXSZ : 0);
+    static constexpr int END = CO + (COEFF ? NCG * 4 : 0);
+    static constexpr int BYTES = END * 8 + 64; // + 2 mbarriers
+    static_assert(AFFINE || true, "");
+};
+
+} // namespace gn
+
+// grid: ntiles * nchunks CTAs (chunk-major), block Lay::NT, dynamic smem Lay::BYTES
+template <int N, bool AFFINE, bool COEFF, int T1, int T2, int MINB>
+__global__ void __launch_bounds__(gn::Lay<N, AFFINE, COEFF, T1, T2>::NT, MINB)
+k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
+      int p_begin, int p_end, int chunk_len, const EOTab<N> E, const MeshArgs M, const double* __restrict__ geo)
+{
+    using Y = gn::Lay<N, AFFINE, COEFF, T1, T2>;
+    constexpr int N2 = Y::N2, N3 = Y::N3, NC = Y::NC, NT = Y::NT, NRL = Y::NRL, NRH = Y::NRH, NF = Y::NF;
+    constexpr int NCG = Y::NCG, NE = Y::NE;
+    constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
+    extern __shared__ __align__(16) double sm[];
+    double* const XS = sm + Y::XS;
+    double* const RX = sm + Y::RX;
+    double* const WB = sm + Y::RX;              // W: [NF][2][N2] (AFFINE, after P1)
+    double* const CG = sm + Y::RX + 2 * NF * N2; // CG: [NF][N2]
+    double* const GE = sm + Y::GE;
+    double* const G0 = sm + Y::G01;
+    double* const G1 = sm + Y::G01 + NC * N3;
+    double* const TRB = sm + Y::TRB;
+    double* const CX = sm + Y::CX;
+    double* const CO = sm + Y::CO;
+    uint64_t* const barA = reinterpret_cast<uint64_t*>(sm + Y::END);
+    uint64_t* const barB = barA + 1;
+    __shared__ double sXi[N + 1];
+
+    const int tid = threadIdx.x;
+    const int ntile2 = M.N2 / T2;
+    const int ntiles = (M.N1 / T1) * ntile2;
+    const int chunk = blockIdx.x / ntiles, tile = blockIdx.x % ntiles;
+    const int ti1 = tile / ntile2, ti2 = tile % ntile2;
+    {
+        const int b = p_begin + chunk * chunk_len;
+        p_end = min(p_end, b + chunk_len);
+        p_begin = b;
+    }
+    const int nsteps = p_end - p_begin;
+    if (nsteps <= 0) return;
+    const int PC = M.plane_cells;
+    auto wrap = [](int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); };
+    auto cidx = [&](int lp, int i1, int i2) -> long long { return (long long)lp * PC + (long long)i1 * M.N2 + i2; };
+    // source of plane lp's blocks (-1: halo below, L: halo above), and of its geometry records (L+2 planes from -1)
+    auto xplane = [&](int lp) -> const double* { return lp < 0 ? xb : (lp >= M.L ? xa : x + (long long)lp * PC * N3); };
+    auto grec = [&](int lp, int i1, int i2) -> const double* { return geo + (cidx(lp + 1, i1, i2)) * GREC; };
+    auto TR = [&](int f, int side, int q) -> double* { return TRB + ((f * 2 + side) * 2 + q) * N2; };
+
+    // fixed thread coordinates: cell mc of the tile, line position (ma, mb)
+    const bool act = tid < Y::NACT;
+    const int mc = act ? tid / N2 : 0, mab = act ? tid % N2 : 0, ma = mab % N, mb = mab / N;
+    const int mc1 = mc / T2, mc2 = mc % T2;
+    // TR face index of the own cell's lower faces d = 1, 2 (in-tile: upper face of the cell below)
+    const int flo1 = mc1 > 0 ? 3 * (mc - T2) + 1 : 3 * NC + mc2;
+    const int flo2 = mc2 > 0 ? 3 * (mc - 1) + 2 : 3 * NC + T2 + mc1;
+
+    if (tid < N) sXi[tid] = E.xi[tid];
+    if (tid == 0) {
+        sXi[N] = 1.0;
+        gn::mbar_init(barA, 1);
+        gn::mbar_init(barB, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // ---------------- async staging ----------------
+    constexpr uint32_t ROWB = T2 * N3 * 8;
+    auto issue_x = [&](int lp, double* dst) { // own blocks of plane lp (T1 rows) on barA (caller adds expect_tx)
+        const double* src = xplane(lp);
+#pragma unroll
+        for (int c1 = 0; c1 < T1; ++c1)
+            gn::bulk_g2s(dst + c1 * T2 * N3, src + ((long long)(ti1 * T1 + c1) * M.N2 + ti2 * T2) * N3, ROWB, barA);
+    };
+    auto issue_geo = [&](int lp, double* dst) { // records of own + ring-below cells of plane lp
+#pragma unroll
+        for (int c1 = 0; c1 < T1; ++c1) gn::bulk_g2s(dst + c1 * T2 * GREC, grec(lp, ti1 * T1 + c1, ti2 * T2), T2 * GREC * 8, barA);
+        gn::bulk_g2s(dst + NC * GREC, grec(lp, wrap(ti1 * T1 - 1, M.N1), ti2 * T2), T2 * GREC * 8, barA);
+#pragma unroll
+        for (int c1 = 0; c1 < T1; ++c1)
+            gn::bulk_g2s(dst + (NC + T2 + c1) * GREC, grec(lp, ti1 * T1 + c1, wrap(ti2 * T2 - 1, M.N2)), GREC * 8, barA);
+    };
+    constexpr uint32_t GEOB = AFFINE ? (uint32_t)(NCG * GREC * 8) : 0u;
+    // ring blocks of plane lp: rows via bulk copies on barB (thread 0), single d=2 cells via cp.async (all threads)
+    constexpr bool D2BULK = (N3 % 2) == 0;
+    auto issue_ring_bulk = [&](int lp) {
+        const double* src = x + (long long)lp * PC * N3;
+        uint32_t bytes = 2 * ROWB + (D2BULK ? 2 * T1 * N3 * 8 : 0);
+        gn::mbar_expect_tx(barB, bytes);
+        gn::bulk_g2s(RX, src + ((long long)wrap(ti1 * T1 - 1, M.N1) * M.N2 + ti2 * T2) * N3, ROWB, barB);
+        gn::bulk_g2s(RX + (T2 + T1) * N3, src + ((long long)wrap(ti1 * T1 + T1, M.N1) * M.N2 + ti2 * T2) * N3, ROWB, barB);
+        if (D2BULK) {
+#pragma unroll
+            for (int c1 = 0; c1 < T1; ++c1) {
+                const long long i1 = ti1 * T1 + c1;
+                gn::bulk_g2s(RX + (T2 + c1) * N3, src + (i1 * M.N2 + wrap(ti2 * T2 - 1, M.N2)) * N3, N3 * 8, barB);
+                gn::bulk_g2s(RX + (2 * T2 + T1 + c1) * N3, src + (i1 * M.N2 + wrap(ti2 * T2 + T2, M.N2)) * N3, N3 * 8, barB);
+            }
+        }
+    };
+    auto issue_ring_cp = [&](int lp) {
+        if (!D2BULK) {
+            const double* src = x + (long long)lp * PC * N3;
+            for (int t = tid; t < 2 * T1 * N3; t += NT) {
+                const int k = t / N3, e = t % N3, c1 = k % T1;
+                const bool above = k >= T1;
+                const long long i1 = ti1 * T1 + c1;
+                const int i2 = above ? wrap(ti2 * T2 + T2, M.N2) : wrap(ti2 * T2 - 1, M.N2);
+                double* dst = RX + ((above ? 2 * T2 + T1 : T2) + c1) * N3 + e;
+                gn::cp_async8(dst, src + (i1 * M.N2 + i2) * N3 + e);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    };
+
+    // c(x) tables of cell slot cc (own: cc < NC, ring below: NC + r) from its record / mesh h
+    auto ctab_task = [&](int cc, int rem, int g0, int i1, const double* gbuf) {
+        double sv, cv;
+        if (rem < NE) {
+            const int k = rem / (3 * (N + 1)), rem2 = rem % (3 * (N + 1)), bax = rem2 / (N + 1), q = rem2 % (N + 1);
+            const double Jkb = AFFINE ? gbuf[cc * GREC + 6 + 3 * k + bax] : (bax == k ? M.h[k] : 0.0);
+            sincospi(2.0 * Jkb * sXi[q], &sv, &cv);
+            double* e = CX + cc * Y::CXSZ + ((k * 3 + bax) * (N + 1) + q) * 2;
+            e[0] = cv;
+            e[1] = sv;
+        } else {
+            const int k = rem - NE;
+            const double o = k == 0 ? (double)g0 / M.N0 : (double)i1 / M.N1;
+            sincospi(2.0 * o, &sv, &cv);
+            CO[cc * 4 + 2 * k] = cv;
+            CO[cc * 4 + 2 * k + 1] = sv;
+        }
+    };
+    auto ctabs = [&](int lp, const double* gbuf) {
+        const int g0 = wrap(M.plane_begin + lp, M.N0);
+        for (int t = tid; t < NCG * (NE + 2); t += NT) {
+            const int cc = t / (NE + 2);
+            int i1;
+            if (cc < NC) i1 = ti1 * T1 + cc / T2;
+            else if (cc < NC + T2) i1 = wrap(ti1 * T1 - 1, M.N1);
+            else i1 = ti1 * T1 + (cc - NC - T2);
+            ctab_task(cc, t % (NE + 2), g0, i1, gbuf);
+        }
+    };
+    // c(x) at a point of cell slot cc (q indexes sXi; q = N is the face coordinate 1)
+    auto cval = [&](int cc, int q0, int q1, int q2) -> double {
+        const double* cx = CX + cc * Y::CXSZ;
+        double z[2][2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double* e0 = cx + ((k * 3 + 0) * (N + 1) + q0) * 2;
+            const double* e1 = cx + ((k * 3 + 1) * (N + 1) + q1) * 2;
+            const double* e2 = cx + ((k * 3 + 2) * (N + 1) + q2) * 2;
+            double tr, ti, ur, ui;
+            gn::cmul(CO[cc * 4 + 2 * k], CO[cc * 4 + 2 * k + 1], e0[0], e0[1], tr, ti);
+            gn::cmul(tr, ti, e1[0], e1[1], ur, ui);
+            gn::cmul(ur, ui, e2[0], e2[1], z[k][0], z[k][1]);
+        }
+        return fma(0.5 * z[0][1], z[1][0], 1.0); // 1 + 0.5 sin(2 pi x0) cos(2 pi x1) (reading R13)
+    };
+
+    // ---------------- face passes (face f, point p = (a, b)) ----------------
+    auto face_dir = [&](int f) { return f < 3 * NC ? f % 3 : (f - 3 * NC < T2 ? 1 : 2); };
+    auto face_rec = [&](int f) { return f < 3 * NC ? f / 3 : NC + (f - 3 * NC); }; // T- cell slot
+    // a-, a+ components (normal d, tangential t1, t2) of face f from its T- record
+    auto face_a = [&](const double* gb, int f, int d, double& mdn, double& mt1, double& mt2, double& pdn, double& pt1,
+                      double& pt2, double& dS) {
+        if (AFFINE) {
+            const double* fr = gb + face_rec(f) * GREC + 12 + 7 * d;
+            dS = fr[0];
+            mdn = d == 0 ? fr[1] : (d == 1 ? fr[2] : fr[3]);
+            mt1 = d == 0 ? fr[2] : fr[1];
+            mt2 = d == 2 ? fr[2] : fr[3];
+            pdn = d == 0 ? fr[4] : (d == 1 ? fr[5] : fr[6]);
+            pt1 = d == 0 ? fr[5] : fr[4];
+            pt2 = d == 2 ? fr[5] : fr[6];
+        } else {
+            const double hd = d == 0 ? M.h[0] : (d == 1 ? M.h[1] : M.h[2]);
+            mdn = pdn = 1.0 / hd;
+            mt1 = mt2 = pt1 = pt2 = 0.0;
+            dS = M.h[0] * M.h[1] * M.h[2] / hd;
+        }
+    };
+    // pass A (AFFINE): w1 = a-_t1 u- + a+_t1 u+, w2 = a-_t2 u- + a+_t2 u+
+    auto passA = [&](const double* gb, int f, int p) {
+        const int d = face_dir(f);
+        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
+        face_a(gb, f, d, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
+        WB[(f * 2 + 0) * N2 + p] = fma(mt1, um, pt1 * up);
+        WB[(f * 2 + 1) * N2 + p] = fma(mt2, um, pt2 * up);
+    };
+    // pass B: flux. AFFINE: Cv- -> TR(f,0,0), Cg -> CG. Axis: V+-, G+- directly.
+    auto passB = [&](const double* gb, int f, int p) {
+        const int d = face_dir(f), gs = face_rec(f);
+        const int a = p % N, b = p / N;
+        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
+        face_a(gb, f, d, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        double cF = 1.0;
+        if (COEFF) {
+            const int q0 = (d == 0) ? N : a, q1 = (d == 1) ? N : (d == 0 ? a : b), q2 = (d == 2) ? N : b;
+            cF = cval(gs, q0, q1, q2); // x_F on the T- cell at xi_d = 1
+        }
+        const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
+        const double gm = TR(f, 0, 1)[p], gp = TR(f, 1, 1)[p];
+        double s = fma(mdn, gm, pdn * gp);
+        if (AFFINE) {
+            const double* W1 = WB + (f * 2 + 0) * N2;
+            const double* W2 = WB + (f * 2 + 1) * N2;
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+                s = fma(E.D[a * N + m], W1[m + N * b], s);
+                s = fma(E.D[b * N + m], W2[a + N * m], s);
+            }
+        }
+        const double gam = d == 0 ? M.gamma[0] : (d == 1 ? M.gamma[1] : M.gamma[2]);
+        const double Wt = E.w[a] * E.w[b] * dS;
+        const double jump = um - up;
+        const double avg = 0.5 * cF * s;
+        const double Cvm = Wt * fma(gam, jump, -avg);
+        const double Cg = -0.5 * Wt * jump * cF;
+        if (AFFINE) {
+            TR(f, 0, 0)[p] = Cvm;
+            CG[f * N2 + p] = Cg;
+        } else {
+            TR(f, 0, 0)[p] = Cvm;
+            TR(f, 0, 1)[p] = mdn * Cg;
+            TR(f, 1, 0)[p] = -Cvm;
+            TR(f, 1, 1)[p] = pdn * Cg;
+        }
+    };
+    // pass C (AFFINE): V+- = +-Cv- + a+-_t1 (D^T_t1 Cg) + a+-_t2 (D^T_t2 Cg), G+- = a+-_d Cg
+    auto passC = [&](const double* gb, int f, int p) {
+        const int d = face_dir(f);
+        const int a = p % N, b = p / N;
+        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
+        face_a(gb, f, d, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        const double* C = CG + f * N2;
+        double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+            t1 = fma(E.D[m * N + a], C[m + N * b], t1);
+            t2 = fma(E.D[m * N + b], C[a + N * m], t2);
+        }
+        const double Cvm = TR(f, 0, 0)[p], Cg = C[p];
+        TR(f, 0, 0)[p] = fma(mt1, t1, fma(mt2, t2, Cvm));
+        TR(f, 0, 1)[p] = mdn * Cg;
+        TR(f, 1, 0)[p] = fma(pt1, t1, fma(pt2, t2, -Cvm));
+        TR(f, 1, 1)[p] = pdn * Cg;
+    };
+
+    // foreign traces: ring cells (their ends facing the tile) and the next plane's lower ends
+    constexpr int NFT = NRL + NRH + NC;
+    auto foreign = [&](const double* XN) {
+        for (int t = tid; t < NFT * N2; t += NT) {
+            const int rc = t / N2, p = t % N2, a = p % N, b = p / N;
+            const double* blk;
+            int d, f, side;
+            if (rc < T2) { blk = RX + rc * N3; d = 1; f = 3 * NC + rc; side = 0; }
+            else if (rc < T2 + T1) { blk = RX + rc * N3; d = 2; f = 3 * NC + rc; side = 0; }
+            else if (rc < 2 * T2 + T1) { const int q = rc - T2 - T1; blk = RX + rc * N3; d = 1; f = 3 * ((T1 - 1) * T2 + q) + 1; side = 1; }
+            else if (rc < NRL + NRH) { const int q = rc - 2 * T2 - T1; blk = RX + rc * N3; d = 2; f = 3 * (q * T2 + T2 - 1) + 2; side = 1; }
+            else { const int q = rc - NRL - NRH; blk = XN + q * N3; d = 0; f = 3 * q; side = 1; }
+            double v[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) v[j] = blk[pidx<N>(d, j, a, b)];
+            double xe[HE], xo[H > 0 ? H : 1];
+            gn::split<N>(v, xe, xo);
+            double ulo, glo, uhi, ghi;
+            gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
+            TR(f, side, 0)[p] = side ? ulo : uhi; // T- (ring below) faces the tile with its upper end
+            TR(f, side, 1)[p] = side ? glo : ghi;
+        }
+    };
+
+    // ---------------- prologue: the lower d=0 face of plane p_begin (T- = plane p_begin - 1) ----------------
+    double pendV = 0.0, pendG = 0.0; // T+ half of the d=0 face below the thread's line (a, b) of cell mc
+    {
+        if (tid == 0) {
+            gn::mbar_expect_tx(barA, 2 * T1 * ROWB + GEOB);
+            issue_x(p_begin - 1, XS + NC * N3);
+            issue_x(p_begin, XS);
+            if (AFFINE) issue_geo(p_begin - 1, GE + NCG * GREC);
+        }
+        gn::mbar_wait(barA, 0);
+        if (COEFF) ctabs(p_begin - 1, GE + NCG * GREC);
+        // T- upper-end traces (plane p_begin - 1) -> TR(3c, 0), T+ lower-end traces (plane p_begin) -> TR(3c, 1)
+        for (int t = tid; t < 2 * NC * N2; t += NT) {
+            const int which = t / (NC * N2), rem = t % (NC * N2), c = rem / N2, p = rem % N2;
+            const double* blk = (which ? XS : XS + NC * N3) + c * N3;
+            double v[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) v[j] = blk[pidx<N>(0, j, p % N, p / N)];
+            double xe[HE], xo[H > 0 ? H : 1];
+            gn::split<N>(v, xe, xo);
+            double ulo, glo, uhi, ghi;
+            gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
+            TR(3 * c, which, 0)[p] = which ? ulo : uhi;
+            TR(3 * c, which, 1)[p] = which ? glo : ghi;
+        }
+        __syncthreads();
+        const double* gb = GE + NCG * GREC;
+        if (AFFINE) {
+            for (int t = tid; t < NC * N2; t += NT) passA(gb, 3 * (t / N2), t % N2);
+            __syncthreads();
+        }
+        for (int t = tid; t < NC * N2; t += NT) passB(gb, 3 * (t / N2), t % N2);
+        __syncthreads();
+        if (AFFINE) {
+            for (int t = tid; t < NC * N2; t += NT) passC(gb, 3 * (t / N2), t % N2);
+            __syncthreads();
+        }
+        if (act) {
+            pendV = TR(3 * mc, 1, 0)[mab];
+            pendG = TR(3 * mc, 1, 1)[mab];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
+            issue_x(p_begin + 1, XS + NC * N3);
+            if (AFFINE) issue_geo(p_begin, GE);
+            issue_ring_bulk(p_begin);
+        }
+        issue_ring_cp(p_begin);
+    }
+
+    for (int s = 0; s < nsteps; ++s) {
+        const int lp = p_begin + s;
+        const double* XC = XS + (s & 1) * NC * N3;     // own plane lp
+        const double* XN = XS + ((s + 1) & 1) * NC * N3; // next plane lp + 1
+        const double* gb = GE + (s & 1) * NCG * GREC;
+        gn::mbar_wait(barA, (s + 1) & 1);
+        gn::mbar_wait(barB, s & 1);
+        if (!D2BULK) gn::cp_async_wait_all();
+        __syncthreads();
+
+        // ---------------- P1: stage 1 + own traces; foreign traces; c(x) tables ----------------
+        double g2[N];
+        if (act) {
+            const double* xc = XC + mc * N3;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                double v[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) v[j] = xc[pidx<N>(d, j, ma, mb)];
+                double xe[HE], xo[H > 0 ? H : 1];
+                gn::split<N>(v, xe, xo);
+                double ulo, glo, uhi, ghi;
+                gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
+                double y[N];
+                gn::sweep<N, false, false>(E, xe, xo, y);
+                TR(3 * mc + d, 0, 0)[mab] = uhi;
+                TR(3 * mc + d, 0, 1)[mab] = ghi;
+                if (d == 0) {
+#pragma unroll
+                    for (int j = 0; j < N; ++j) G0[mc * N3 + pidx<N>(0, j, ma, mb)] = y[j];
+                } else if (d == 1) {
+#pragma unroll
+                    for (int j = 0; j < N; ++j) G1[mc * N3 + pidx<N>(1, j, ma, mb)] = y[j];
+                    TR(flo1, 1, 0)[mab] = ulo;
+                    TR(flo1, 1, 1)[mab] = glo;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < N; ++j) g2[j] = y[j];
+                    TR(flo2, 1, 0)[mab] = ulo;
+                    TR(flo2, 1, 1)[mab] = glo;
+                }
+            }
+        }
+        foreign(XN);
+        if (COEFF) ctabs(lp, gb);
+        __syncthreads();
+
+        // stream the next step's own blocks (plane lp + 2) and geometry (plane lp + 1) behind the compute
+        if (tid == 0 && s + 1 < nsteps) {
+            gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
+            issue_x(lp + 2, XS + (s & 1) * NC * N3);
+            if (AFFINE) issue_geo(lp + 1, GE + ((s + 1) & 1) * NCG * GREC);
+        }
+
+        // ---------------- P2: stage 2 at the thread's d=2 line points (a, b, q); face pass A ----------------
+        double q2[N];
+        if (act) {
+            double gt[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) gt[i] = AFFINE ? gb[mc * GREC + i] : 0.0;
+            double z0r = 0, z0i = 0, z1r = 0, z1i = 0;
+            if (COEFF) {
+                const double* cx = CX + mc * Y::CXSZ;
+                double tr, ti;
+                gn::cmul(CO[mc * 4 + 0], CO[mc * 4 + 1], cx[((0 * 3 + 0) * (N + 1) + ma) * 2], cx[((0 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
+                gn::cmul(tr, ti, cx[((0 * 3 + 1) * (N + 1) + mb) * 2], cx[((0 * 3 + 1) * (N + 1) + mb) * 2 + 1], z0r, z0i);
+                gn::cmul(CO[mc * 4 + 2], CO[mc * 4 + 3], cx[((1 * 3 + 0) * (N + 1) + ma) * 2], cx[((1 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
+                gn::cmul(tr, ti, cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
+            }
+            const double wab = E.w[ma] * E.w[mb];
+            double* g0 = G0 + mc * N3;
+            double* g1 = G1 + mc * N3;
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                const int P = mab + N2 * q;
+                double cW = wab * E.w[q];
+                if (COEFF) {
+                    const double* cx = CX + mc * Y::CXSZ;
+                    const double* e0 = cx + ((0 * 3 + 2) * (N + 1) + q) * 2;
+                    const double* e1 = cx + ((1 * 3 + 2) * (N + 1) + q) * 2;
+                    const double s0 = fma(z0r, e0[1], z0i * e0[0]);  // Im(z0 e0) = sin(2 pi x0)
+                    const double c1 = fma(z1r, e1[0], -z1i * e1[1]); // Re(z1 e1) = cos(2 pi x1)
+                    cW *= fma(0.5 * s0, c1, 1.0);
+                }
+                const double a0 = g0[P], a1 = g1[P], a2 = g2[q];
+                if (AFFINE) {
+                    g0[P] = cW * fma(gt[0], a0, fma(gt[3], a1, gt[4] * a2));
+                    g1[P] = cW * fma(gt[3], a0, fma(gt[1], a1, gt[5] * a2));
+                    q2[q] = cW * fma(gt[4], a0, fma(gt[5], a1, gt[2] * a2));
+                } else {
+                    const double adet = M.h[0] * M.h[1] * M.h[2];
+                    g0[P] = cW * (adet / (M.h[0] * M.h[0])) * a0;
+                    g1[P] = cW * (adet / (M.h[1] * M.h[1])) * a1;
+                    q2[q] = cW * (adet / (M.h[2] * M.h[2])) * a2;
+                }
+            }
+        }
+        if (AFFINE) {
+            for (int t = tid; t < NF * N2; t += NT) passA(gb, t / N2, t % N2);
+            __syncthreads();
+        }
+        // ---------------- P3: face pass B (flux) ----------------
+        for (int t = tid; t < NF * N2; t += NT) passB(gb, t / N2, t % N2);
+        __syncthreads();
+        // ---------------- P4: face pass C (tangential back-projection) ----------------
+        if (AFFINE) {
+            for (int t = tid; t < NF * N2; t += NT) passC(gb, t / N2, t % N2);
+            __syncthreads();
+        }
+        // the ring buffer (aliased by W / CG) is free: stream the next plane's ring blocks
+        if (s + 1 < nsteps) {
+            if (tid == 0) issue_ring_bulk(lp + 1);
+            issue_ring_cp(lp + 1);
+        }
+
+        // ---------------- P5: stage 3 + face back-projection; d = 0, 1 in place, d = 2 -> r ----------------
+        if (act) {
+            {
+                double* qd = G0 + mc * N3;
+                double v[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) v[j] = qd[pidx<N>(0, j, ma, mb)];
+                double xe[HE], xo[H > 0 ? H : 1];
+                gn::split<N>(v, xe, xo);
+                double y[N];
+                gn::sweep<N, true, true>(E, xe, xo, y, pendV, pendG, TR(3 * mc, 0, 0)[mab], TR(3 * mc, 0, 1)[mab]);
+#pragma unroll
+                for (int j = 0; j < N; ++j) qd[pidx<N>(0, j, ma, mb)] = y[j];
+                pendV = TR(3 * mc, 1, 0)[mab]; // the T+ half of this face is the next plane's lower face
+                pendG = TR(3 * mc, 1, 1)[mab];
+            }
+            {
+                double* qd = G1 + mc * N3;
+                double v[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) v[j] = qd[pidx<N>(1, j, ma, mb)];
+                double xe[HE], xo[H > 0 ? H : 1];
+                gn::split<N>(v, xe, xo);
+                double y[N];
+                gn::sweep<N, true, true>(E, xe, xo, y, TR(flo1, 1, 0)[mab], TR(flo1, 1, 1)[mab], TR(3 * mc + 1, 0, 0)[mab],
+                                         TR(3 * mc + 1, 0, 1)[mab]);
+#pragma unroll
+                for (int j = 0; j < N; ++j) qd[pidx<N>(1, j, ma, mb)] = y[j];
+            }
+        }
+        __syncthreads();
+        if (act) {
+            double xe[HE], xo[H > 0 ? H : 1];
+            gn::split<N>(q2, xe, xo);
+            double y[N];
+            gn::sweep<N, true, true>(E, xe, xo, y, TR(flo2, 1, 0)[mab], TR(flo2, 1, 1)[mab], TR(3 * mc + 2, 0, 0)[mab],
+                                     TR(3 * mc + 2, 0, 1)[mab]);
+            const double* r0 = G0 + mc * N3;
+            const double* r1 = G1 + mc * N3;
+            double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const int P = pidx<N>(2, j, ma, mb);
+                dst[P] = y[j] + r0[P] + r1[P];
+            }
+        }
+        // (the barrier at the top of the next step orders these reads before the next writes)
+    }
+}
+
+} // namespace dg

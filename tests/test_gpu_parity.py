@@ -222,3 +222,91 @@ def test_axis8_slab_loopback_bitwise(world):
         op.close()
     assert torch.equal(got, ref)
     full.close()
+
+
+# k_gen tile shapes (dg_capi.cu GenShape): n -> (T1, T2)
+GEN_TILE = {2: (4, 4), 3: (2, 4), 4: (2, 4), 5: (2, 2), 6: (2, 2), 7: (2, 2), 8: (2, 2)}
+
+
+@pytest.mark.parametrize("k", range(1, 8))
+@pytest.mark.parametrize("geom,coeff", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gen_all_degrees(k, geom, coeff):
+    """k_gen (marching tiles with async staging) for every degree and geometry/coefficient
+    combination, on meshes of 1 and 2-3 tiles per direction (ring cells wrapping onto the tile
+    itself), against the oracle."""
+    T1, T2 = GEN_TILE[k + 1]
+    N = (3, T1, 3 * T2) if k % 2 else (4, 2 * T1, T2)
+    if k == 7 and geom == 0 and coeff == 0:
+        pytest.skip("axis-aligned Q7 runs k_axis8")
+    w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=200 + k)
+    op = _op(w)
+    assert op.kernel_name == "k_gen"
+    op.close()
+    assert _full_check(w) <= TOL
+
+
+@pytest.mark.parametrize("k,geom,coeff", [(4, 1, 1), (5, 1, 1), (3, 0, 0), (2, 1, 0)])
+def test_gen_chunks(k, geom, coeff, monkeypatch):
+    """Plane chunks (DG_GEN_CHUNK) with a ragged last chunk: each chunk re-evaluates the face
+    below its first plane (prologue); the result is identical to one chunk per tile column."""
+    T1, T2 = GEN_TILE[k + 1]
+    w = synth.small(k, (7, 2 * T1, 2 * T2), geom_kind=geom, coeff_kind=coeff, seed=300 + k)
+    x = synth.x_torch(w, device="cuda")
+    monkeypatch.setenv("DG_GEN_CHUNK", "3")
+    a = _op(w)
+    monkeypatch.setenv("DG_GEN_CHUNK", "0")
+    b = _op(w)
+    ra, rb = a.apply(x), b.apply(x)
+    assert a.kernel_name == b.kernel_name == "k_gen"
+    assert (ra - rb).abs().max().item() <= 1e-14 * rb.abs().max().item()
+    a.close()
+    b.close()
+    assert _full_check(w) <= TOL
+
+
+@pytest.mark.parametrize("k", [2, 4, 5])
+def test_gen_matches_cell_kernel(k, monkeypatch):
+    """k_gen against the plain cell-centric kernel (k_cell_general) on an affine c(x) mesh."""
+    T1, T2 = GEN_TILE[k + 1]
+    w = synth.small(k, (4, 2 * T1, 2 * T2), geom_kind=1, coeff_kind=1, seed=400 + k)
+    x = synth.x_torch(w, device="cuda")
+    g = _op(w)
+    monkeypatch.setenv("DG_FORCE_GENERAL", "1")
+    c = _op(w)
+    assert g.kernel_name == "k_gen" and c.kernel_name == "k_cell_general"
+    a, b = g.apply(x), c.apply(x)
+    assert (a - b).abs().max().item() <= 1e-13 * b.abs().max().item()
+    g.close()
+    c.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gen_slab_loopback_bitwise(world):
+    """k_gen in the slab decomposition (halo planes from the neighbours, interior/boundary split)
+    is bitwise equal to the whole-mesh apply."""
+    from paper_1812_08075_b200 import Operator, slab
+    w = synth.small(4, (6, 4, 4), geom_kind=1, coeff_kind=1, seed=41)
+    full = _op(w)
+    assert full.kernel_name == "k_gen"
+    x = synth.x_torch(w, device="cuda")
+    ref = full.apply(x)
+    pd = full.plane_ndofs
+    got = torch.full_like(x, float("nan"))
+    for q in range(world):
+        p = slab.plan(w.N[0], q, world)
+        jac = synth.jac_planes_torch(w, p.plane_begin - 1, p.nplanes + 2).numpy()
+        op = Operator(w.N, w.k, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind, penalty_scale=w.penalty_scale,
+                      jac=jac, plane_begin=p.plane_begin, nplanes=p.nplanes)
+        xs = x[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        rs = got[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        hb = x[((p.plane_begin - 1) % w.N[0]) * pd:][:pd].clone()
+        ha = x[((p.plane_begin + p.nplanes) % w.N[0]) * pd:][:pd].clone()
+        a, b = p.interior
+        if b > a:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        for a, b in p.boundary:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        torch.cuda.synchronize()
+        op.close()
+    assert torch.equal(got, ref)
+    full.close()
