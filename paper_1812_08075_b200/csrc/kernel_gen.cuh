@@ -24,6 +24,8 @@
 //    fewer); direction 2 stays in registers from stage 1 to stage 3.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernel_tile.cuh" // k_geom / GREC records, tl:: mbarrier + bulk-copy helpers
 
@@ -181,7 +183,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     double* const CO = sm + Y::CO;
     uint64_t* const barA = reinterpret_cast<uint64_t*>(sm + Y::END);
     uint64_t* const barB = barA + 1;
-    __shared__ double sXi[N + 1];
+    __shared__ double sXi[N + 1], sD[N * N], sW[N];
 
     const int tid = threadIdx.x;
     const int ntile2 = M.N2 / T2;
@@ -211,7 +213,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     const int flo1 = mc1 > 0 ? 3 * (mc - T2) + 1 : 3 * NC + mc2;
     const int flo2 = mc2 > 0 ? 3 * (mc - 1) + 2 : 3 * NC + T2 + mc1;
 
-    if (tid < N) sXi[tid] = E.xi[tid];
+    if (tid < N) { sXi[tid] = E.xi[tid]; sW[tid] = E.w[tid]; }
+    for (int i = tid; i < N * N; i += NT) sD[i] = E.D[i];
     if (tid == 0) {
         sXi[N] = 1.0;
         gn::mbar_init(barA, 1);
@@ -315,65 +318,65 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         return fma(0.5 * z[0][1], z[1][0], 1.0); // 1 + 0.5 sin(2 pi x0) cos(2 pi x1) (reading R13)
     };
 
-    // ---------------- face passes (face f, point p = (a, b)) ----------------
-    auto face_dir = [&](int f) { return f < 3 * NC ? f % 3 : (f - 3 * NC < T2 ? 1 : 2); };
-    auto face_rec = [&](int f) { return f < 3 * NC ? f / 3 : NC + (f - 3 * NC); }; // T- cell slot
+    // ---------------- face passes (face f with normal DC, point p = (a, b)) ----------------
+    // the T- record slot of face f: own upper faces 3c + d -> c, tile-boundary faces 3 NC + r -> NC + r
+    auto face_rec = [&](int f) { return f < 3 * NC ? f / 3 : NC + (f - 3 * NC); };
     // a-, a+ components (normal d, tangential t1, t2) of face f from its T- record
-    auto face_a = [&](const double* gb, int f, int d, double& mdn, double& mt1, double& mt2, double& pdn, double& pt1,
+    auto face_a = [&](auto DC, const double* gb, int f, double& mdn, double& mt1, double& mt2, double& pdn, double& pt1,
                       double& pt2, double& dS) {
+        constexpr int d = decltype(DC)::value;
         if (AFFINE) {
             const double* fr = gb + face_rec(f) * GREC + 12 + 7 * d;
             dS = fr[0];
-            mdn = d == 0 ? fr[1] : (d == 1 ? fr[2] : fr[3]);
-            mt1 = d == 0 ? fr[2] : fr[1];
-            mt2 = d == 2 ? fr[2] : fr[3];
-            pdn = d == 0 ? fr[4] : (d == 1 ? fr[5] : fr[6]);
-            pt1 = d == 0 ? fr[5] : fr[4];
-            pt2 = d == 2 ? fr[5] : fr[6];
+            mdn = fr[1 + d];
+            mt1 = fr[d == 0 ? 2 : 1];
+            mt2 = fr[d == 2 ? 2 : 3];
+            pdn = fr[4 + d];
+            pt1 = fr[d == 0 ? 5 : 4];
+            pt2 = fr[d == 2 ? 5 : 6];
         } else {
-            const double hd = d == 0 ? M.h[0] : (d == 1 ? M.h[1] : M.h[2]);
-            mdn = pdn = 1.0 / hd;
+            mdn = pdn = 1.0 / M.h[d];
             mt1 = mt2 = pt1 = pt2 = 0.0;
-            dS = M.h[0] * M.h[1] * M.h[2] / hd;
+            dS = M.h[(d + 1) % 3] * M.h[(d + 2) % 3];
         }
     };
     // pass A (AFFINE): w1 = a-_t1 u- + a+_t1 u+, w2 = a-_t2 u- + a+_t2 u+
-    auto passA = [&](const double* gb, int f, int p) {
-        const int d = face_dir(f);
+    auto passA = [&](auto DC, const double* gb, int f, int p) {
         double mdn, mt1, mt2, pdn, pt1, pt2, dS;
-        face_a(gb, f, d, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        face_a(DC, gb, f, mdn, mt1, mt2, pdn, pt1, pt2, dS);
         const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
         WB[(f * 2 + 0) * N2 + p] = fma(mt1, um, pt1 * up);
         WB[(f * 2 + 1) * N2 + p] = fma(mt2, um, pt2 * up);
     };
     // pass B: flux. AFFINE: Cv- -> TR(f,0,0), Cg -> CG. Axis: V+-, G+- directly.
-    auto passB = [&](const double* gb, int f, int p) {
-        const int d = face_dir(f), gs = face_rec(f);
+    auto passB = [&](auto DC, const double* gb, int f, int p) {
+        constexpr int d = decltype(DC)::value;
         const int a = p % N, b = p / N;
         double mdn, mt1, mt2, pdn, pt1, pt2, dS;
-        face_a(gb, f, d, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        face_a(DC, gb, f, mdn, mt1, mt2, pdn, pt1, pt2, dS);
         double cF = 1.0;
         if (COEFF) {
             const int q0 = (d == 0) ? N : a, q1 = (d == 1) ? N : (d == 0 ? a : b), q2 = (d == 2) ? N : b;
-            cF = cval(gs, q0, q1, q2); // x_F on the T- cell at xi_d = 1
+            cF = cval(face_rec(f), q0, q1, q2); // x_F on the T- cell at xi_d = 1
         }
         const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
         const double gm = TR(f, 0, 1)[p], gp = TR(f, 1, 1)[p];
         double s = fma(mdn, gm, pdn * gp);
         if (AFFINE) {
-            const double* W1 = WB + (f * 2 + 0) * N2;
-            const double* W2 = WB + (f * 2 + 1) * N2;
+            const double* W1 = WB + (f * 2 + 0) * N2 + N * b;
+            const double* W2 = WB + (f * 2 + 1) * N2 + a;
+            const double* Da = sD + a * N;
+            const double* Db = sD + b * N;
 #pragma unroll
             for (int m = 0; m < N; ++m) {
-                s = fma(E.D[a * N + m], W1[m + N * b], s);
-                s = fma(E.D[b * N + m], W2[a + N * m], s);
+                s = fma(Da[m], W1[m], s);
+                s = fma(Db[m], W2[N * m], s);
             }
         }
-        const double gam = d == 0 ? M.gamma[0] : (d == 1 ? M.gamma[1] : M.gamma[2]);
-        const double Wt = E.w[a] * E.w[b] * dS;
+        const double Wt = sW[a] * sW[b] * dS;
         const double jump = um - up;
         const double avg = 0.5 * cF * s;
-        const double Cvm = Wt * fma(gam, jump, -avg);
+        const double Cvm = Wt * fma(M.gamma[d], jump, -avg);
         const double Cg = -0.5 * Wt * jump * cF;
         if (AFFINE) {
             TR(f, 0, 0)[p] = Cvm;
@@ -386,46 +389,67 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
     };
     // pass C (AFFINE): V+- = +-Cv- + a+-_t1 (D^T_t1 Cg) + a+-_t2 (D^T_t2 Cg), G+- = a+-_d Cg
-    auto passC = [&](const double* gb, int f, int p) {
-        const int d = face_dir(f);
+    auto passC = [&](auto DC, const double* gb, int f, int p) {
         const int a = p % N, b = p / N;
         double mdn, mt1, mt2, pdn, pt1, pt2, dS;
-        face_a(gb, f, d, mdn, mt1, mt2, pdn, pt1, pt2, dS);
-        const double* C = CG + f * N2;
+        face_a(DC, gb, f, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        const double* C1 = CG + f * N2 + N * b;
+        const double* C2 = CG + f * N2 + a;
         double t1 = 0.0, t2 = 0.0;
 #pragma unroll
         for (int m = 0; m < N; ++m) {
-            t1 = fma(E.D[m * N + a], C[m + N * b], t1);
-            t2 = fma(E.D[m * N + b], C[a + N * m], t2);
+            t1 = fma(sD[m * N + a], C1[m], t1);
+            t2 = fma(sD[m * N + b], C2[N * m], t2);
         }
-        const double Cvm = TR(f, 0, 0)[p], Cg = C[p];
+        const double Cvm = TR(f, 0, 0)[p], Cg = CG[f * N2 + p];
         TR(f, 0, 0)[p] = fma(mt1, t1, fma(mt2, t2, Cvm));
         TR(f, 0, 1)[p] = mdn * Cg;
         TR(f, 1, 0)[p] = fma(pt1, t1, fma(pt2, t2, -Cvm));
         TR(f, 1, 1)[p] = pdn * Cg;
     };
+    // all faces of the plane step: the thread's 3 upper faces (fixed point) + the tile-boundary lower faces
+    auto all_faces = [&](auto pass, const double* gb) {
+        if (act) {
+            pass(std::integral_constant<int, 0>{}, gb, 3 * mc + 0, mab);
+            pass(std::integral_constant<int, 1>{}, gb, 3 * mc + 1, mab);
+            pass(std::integral_constant<int, 2>{}, gb, 3 * mc + 2, mab);
+        }
+        for (int t = tid; t < NRL * N2; t += NT) {
+            const int rr = t / N2, p = t - rr * N2;
+            if (rr < T2) pass(std::integral_constant<int, 1>{}, gb, 3 * NC + rr, p);
+            else pass(std::integral_constant<int, 2>{}, gb, 3 * NC + rr, p);
+        }
+    };
 
-    // foreign traces: ring cells (their ends facing the tile) and the next plane's lower ends
-    constexpr int NFT = NRL + NRH + NC;
-    auto foreign = [&](const double* XN) {
-        for (int t = tid; t < NFT * N2; t += NT) {
-            const int rc = t / N2, p = t % N2, a = p % N, b = p / N;
-            const double* blk;
-            int d, f, side;
-            if (rc < T2) { blk = RX + rc * N3; d = 1; f = 3 * NC + rc; side = 0; }
-            else if (rc < T2 + T1) { blk = RX + rc * N3; d = 2; f = 3 * NC + rc; side = 0; }
-            else if (rc < 2 * T2 + T1) { const int q = rc - T2 - T1; blk = RX + rc * N3; d = 1; f = 3 * ((T1 - 1) * T2 + q) + 1; side = 1; }
-            else if (rc < NRL + NRH) { const int q = rc - 2 * T2 - T1; blk = RX + rc * N3; d = 2; f = 3 * (q * T2 + T2 - 1) + 2; side = 1; }
-            else { const int q = rc - NRL - NRH; blk = XN + q * N3; d = 0; f = 3 * q; side = 1; }
-            double v[N];
+    // foreign traces: ring cells (their ends facing the tile) and the next plane's lower ends,
+    // grouped by line direction (d = 1: rings along i1, d = 2: rings along i2, d = 0: next plane)
+    auto trace_task = [&](auto DC, const double* blk, int p, int f, int side) {
+        constexpr int d = decltype(DC)::value;
+        const int a = p % N, b = p / N;
+        double v[N];
 #pragma unroll
-            for (int j = 0; j < N; ++j) v[j] = blk[pidx<N>(d, j, a, b)];
-            double xe[HE], xo[H > 0 ? H : 1];
-            gn::split<N>(v, xe, xo);
-            double ulo, glo, uhi, ghi;
-            gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
-            TR(f, side, 0)[p] = side ? ulo : uhi; // T- (ring below) faces the tile with its upper end
-            TR(f, side, 1)[p] = side ? glo : ghi;
+        for (int j = 0; j < N; ++j) v[j] = blk[pidx<N>(d, j, a, b)];
+        double xe[HE], xo[H > 0 ? H : 1];
+        gn::split<N>(v, xe, xo);
+        double ulo, glo, uhi, ghi;
+        gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
+        TR(f, side, 0)[p] = side ? ulo : uhi; // T- (ring below) faces the tile with its upper end
+        TR(f, side, 1)[p] = side ? glo : ghi;
+    };
+    auto foreign = [&](const double* XN) {
+        for (int t = tid; t < 2 * T2 * N2; t += NT) {
+            const int k = t / N2, p = t - k * N2;
+            if (k < T2) trace_task(std::integral_constant<int, 1>{}, RX + k * N3, p, 3 * NC + k, 0);
+            else trace_task(std::integral_constant<int, 1>{}, RX + (T1 + k) * N3, p, 3 * ((T1 - 1) * T2 + k - T2) + 1, 1);
+        }
+        for (int t = tid; t < 2 * T1 * N2; t += NT) {
+            const int k = t / N2, p = t - k * N2;
+            if (k < T1) trace_task(std::integral_constant<int, 2>{}, RX + (T2 + k) * N3, p, 3 * NC + T2 + k, 0);
+            else trace_task(std::integral_constant<int, 2>{}, RX + (2 * T2 + k) * N3, p, 3 * ((k - T1) * T2 + T2 - 1) + 2, 1);
+        }
+        for (int t = tid; t < NC * N2; t += NT) {
+            const int q = t / N2, p = t - q * N2;
+            trace_task(std::integral_constant<int, 0>{}, XN + q * N3, p, 3 * q, 1);
         }
     };
 
@@ -441,29 +465,21 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         gn::mbar_wait(barA, 0);
         if (COEFF) ctabs(p_begin - 1, GE + NCG * GREC);
         // T- upper-end traces (plane p_begin - 1) -> TR(3c, 0), T+ lower-end traces (plane p_begin) -> TR(3c, 1)
-        for (int t = tid; t < 2 * NC * N2; t += NT) {
-            const int which = t / (NC * N2), rem = t % (NC * N2), c = rem / N2, p = rem % N2;
-            const double* blk = (which ? XS : XS + NC * N3) + c * N3;
-            double v[N];
-#pragma unroll
-            for (int j = 0; j < N; ++j) v[j] = blk[pidx<N>(0, j, p % N, p / N)];
-            double xe[HE], xo[H > 0 ? H : 1];
-            gn::split<N>(v, xe, xo);
-            double ulo, glo, uhi, ghi;
-            gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
-            TR(3 * c, which, 0)[p] = which ? ulo : uhi;
-            TR(3 * c, which, 1)[p] = which ? glo : ghi;
+        for (int t = tid; t < NC * N2; t += NT) {
+            const int c = t / N2, p = t - c * N2;
+            trace_task(std::integral_constant<int, 0>{}, XS + NC * N3 + c * N3, p, 3 * c, 0);
+            trace_task(std::integral_constant<int, 0>{}, XS + c * N3, p, 3 * c, 1);
         }
         __syncthreads();
         const double* gb = GE + NCG * GREC;
         if (AFFINE) {
-            for (int t = tid; t < NC * N2; t += NT) passA(gb, 3 * (t / N2), t % N2);
+            if (act) passA(std::integral_constant<int, 0>{}, gb, 3 * mc, mab);
             __syncthreads();
         }
-        for (int t = tid; t < NC * N2; t += NT) passB(gb, 3 * (t / N2), t % N2);
+        if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab);
         __syncthreads();
         if (AFFINE) {
-            for (int t = tid; t < NC * N2; t += NT) passC(gb, 3 * (t / N2), t % N2);
+            if (act) passC(std::integral_constant<int, 0>{}, gb, 3 * mc, mab);
             __syncthreads();
         }
         if (act) {
@@ -549,7 +565,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 gn::cmul(CO[mc * 4 + 2], CO[mc * 4 + 3], cx[((1 * 3 + 0) * (N + 1) + ma) * 2], cx[((1 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
                 gn::cmul(tr, ti, cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
             }
-            const double wab = E.w[ma] * E.w[mb];
+            const double wab = sW[ma] * sW[mb];
             double* g0 = G0 + mc * N3;
             double* g1 = G1 + mc * N3;
 #pragma unroll
@@ -578,15 +594,15 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             }
         }
         if (AFFINE) {
-            for (int t = tid; t < NF * N2; t += NT) passA(gb, t / N2, t % N2);
+            all_faces(passA, gb);
             __syncthreads();
         }
         // ---------------- P3: face pass B (flux) ----------------
-        for (int t = tid; t < NF * N2; t += NT) passB(gb, t / N2, t % N2);
+        all_faces(passB, gb);
         __syncthreads();
         // ---------------- P4: face pass C (tangential back-projection) ----------------
         if (AFFINE) {
-            for (int t = tid; t < NF * N2; t += NT) passC(gb, t / N2, t % N2);
+            all_faces(passC, gb);
             __syncthreads();
         }
         // the ring buffer (aliased by W / CG) is free: stream the next plane's ring blocks
