@@ -165,11 +165,12 @@ template <> struct GenShape<7> { static constexpr int T1 = 2, T2 = 2, MINB = 1; 
 template <> struct GenShape<8> { static constexpr int T1 = 2, T2 = 2, MINB = 1; };
 
 using GenFn = cudaError_t (*)(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                              double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo);
+                              double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo,
+                              const double* ctab);
 
 template <int N, bool AFF, bool COEF>
 cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                       double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo)
+                       double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo, const double* ctab)
 {
     constexpr int T1 = GenShape<N>::T1, T2 = GenShape<N>::T2, MB = GenShape<N>::MINB;
     using Y = dg::gn::Lay<N, AFF, COEF, T1, T2>;
@@ -178,7 +179,7 @@ cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, 
     const int CL = chunk > 0 && chunk < np ? chunk : np;
     const unsigned grid = (unsigned)((M.N1 / T1) * (M.N2 / T2) * ((np + CL - 1) / CL));
     dg::k_gen<N, AFF, COEF, T1, T2, MB><<<grid, Y::NT, Y::BYTES, st>>>(
-        x, xb, xa, r, p0, p1, CL, *static_cast<const dg::EOTab<N>*>(eot), M, geo);
+        x, xb, xa, r, p0, p1, CL, *static_cast<const dg::EOTab<N>*>(eot), M, geo, ctab);
     return cudaGetLastError();
 }
 
@@ -371,7 +372,8 @@ struct dg_ctx {
     const double* tmap_ptr;
     long long* dbg; // DG_TRACE: device buffer of per-phase clock64 stamps (k_axis8)
     double* d_jac;
-    double* d_geo; // k_tile geometry records (affine)
+    double* d_geo;  // k_tile / k_gen geometry records (affine)
+    double* d_ctab; // k_gen c(x) factor tables (coefficient c(x))
     // host-pipeline state (dg_apply_host)
     double* hx_d;
     double* hr_d;
@@ -410,7 +412,7 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         }
         return cudaGetLastError();
     }
-    if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo);
+    if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo, c->d_ctab);
     if (c->tile) return c->tinfo.fn(c->tab, c->M, x, xb, xa, r, p0, p1, st, c->d_geo);
     const long long pc = c->M.plane_cells;
     return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
@@ -530,6 +532,31 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
                 if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_geo); c->d_geo = nullptr; c->tile = c->gen = false; }
             }
         }
+        if (c->gen && mesh->coeff_kind == DG_COEFF_SINCOS) {
+            // per-cell c(x) factor tables for k_gen (k_ctab, once)
+            const long long nc = (long long)M.plane_cells * (M.L + 2);
+            const long long nen = 2LL * 3 * (n + 1);
+            cudaError_t e = cudaMalloc(&c->d_ctab, sizeof(double) * 2 * nen * (size_t)nc);
+            if (e != cudaSuccess) {
+                c->gen = false;
+            } else {
+                dg::XiTab X;
+                for (int i = 0; i < 9; ++i) X.xi[i] = i < n ? H.xi[i] : 1.0;
+                X.xi[n] = 1.0;
+                const long long tot = nc * nen;
+                const unsigned g = (unsigned)((tot + 255) / 256);
+                switch (n) {
+                case 2: dg::k_ctab<2><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                case 3: dg::k_ctab<3><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                case 4: dg::k_ctab<4><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                case 5: dg::k_ctab<5><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                case 6: dg::k_ctab<6><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                case 7: dg::k_ctab<7><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                case 8: dg::k_ctab<8><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+                }
+                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_ctab); c->d_ctab = nullptr; c->gen = false; }
+            }
+        }
         if (c->tile) c->kname = "k_tile";
         if (c->gen) c->kname = "k_gen";
     }
@@ -578,6 +605,7 @@ int dg_destroy(dg_ctx* c)
     cudaSetDevice(c->device);
     if (c->d_jac) cudaFree(c->d_jac);
     if (c->d_geo) cudaFree(c->d_geo);
+    if (c->d_ctab) cudaFree(c->d_ctab);
     if (c->dbg) {
         // DG_TRACE: dump the stamps of the last launch
         static long long h[1024 * 16 * 8];

@@ -140,7 +140,6 @@ struct Lay {
     static constexpr int NRL = T1 + T2, NRH = T1 + T2; // ring cells below / above the tile
     static constexpr int NF = 3 * NC + NRL;            // faces evaluated by the CTA per plane
     static constexpr int CXSZ = 2 * 3 * (N + 1) * 2;   // per cell: [coord k][axis b][q = 0..N] complex
-    static constexpr int NE = 2 * 3 * (N + 1);
     static constexpr int NCG = NC + NRL;               // cells with geometry / c tables (own + ring below)
     // regions
     static constexpr int XS = 0;                                        // [2][NC][N3] own planes
@@ -151,24 +150,56 @@ struct Lay {
     static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
     static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // [2][NC][N3] grad0/1 -> Q0/1 -> R0/1
     static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][side][u|V, gn|G][N2]
-    static constexpr int CX = TRB + NF * 4 * N2;
-    static constexpr int CO = CX + (COEFF ? NCG * CXSZ : 0);
-    static constexpr int END = CO + (COEFF ? NCG * 4 : 0);
+    static constexpr int CX = TRB + NF * 4 * N2;                        // [2][NCG][CXSZ] c(x) factor tables
+    static constexpr int END = CX + (COEFF ? 2 * NCG * CXSZ : 0);
     static constexpr int BYTES = END * 8 + 64; // + 2 mbarriers
     static_assert(AFFINE || true, "");
 };
 
 } // namespace gn
 
+// c(x) factor tables, once at setup (reading R13, c = 1 + 0.5 sin(2 pi x0) cos(2 pi x1) at the mapped
+// points x = o_T + J_T xi): per cell of the L+2 planes (plane_begin-1 .. plane_begin+L, the
+// jac / geo layout), E'_kb(q) = exp(2 pi i (J_kb xi_q + [b = 0] o_k)), k = 0, 1, b = 0..2, q = 0..N
+// (xi_N = 1: the upper faces), stored as (cos, sin) pairs: [cell][k][b][q][2].
+struct XiTab {
+    double xi[9];
+};
+template <int N>
+__global__ void k_ctab(const double* __restrict__ jac, double* __restrict__ out, long long ncell, const MeshArgs M,
+                       const XiTab X)
+{
+    constexpr int NEN = 2 * 3 * (N + 1);
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncell * NEN) return;
+    const long long c = t / NEN;
+    const int e = (int)(t % NEN), k = e / (3 * (N + 1)), b = (e / (N + 1)) % 3, q = e % (N + 1);
+    const int pl = (int)(c / M.plane_cells), rem = (int)(c % M.plane_cells), i1 = rem / M.N2;
+    double Jkb;
+    if (jac) Jkb = jac[c * 9 + 3 * k + b];
+    else Jkb = (b == k) ? M.h[k] : 0.0;
+    double ph = Jkb * X.xi[q];
+    if (b == 0) {
+        int g0 = (M.plane_begin - 1 + pl) % M.N0;
+        if (g0 < 0) g0 += M.N0;
+        ph += k == 0 ? (double)g0 / M.N0 : (double)i1 / M.N1;
+    }
+    double sv, cv;
+    sincospi(2.0 * ph, &sv, &cv);
+    out[t * 2] = cv;
+    out[t * 2 + 1] = sv;
+}
+
 // grid: ntiles * nchunks CTAs (chunk-major), block Lay::NT, dynamic smem Lay::BYTES
 template <int N, bool AFFINE, bool COEFF, int T1, int T2, int MINB>
 __global__ void __launch_bounds__(gn::Lay<N, AFFINE, COEFF, T1, T2>::NT, MINB)
 k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
-      int p_begin, int p_end, int chunk_len, const EOTab<N> E, const MeshArgs M, const double* __restrict__ geo)
+      int p_begin, int p_end, int chunk_len, const EOTab<N> E, const MeshArgs M, const double* __restrict__ geo,
+      const double* __restrict__ ctab)
 {
     using Y = gn::Lay<N, AFFINE, COEFF, T1, T2>;
     constexpr int N2 = Y::N2, N3 = Y::N3, NC = Y::NC, NT = Y::NT, NRL = Y::NRL, NRH = Y::NRH, NF = Y::NF;
-    constexpr int NCG = Y::NCG, NE = Y::NE;
+    constexpr int NCG = Y::NCG, CXSZ = Y::CXSZ;
     constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
     extern __shared__ __align__(16) double sm[];
     double* const XS = sm + Y::XS;
@@ -180,7 +211,6 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     double* const G1 = sm + Y::G01 + NC * N3;
     double* const TRB = sm + Y::TRB;
     double* const CX = sm + Y::CX;
-    double* const CO = sm + Y::CO;
     uint64_t* const barA = reinterpret_cast<uint64_t*>(sm + Y::END);
     uint64_t* const barB = barA + 1;
     __shared__ double sXi[N + 1], sD[N * N], sW[N];
@@ -231,15 +261,21 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         for (int c1 = 0; c1 < T1; ++c1)
             gn::bulk_g2s(dst + c1 * T2 * N3, src + ((long long)(ti1 * T1 + c1) * M.N2 + ti2 * T2) * N3, ROWB, barA);
     };
-    auto issue_geo = [&](int lp, double* dst) { // records of own + ring-below cells of plane lp
+    // records (AFFINE) and c(x) factor tables (COEFF) of own + ring-below cells of plane lp into buffer `buf`
+    auto issue_geo = [&](int lp, int buf) {
+        auto rows = [&](const double* base, int per, double* dst) {
+            auto at = [&](int i1, int i2) { return base + cidx(lp + 1, i1, i2) * per; };
 #pragma unroll
-        for (int c1 = 0; c1 < T1; ++c1) gn::bulk_g2s(dst + c1 * T2 * GREC, grec(lp, ti1 * T1 + c1, ti2 * T2), T2 * GREC * 8, barA);
-        gn::bulk_g2s(dst + NC * GREC, grec(lp, wrap(ti1 * T1 - 1, M.N1), ti2 * T2), T2 * GREC * 8, barA);
+            for (int c1 = 0; c1 < T1; ++c1) gn::bulk_g2s(dst + c1 * T2 * per, at(ti1 * T1 + c1, ti2 * T2), T2 * per * 8, barA);
+            gn::bulk_g2s(dst + NC * per, at(wrap(ti1 * T1 - 1, M.N1), ti2 * T2), T2 * per * 8, barA);
 #pragma unroll
-        for (int c1 = 0; c1 < T1; ++c1)
-            gn::bulk_g2s(dst + (NC + T2 + c1) * GREC, grec(lp, ti1 * T1 + c1, wrap(ti2 * T2 - 1, M.N2)), GREC * 8, barA);
+            for (int c1 = 0; c1 < T1; ++c1)
+                gn::bulk_g2s(dst + (NC + T2 + c1) * per, at(ti1 * T1 + c1, wrap(ti2 * T2 - 1, M.N2)), per * 8, barA);
+        };
+        if (AFFINE) rows(geo, GREC, GE + buf * NCG * GREC);
+        if (COEFF) rows(ctab, CXSZ, CX + buf * NCG * CXSZ);
     };
-    constexpr uint32_t GEOB = AFFINE ? (uint32_t)(NCG * GREC * 8) : 0u;
+    constexpr uint32_t GEOB = (AFFINE ? (uint32_t)(NCG * GREC * 8) : 0u) + (COEFF ? (uint32_t)(NCG * CXSZ * 8) : 0u);
     // ring blocks of plane lp: rows via bulk copies on barB (thread 0), single d=2 cells via cp.async (all threads)
     constexpr bool D2BULK = (N3 % 2) == 0;
     auto issue_ring_bulk = [&](int lp) {
@@ -272,52 +308,24 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
     };
 
-    // c(x) tables of cell slot cc (own: cc < NC, ring below: NC + r) from its record / mesh h
-    auto ctab_task = [&](int cc, int rem, int g0, int i1, const double* gbuf) {
-        double sv, cv;
-        if (rem < NE) {
-            const int k = rem / (3 * (N + 1)), rem2 = rem % (3 * (N + 1)), bax = rem2 / (N + 1), q = rem2 % (N + 1);
-            const double Jkb = AFFINE ? gbuf[cc * GREC + 6 + 3 * k + bax] : (bax == k ? M.h[k] : 0.0);
-            sincospi(2.0 * Jkb * sXi[q], &sv, &cv);
-            double* e = CX + cc * Y::CXSZ + ((k * 3 + bax) * (N + 1) + q) * 2;
-            e[0] = cv;
-            e[1] = sv;
-        } else {
-            const int k = rem - NE;
-            const double o = k == 0 ? (double)g0 / M.N0 : (double)i1 / M.N1;
-            sincospi(2.0 * o, &sv, &cv);
-            CO[cc * 4 + 2 * k] = cv;
-            CO[cc * 4 + 2 * k + 1] = sv;
-        }
-    };
-    auto ctabs = [&](int lp, const double* gbuf) {
-        const int g0 = wrap(M.plane_begin + lp, M.N0);
-        for (int t = tid; t < NCG * (NE + 2); t += NT) {
-            const int cc = t / (NE + 2);
-            int i1;
-            if (cc < NC) i1 = ti1 * T1 + cc / T2;
-            else if (cc < NC + T2) i1 = wrap(ti1 * T1 - 1, M.N1);
-            else i1 = ti1 * T1 + (cc - NC - T2);
-            ctab_task(cc, t % (NE + 2), g0, i1, gbuf);
-        }
-    };
-    // c(x) at a point of cell slot cc (q indexes sXi; q = N is the face coordinate 1)
-    auto cval = [&](int cc, int q0, int q1, int q2) -> double {
-        const double* cx = CX + cc * Y::CXSZ;
+    // c(x) at a point of cell slot cc from its factor tables E'_kb(q) = exp(2 pi i (J_kb xi_q + [b = 0] o_k))
+    // (k_ctab, once at setup): e^{2 pi i x_k} = prod_b E'_kb(q_b); q indexes the nodes, q = N is xi = 1
+    auto cval = [&](const double* cxb, int cc, int q0, int q1, int q2) -> double {
+        const double* cx = cxb + cc * CXSZ;
         double z[2][2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const double* e0 = cx + ((k * 3 + 0) * (N + 1) + q0) * 2;
             const double* e1 = cx + ((k * 3 + 1) * (N + 1) + q1) * 2;
             const double* e2 = cx + ((k * 3 + 2) * (N + 1) + q2) * 2;
-            double tr, ti, ur, ui;
-            gn::cmul(CO[cc * 4 + 2 * k], CO[cc * 4 + 2 * k + 1], e0[0], e0[1], tr, ti);
-            gn::cmul(tr, ti, e1[0], e1[1], ur, ui);
-            gn::cmul(ur, ui, e2[0], e2[1], z[k][0], z[k][1]);
+            double tr, ti;
+            gn::cmul(e0[0], e0[1], e1[0], e1[1], tr, ti);
+            gn::cmul(tr, ti, e2[0], e2[1], z[k][0], z[k][1]);
         }
         return fma(0.5 * z[0][1], z[1][0], 1.0); // 1 + 0.5 sin(2 pi x0) cos(2 pi x1) (reading R13)
     };
 
+    const double* cxcur = CX; // c(x) tables of the plane being evaluated (set per step)
     // ---------------- face passes (face f with normal DC, point p = (a, b)) ----------------
     // the T- record slot of face f: own upper faces 3c + d -> c, tile-boundary faces 3 NC + r -> NC + r
     auto face_rec = [&](int f) { return f < 3 * NC ? f / 3 : NC + (f - 3 * NC); };
@@ -357,7 +365,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         double cF = 1.0;
         if (COEFF) {
             const int q0 = (d == 0) ? N : a, q1 = (d == 1) ? N : (d == 0 ? a : b), q2 = (d == 2) ? N : b;
-            cF = cval(face_rec(f), q0, q1, q2); // x_F on the T- cell at xi_d = 1
+            cF = cval(cxcur, face_rec(f), q0, q1, q2); // x_F on the T- cell at xi_d = 1
         }
         const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
         const double gm = TR(f, 0, 1)[p], gp = TR(f, 1, 1)[p];
@@ -460,10 +468,10 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             gn::mbar_expect_tx(barA, 2 * T1 * ROWB + GEOB);
             issue_x(p_begin - 1, XS + NC * N3);
             issue_x(p_begin, XS);
-            if (AFFINE) issue_geo(p_begin - 1, GE + NCG * GREC);
+            if (AFFINE || COEFF) issue_geo(p_begin - 1, 1);
         }
         gn::mbar_wait(barA, 0);
-        if (COEFF) ctabs(p_begin - 1, GE + NCG * GREC);
+        cxcur = CX + NCG * CXSZ;
         // T- upper-end traces (plane p_begin - 1) -> TR(3c, 0), T+ lower-end traces (plane p_begin) -> TR(3c, 1)
         for (int t = tid; t < NC * N2; t += NT) {
             const int c = t / N2, p = t - c * N2;
@@ -490,7 +498,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         if (tid == 0) {
             gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
             issue_x(p_begin + 1, XS + NC * N3);
-            if (AFFINE) issue_geo(p_begin, GE);
+            if (AFFINE || COEFF) issue_geo(p_begin, 0);
             issue_ring_bulk(p_begin);
         }
         issue_ring_cp(p_begin);
@@ -540,14 +548,14 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             }
         }
         foreign(XN);
-        if (COEFF) ctabs(lp, gb);
+        cxcur = CX + (s & 1) * NCG * CXSZ;
         __syncthreads();
 
         // stream the next step's own blocks (plane lp + 2) and geometry (plane lp + 1) behind the compute
         if (tid == 0 && s + 1 < nsteps) {
             gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
             issue_x(lp + 2, XS + (s & 1) * NC * N3);
-            if (AFFINE) issue_geo(lp + 1, GE + ((s + 1) & 1) * NCG * GREC);
+            if (AFFINE || COEFF) issue_geo(lp + 1, (s + 1) & 1);
         }
 
         // ---------------- P2: stage 2 at the thread's d=2 line points (a, b, q); face pass A ----------------
@@ -558,12 +566,11 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             for (int i = 0; i < 6; ++i) gt[i] = AFFINE ? gb[mc * GREC + i] : 0.0;
             double z0r = 0, z0i = 0, z1r = 0, z1i = 0;
             if (COEFF) {
-                const double* cx = CX + mc * Y::CXSZ;
-                double tr, ti;
-                gn::cmul(CO[mc * 4 + 0], CO[mc * 4 + 1], cx[((0 * 3 + 0) * (N + 1) + ma) * 2], cx[((0 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
-                gn::cmul(tr, ti, cx[((0 * 3 + 1) * (N + 1) + mb) * 2], cx[((0 * 3 + 1) * (N + 1) + mb) * 2 + 1], z0r, z0i);
-                gn::cmul(CO[mc * 4 + 2], CO[mc * 4 + 3], cx[((1 * 3 + 0) * (N + 1) + ma) * 2], cx[((1 * 3 + 0) * (N + 1) + ma) * 2 + 1], tr, ti);
-                gn::cmul(tr, ti, cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
+                const double* cx = cxcur + mc * CXSZ;
+                gn::cmul(cx[((0 * 3 + 0) * (N + 1) + ma) * 2], cx[((0 * 3 + 0) * (N + 1) + ma) * 2 + 1],
+                         cx[((0 * 3 + 1) * (N + 1) + mb) * 2], cx[((0 * 3 + 1) * (N + 1) + mb) * 2 + 1], z0r, z0i);
+                gn::cmul(cx[((1 * 3 + 0) * (N + 1) + ma) * 2], cx[((1 * 3 + 0) * (N + 1) + ma) * 2 + 1],
+                         cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
             }
             const double wab = sW[ma] * sW[mb];
             double* g0 = G0 + mc * N3;
@@ -573,7 +580,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 const int P = mab + N2 * q;
                 double cW = wab * E.w[q];
                 if (COEFF) {
-                    const double* cx = CX + mc * Y::CXSZ;
+                    const double* cx = cxcur + mc * CXSZ;
                     const double* e0 = cx + ((0 * 3 + 2) * (N + 1) + q) * 2;
                     const double* e1 = cx + ((1 * 3 + 2) * (N + 1) + q) * 2;
                     const double s0 = fma(z0r, e0[1], z0i * e0[0]);  // Im(z0 e0) = sin(2 pi x0)
