@@ -158,9 +158,27 @@ TileInfo pick_tile(int n, bool aff, bool coef)
 template <int N> struct GenShape;
 template <> struct GenShape<2> { static constexpr int T1 = 4, T2 = 4, MINB = 4; };
 template <> struct GenShape<3> { static constexpr int T1 = 2, T2 = 4, MINB = 4; };
-template <> struct GenShape<4> { static constexpr int T1 = 2, T2 = 4, MINB = 3; };
-template <> struct GenShape<5> { static constexpr int T1 = 2, T2 = 2, MINB = 3; };
-template <> struct GenShape<6> { static constexpr int T1 = 2, T2 = 2, MINB = 2; };
+
+// (T1, T2, min CTAs/SM) for n = 4, 5, 6; overridable at build time for tuning sweeps
+#ifndef GEN4_T1
+#define GEN4_T1 2
+#define GEN4_T2 4
+#define GEN4_MB 4
+#endif
+#ifndef GEN5_T1
+#define GEN5_T1 2
+#define GEN5_T2 4
+#define GEN5_MB 2
+#endif
+#ifndef GEN6_T1
+#define GEN6_T1 2
+#define GEN6_T2 2
+#define GEN6_MB 3
+#endif
+template <int a, int b, int c> struct GenS { static constexpr int T1 = a, T2 = b, MINB = c; };
+template <> struct GenShape<4> : GenS<GEN4_T1, GEN4_T2, GEN4_MB> {};
+template <> struct GenShape<5> : GenS<GEN5_T1, GEN5_T2, GEN5_MB> {};
+template <> struct GenShape<6> : GenS<GEN6_T1, GEN6_T2, GEN6_MB> {};
 template <> struct GenShape<7> { static constexpr int T1 = 2, T2 = 2, MINB = 1; };
 template <> struct GenShape<8> { static constexpr int T1 = 2, T2 = 2, MINB = 1; };
 
@@ -507,8 +525,13 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
                  ((n3 % 2 == 0) || (mesh->N[2] % 2 == 0 && c->ginfo.T2 % 2 == 0)) && getenv("DG_FORCE_GENERAL") == nullptr &&
                  getenv("DG_NO_GEN") == nullptr && c->ginfo.attr() == cudaSuccess;
         {
+            // planes per work item: enough (chunk, tile) items for ~8 per SM, at most 32 planes
+            // (each chunk re-evaluates the face below its first plane)
             const char* gc = getenv("DG_GEN_CHUNK");
-            c->gen_chunk = gc ? atoi(gc) : 16;
+            const long long items = (long long)(M.N1 / c->ginfo.T1) * (M.N2 / c->ginfo.T2) * M.L;
+            int ch = (int)(items / (8 * 148));
+            ch = ch < 2 ? 2 : (ch > 32 ? 32 : ch);
+            c->gen_chunk = gc ? atoi(gc) : ch;
         }
         if (c->gen) {
             switch (n) {

@@ -225,7 +225,7 @@ def test_axis8_slab_loopback_bitwise(world):
 
 
 # k_gen tile shapes (dg_capi.cu GenShape): n -> (T1, T2)
-GEN_TILE = {2: (4, 4), 3: (2, 4), 4: (2, 4), 5: (2, 2), 6: (2, 2), 7: (2, 2), 8: (2, 2)}
+GEN_TILE = {2: (4, 4), 3: (2, 4), 4: (2, 4), 5: (2, 4), 6: (2, 2), 7: (2, 2), 8: (2, 2)}
 
 
 @pytest.mark.parametrize("k", range(1, 8))
