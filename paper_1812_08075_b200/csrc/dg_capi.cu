@@ -173,7 +173,7 @@ template <> struct GenShape<3> { static constexpr int T1 = 2, T2 = 4, MINB = 4; 
 #ifndef GEN6_T1
 #define GEN6_T1 2
 #define GEN6_T2 2
-#define GEN6_MB 3
+#define GEN6_MB 2
 #endif
 template <int a, int b, int c> struct GenS { static constexpr int T1 = a, T2 = b, MINB = c; };
 template <> struct GenShape<4> : GenS<GEN4_T1, GEN4_T2, GEN4_MB> {};
@@ -184,11 +184,12 @@ template <> struct GenShape<8> { static constexpr int T1 = 2, T2 = 2, MINB = 1; 
 
 using GenFn = cudaError_t (*)(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                               double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo,
-                              const double* ctab);
+                              const double* ctab, const double* cface);
 
 template <int N, bool AFF, bool COEF>
 cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                       double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo, const double* ctab)
+                       double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo, const double* ctab,
+                       const double* cface)
 {
     constexpr int T1 = GenShape<N>::T1, T2 = GenShape<N>::T2, MB = GenShape<N>::MINB;
     using Y = dg::gn::Lay<N, AFF, COEF, T1, T2>;
@@ -197,7 +198,7 @@ cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, 
     const int CL = chunk > 0 && chunk < np ? chunk : np;
     const unsigned grid = (unsigned)((M.N1 / T1) * (M.N2 / T2) * ((np + CL - 1) / CL));
     dg::k_gen<N, AFF, COEF, T1, T2, MB><<<grid, Y::NT, Y::BYTES, st>>>(
-        x, xb, xa, r, p0, p1, CL, *static_cast<const dg::EOTab<N>*>(eot), M, geo, ctab);
+        x, xb, xa, r, p0, p1, CL, *static_cast<const dg::EOTab<N>*>(eot), M, geo, ctab, cface);
     return cudaGetLastError();
 }
 
@@ -391,7 +392,8 @@ struct dg_ctx {
     long long* dbg; // DG_TRACE: device buffer of per-phase clock64 stamps (k_axis8)
     double* d_jac;
     double* d_geo;  // k_tile / k_gen geometry records (affine)
-    double* d_ctab; // k_gen c(x) factor tables (coefficient c(x))
+    double* d_ctab;  // k_gen c(x) factor tables (coefficient c(x))
+    double* d_cface; // k_gen c(x) at the upper-face points of every cell
     // host-pipeline state (dg_apply_host)
     double* hx_d;
     double* hr_d;
@@ -430,7 +432,7 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         }
         return cudaGetLastError();
     }
-    if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo, c->d_ctab);
+    if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo, c->d_ctab, c->d_cface);
     if (c->tile) return c->tinfo.fn(c->tab, c->M, x, xb, xa, r, p0, p1, st, c->d_geo);
     const long long pc = c->M.plane_cells;
     return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
@@ -559,7 +561,9 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             // per-cell c(x) factor tables for k_gen (k_ctab, once)
             const long long nc = (long long)M.plane_cells * (M.L + 2);
             const long long nen = 2LL * 3 * (n + 1);
+            const long long cfsz = (3LL * n * n + 1) / 2 * 2;
             cudaError_t e = cudaMalloc(&c->d_ctab, sizeof(double) * 2 * nen * (size_t)nc);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_cface, sizeof(double) * cfsz * (size_t)nc);
             if (e != cudaSuccess) {
                 c->gen = false;
             } else {
@@ -577,7 +581,17 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
                 case 7: dg::k_ctab<7><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
                 case 8: dg::k_ctab<8><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
                 }
-                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_ctab); c->d_ctab = nullptr; c->gen = false; }
+                const unsigned g2 = (unsigned)((nc * cfsz + 255) / 256);
+                switch (n) {
+                case 2: dg::k_cface<2><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                case 3: dg::k_cface<3><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                case 4: dg::k_cface<4><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                case 5: dg::k_cface<5><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                case 6: dg::k_cface<6><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                case 7: dg::k_cface<7><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                case 8: dg::k_cface<8><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+                }
+                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_ctab); cudaFree(c->d_cface); c->d_ctab = c->d_cface = nullptr; c->gen = false; }
             }
         }
         if (c->tile) c->kname = "k_tile";
@@ -629,6 +643,7 @@ int dg_destroy(dg_ctx* c)
     if (c->d_jac) cudaFree(c->d_jac);
     if (c->d_geo) cudaFree(c->d_geo);
     if (c->d_ctab) cudaFree(c->d_ctab);
+    if (c->d_cface) cudaFree(c->d_cface);
     if (c->dbg) {
         // DG_TRACE: dump the stamps of the last launch
         static long long h[1024 * 16 * 8];

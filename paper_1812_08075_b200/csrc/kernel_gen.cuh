@@ -140,6 +140,7 @@ struct Lay {
     static constexpr int NRL = T1 + T2, NRH = T1 + T2; // ring cells below / above the tile
     static constexpr int NF = 3 * NC + NRL;            // faces evaluated by the CTA per plane
     static constexpr int CXSZ = 2 * 3 * (N + 1) * 2;   // per cell: [coord k][axis b][q = 0..N] complex
+    static constexpr int CFSZ = (3 * N2 + 1) / 2 * 2;  // per cell: c at the points of its 3 upper faces (even)
     static constexpr int NCG = NC + NRL;               // cells with geometry / c tables (own + ring below)
     // regions
     static constexpr int XS = 0;                                        // [2][NC][N3] own planes
@@ -150,8 +151,9 @@ struct Lay {
     static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
     static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // [2][NC][N3] grad0/1 -> Q0/1 -> R0/1
     static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][side][u|V, gn|G][N2]
-    static constexpr int CX = TRB + NF * 4 * N2;                        // [2][NCG][CXSZ] c(x) factor tables
-    static constexpr int END = CX + (COEFF ? 2 * NCG * CXSZ : 0);
+    static constexpr int CX = TRB + NF * 4 * N2;                        // [2][NC][CXSZ] c(x) factor tables (volume)
+    static constexpr int CF = CX + (COEFF ? 2 * NC * CXSZ : 0);         // [2][NCG][CFSZ] c(x) at upper-face points
+    static constexpr int END = CF + (COEFF ? 2 * NCG * CFSZ : 0);
     static constexpr int BYTES = END * 8 + 64; // + 2 mbarriers
     static_assert(AFFINE || true, "");
 };
@@ -190,16 +192,48 @@ __global__ void k_ctab(const double* __restrict__ jac, double* __restrict__ out,
     out[t * 2 + 1] = sv;
 }
 
+// c(x) at the points of each cell's 3 upper faces (reading R12: c_F = c(x_F) at the T- mapped point
+// x_F = o_T + J_T xi, xi_d = 1, tangential Gauss nodes), once at setup: [cell][CFSZ], face d at d N^2.
+template <int N>
+__global__ void k_cface(const double* __restrict__ jac, double* __restrict__ out, long long ncell, const MeshArgs M,
+                        const XiTab X)
+{
+    constexpr int N2 = N * N, CFSZ = (3 * N2 + 1) / 2 * 2;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncell * CFSZ) return;
+    const long long c = t / CFSZ;
+    const int e = (int)(t % CFSZ);
+    if (e >= 3 * N2) { out[t] = 0.0; return; }
+    const int d = e / N2, p = e % N2, a = p % N, b = p / N;
+    const int pl = (int)(c / M.plane_cells), rem = (int)(c % M.plane_cells), i1 = rem / M.N2;
+    int g0 = (M.plane_begin - 1 + pl) % M.N0;
+    if (g0 < 0) g0 += M.N0;
+    double xi[3];
+    xi[d] = 1.0;
+    xi[d == 0 ? 1 : 0] = X.xi[a];
+    xi[d == 2 ? 1 : 2] = X.xi[b];
+    double x0, x1;
+    if (jac) {
+        const double* J = jac + c * 9;
+        x0 = (double)g0 / M.N0 + J[0] * xi[0] + J[1] * xi[1] + J[2] * xi[2];
+        x1 = (double)i1 / M.N1 + J[3] * xi[0] + J[4] * xi[1] + J[5] * xi[2];
+    } else {
+        x0 = (g0 + xi[0]) * M.h[0];
+        x1 = (i1 + xi[1]) * M.h[1];
+    }
+    out[t] = 1.0 + 0.5 * sinpi(2.0 * x0) * cospi(2.0 * x1);
+}
+
 // grid: ntiles * nchunks CTAs (chunk-major), block Lay::NT, dynamic smem Lay::BYTES
 template <int N, bool AFFINE, bool COEFF, int T1, int T2, int MINB>
 __global__ void __launch_bounds__(gn::Lay<N, AFFINE, COEFF, T1, T2>::NT, MINB)
 k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
       int p_begin, int p_end, int chunk_len, const EOTab<N> E, const MeshArgs M, const double* __restrict__ geo,
-      const double* __restrict__ ctab)
+      const double* __restrict__ ctab, const double* __restrict__ cface)
 {
     using Y = gn::Lay<N, AFFINE, COEFF, T1, T2>;
     constexpr int N2 = Y::N2, N3 = Y::N3, NC = Y::NC, NT = Y::NT, NRL = Y::NRL, NRH = Y::NRH, NF = Y::NF;
-    constexpr int NCG = Y::NCG, CXSZ = Y::CXSZ;
+    constexpr int NCG = Y::NCG, CXSZ = Y::CXSZ, CFSZ = Y::CFSZ;
     constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
     extern __shared__ __align__(16) double sm[];
     double* const XS = sm + Y::XS;
@@ -211,6 +245,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     double* const G1 = sm + Y::G01 + NC * N3;
     double* const TRB = sm + Y::TRB;
     double* const CX = sm + Y::CX;
+    double* const CF = sm + Y::CF;
     uint64_t* const barA = reinterpret_cast<uint64_t*>(sm + Y::END);
     uint64_t* const barB = barA + 1;
     __shared__ double sXi[N + 1], sD[N * N], sW[N];
@@ -233,7 +268,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // source of plane lp's blocks (-1: halo below, L: halo above), and of its geometry records (L+2 planes from -1)
     auto xplane = [&](int lp) -> const double* { return lp < 0 ? xb : (lp >= M.L ? xa : x + (long long)lp * PC * N3); };
     auto grec = [&](int lp, int i1, int i2) -> const double* { return geo + (cidx(lp + 1, i1, i2)) * GREC; };
-    auto TR = [&](int f, int side, int q) -> double* { return TRB + ((f * 2 + side) * 2 + q) * N2; };
+    // face slots: (u, gn) -> (V, G) pairs per face f, side (0: T-, 1: T+), point p
+    double2* const TR2 = reinterpret_cast<double2*>(TRB);
+    auto TRp = [&](int f, int side) -> double2* { return TR2 + (f * 2 + side) * N2; };
 
     // fixed thread coordinates: cell mc of the tile, line position (ma, mb)
     const bool act = tid < Y::NACT;
@@ -263,19 +300,23 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     };
     // records (AFFINE) and c(x) factor tables (COEFF) of own + ring-below cells of plane lp into buffer `buf`
     auto issue_geo = [&](int lp, int buf) {
-        auto rows = [&](const double* base, int per, double* dst) {
+        auto rows = [&](const double* base, int per, double* dst, bool ring) {
             auto at = [&](int i1, int i2) { return base + cidx(lp + 1, i1, i2) * per; };
 #pragma unroll
             for (int c1 = 0; c1 < T1; ++c1) gn::bulk_g2s(dst + c1 * T2 * per, at(ti1 * T1 + c1, ti2 * T2), T2 * per * 8, barA);
+            if (!ring) return;
             gn::bulk_g2s(dst + NC * per, at(wrap(ti1 * T1 - 1, M.N1), ti2 * T2), T2 * per * 8, barA);
 #pragma unroll
             for (int c1 = 0; c1 < T1; ++c1)
                 gn::bulk_g2s(dst + (NC + T2 + c1) * per, at(ti1 * T1 + c1, wrap(ti2 * T2 - 1, M.N2)), per * 8, barA);
         };
-        if (AFFINE) rows(geo, GREC, GE + buf * NCG * GREC);
-        if (COEFF) rows(ctab, CXSZ, CX + buf * NCG * CXSZ);
+        if (AFFINE) rows(geo, GREC, GE + buf * NCG * GREC, true);
+        if (COEFF) {
+            rows(ctab, CXSZ, CX + buf * NC * CXSZ, false);
+            rows(cface, CFSZ, CF + buf * NCG * CFSZ, true);
+        }
     };
-    constexpr uint32_t GEOB = (AFFINE ? (uint32_t)(NCG * GREC * 8) : 0u) + (COEFF ? (uint32_t)(NCG * CXSZ * 8) : 0u);
+    constexpr uint32_t GEOB = (AFFINE ? (uint32_t)(NCG * GREC * 8) : 0u) + (COEFF ? (uint32_t)((NC * CXSZ + NCG * CFSZ) * 8) : 0u);
     // ring blocks of plane lp: rows via bulk copies on barB (thread 0), single d=2 cells via cp.async (all threads)
     constexpr bool D2BULK = (N3 % 2) == 0;
     auto issue_ring_bulk = [&](int lp) {
@@ -308,124 +349,120 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
     };
 
-    // c(x) at a point of cell slot cc from its factor tables E'_kb(q) = exp(2 pi i (J_kb xi_q + [b = 0] o_k))
-    // (k_ctab, once at setup): e^{2 pi i x_k} = prod_b E'_kb(q_b); q indexes the nodes, q = N is xi = 1
-    auto cval = [&](const double* cxb, int cc, int q0, int q1, int q2) -> double {
-        const double* cx = cxb + cc * CXSZ;
-        double z[2][2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const double* e0 = cx + ((k * 3 + 0) * (N + 1) + q0) * 2;
-            const double* e1 = cx + ((k * 3 + 1) * (N + 1) + q1) * 2;
-            const double* e2 = cx + ((k * 3 + 2) * (N + 1) + q2) * 2;
-            double tr, ti;
-            gn::cmul(e0[0], e0[1], e1[0], e1[1], tr, ti);
-            gn::cmul(tr, ti, e2[0], e2[1], z[k][0], z[k][1]);
-        }
-        return fma(0.5 * z[0][1], z[1][0], 1.0); // 1 + 0.5 sin(2 pi x0) cos(2 pi x1) (reading R13)
-    };
-
-    const double* cxcur = CX; // c(x) tables of the plane being evaluated (set per step)
+    const double* cxcur = CX; // c(x) factor tables of the plane being evaluated (set per step)
+    const double* cfcur = CF; // c(x) at the upper-face points of its own / ring-below cells
     // ---------------- face passes (face f with normal DC, point p = (a, b)) ----------------
     // the T- record slot of face f: own upper faces 3c + d -> c, tile-boundary faces 3 NC + r -> NC + r
     auto face_rec = [&](int f) { return f < 3 * NC ? f / 3 : NC + (f - 3 * NC); };
-    // a-, a+ components (normal d, tangential t1, t2) of face f from its T- record
-    auto face_a = [&](auto DC, const double* gb, int f, double& mdn, double& mt1, double& mt2, double& pdn, double& pt1,
-                      double& pt2, double& dS) {
+    // a-, a+ components (normal d, tangential t1, t2) and dS of face f from its T- record (16-B pairs)
+    struct FaceA {
+        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
+    };
+    auto face_a = [&](auto DC, const double* gb, int f) -> FaceA {
         constexpr int d = decltype(DC)::value;
+        FaceA A;
         if (AFFINE) {
-            const double* fr = gb + face_rec(f) * GREC + 12 + 7 * d;
-            dS = fr[0];
-            mdn = fr[1 + d];
-            mt1 = fr[d == 0 ? 2 : 1];
-            mt2 = fr[d == 2 ? 2 : 3];
-            pdn = fr[4 + d];
-            pt1 = fr[d == 0 ? 5 : 4];
-            pt2 = fr[d == 2 ? 5 : 6];
+            const double2* fr = reinterpret_cast<const double2*>(gb + face_rec(f) * GREC + 12 + 8 * d);
+            const double2 r0 = fr[0], r1 = fr[1], r2 = fr[2], r3 = fr[3]; // (dS, a-0) (a-1, a-2) (a+0, a+1) (a+2, 0)
+            const double am[3] = {r0.y, r1.x, r1.y}, ap[3] = {r2.x, r2.y, r3.x};
+            A.dS = r0.x;
+            A.mdn = am[d];
+            A.mt1 = am[d == 0 ? 1 : 0];
+            A.mt2 = am[d == 2 ? 1 : 2];
+            A.pdn = ap[d];
+            A.pt1 = ap[d == 0 ? 1 : 0];
+            A.pt2 = ap[d == 2 ? 1 : 2];
         } else {
-            mdn = pdn = 1.0 / M.h[d];
-            mt1 = mt2 = pt1 = pt2 = 0.0;
-            dS = M.h[(d + 1) % 3] * M.h[(d + 2) % 3];
+            A.mdn = A.pdn = 1.0 / M.h[d];
+            A.mt1 = A.mt2 = A.pt1 = A.pt2 = 0.0;
+            A.dS = M.h[(d + 1) % 3] * M.h[(d + 2) % 3];
         }
+        return A;
     };
     // pass A (AFFINE): w1 = a-_t1 u- + a+_t1 u+, w2 = a-_t2 u- + a+_t2 u+
-    auto passA = [&](auto DC, const double* gb, int f, int p) {
-        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
-        face_a(DC, gb, f, mdn, mt1, mt2, pdn, pt1, pt2, dS);
-        const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
-        WB[(f * 2 + 0) * N2 + p] = fma(mt1, um, pt1 * up);
-        WB[(f * 2 + 1) * N2 + p] = fma(mt2, um, pt2 * up);
+    auto passA = [&](auto DC, const double* gb, int f, int p, const double*, const double*) {
+        const FaceA A = face_a(DC, gb, f);
+        const double um = TRp(f, 0)[p].x, up = TRp(f, 1)[p].x;
+        WB[(f * 2 + 0) * N2 + p] = fma(A.mt1, um, A.pt1 * up);
+        WB[(f * 2 + 1) * N2 + p] = fma(A.mt2, um, A.pt2 * up);
     };
-    // pass B: flux. AFFINE: Cv- -> TR(f,0,0), Cg -> CG. Axis: V+-, G+- directly.
-    auto passB = [&](auto DC, const double* gb, int f, int p) {
+    // pass B: flux. AFFINE: Cv- -> TR(f,0).x, Cg -> CG. Axis: (V, G) of both sides directly.
+    // Ra, Rb: rows a, b of D (registers for the thread's own faces)
+    auto passB = [&](auto DC, const double* gb, int f, int p, const double* Ra, const double* Rb) {
         constexpr int d = decltype(DC)::value;
         const int a = p % N, b = p / N;
-        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
-        face_a(DC, gb, f, mdn, mt1, mt2, pdn, pt1, pt2, dS);
-        double cF = 1.0;
-        if (COEFF) {
-            const int q0 = (d == 0) ? N : a, q1 = (d == 1) ? N : (d == 0 ? a : b), q2 = (d == 2) ? N : b;
-            cF = cval(cxcur, face_rec(f), q0, q1, q2); // x_F on the T- cell at xi_d = 1
-        }
-        const double um = TR(f, 0, 0)[p], up = TR(f, 1, 0)[p];
-        const double gm = TR(f, 0, 1)[p], gp = TR(f, 1, 1)[p];
-        double s = fma(mdn, gm, pdn * gp);
+        const FaceA A = face_a(DC, gb, f);
+        const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0; // c at x_F on T- (R12)
+        const double2 m = TRp(f, 0)[p], pl = TRp(f, 1)[p];
+        double s = fma(A.mdn, m.y, A.pdn * pl.y);
         if (AFFINE) {
             const double* W1 = WB + (f * 2 + 0) * N2 + N * b;
             const double* W2 = WB + (f * 2 + 1) * N2 + a;
-            const double* Da = sD + a * N;
-            const double* Db = sD + b * N;
 #pragma unroll
-            for (int m = 0; m < N; ++m) {
-                s = fma(Da[m], W1[m], s);
-                s = fma(Db[m], W2[N * m], s);
+            for (int k = 0; k < N; ++k) {
+                s = fma(Ra[k], W1[k], s);
+                s = fma(Rb[k], W2[N * k], s);
             }
         }
-        const double Wt = sW[a] * sW[b] * dS;
-        const double jump = um - up;
+        const double Wt = sW[a] * sW[b] * A.dS;
+        const double jump = m.x - pl.x;
         const double avg = 0.5 * cF * s;
         const double Cvm = Wt * fma(M.gamma[d], jump, -avg);
         const double Cg = -0.5 * Wt * jump * cF;
         if (AFFINE) {
-            TR(f, 0, 0)[p] = Cvm;
+            TRp(f, 0)[p].x = Cvm;
             CG[f * N2 + p] = Cg;
         } else {
-            TR(f, 0, 0)[p] = Cvm;
-            TR(f, 0, 1)[p] = mdn * Cg;
-            TR(f, 1, 0)[p] = -Cvm;
-            TR(f, 1, 1)[p] = pdn * Cg;
+            TRp(f, 0)[p] = make_double2(Cvm, A.mdn * Cg);
+            TRp(f, 1)[p] = make_double2(-Cvm, A.pdn * Cg);
         }
     };
     // pass C (AFFINE): V+- = +-Cv- + a+-_t1 (D^T_t1 Cg) + a+-_t2 (D^T_t2 Cg), G+- = a+-_d Cg
-    auto passC = [&](auto DC, const double* gb, int f, int p) {
+    // Ca, Cb: columns a, b of D
+    auto passC = [&](auto DC, const double* gb, int f, int p, const double* Ca, const double* Cb) {
         const int a = p % N, b = p / N;
-        double mdn, mt1, mt2, pdn, pt1, pt2, dS;
-        face_a(DC, gb, f, mdn, mt1, mt2, pdn, pt1, pt2, dS);
+        const FaceA A = face_a(DC, gb, f);
         const double* C1 = CG + f * N2 + N * b;
         const double* C2 = CG + f * N2 + a;
         double t1 = 0.0, t2 = 0.0;
 #pragma unroll
-        for (int m = 0; m < N; ++m) {
-            t1 = fma(sD[m * N + a], C1[m], t1);
-            t2 = fma(sD[m * N + b], C2[N * m], t2);
+        for (int k = 0; k < N; ++k) {
+            t1 = fma(Ca[k], C1[k], t1);
+            t2 = fma(Cb[k], C2[N * k], t2);
         }
-        const double Cvm = TR(f, 0, 0)[p], Cg = CG[f * N2 + p];
-        TR(f, 0, 0)[p] = fma(mt1, t1, fma(mt2, t2, Cvm));
-        TR(f, 0, 1)[p] = mdn * Cg;
-        TR(f, 1, 0)[p] = fma(pt1, t1, fma(pt2, t2, -Cvm));
-        TR(f, 1, 1)[p] = pdn * Cg;
+        const double Cvm = TRp(f, 0)[p].x, Cg = CG[f * N2 + p];
+        TRp(f, 0)[p] = make_double2(fma(A.mt1, t1, fma(A.mt2, t2, Cvm)), A.mdn * Cg);
+        TRp(f, 1)[p] = make_double2(fma(A.pt1, t1, fma(A.pt2, t2, -Cvm)), A.pdn * Cg);
     };
-    // all faces of the plane step: the thread's 3 upper faces (fixed point) + the tile-boundary lower faces
-    auto all_faces = [&](auto pass, const double* gb) {
+    // all faces of the plane step: the thread's 3 upper faces (fixed point, D rows / columns in
+    // registers) + the tile-boundary lower faces. COLS: pass C wants columns of D, pass B rows.
+    auto all_faces = [&](auto pass, auto COLS, const double* gb) {
+        constexpr bool cols = decltype(COLS)::value;
         if (act) {
-            pass(std::integral_constant<int, 0>{}, gb, 3 * mc + 0, mab);
-            pass(std::integral_constant<int, 1>{}, gb, 3 * mc + 1, mab);
-            pass(std::integral_constant<int, 2>{}, gb, 3 * mc + 2, mab);
+            double Ra[N], Rb[N];
+            if (AFFINE) {
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    Ra[k] = cols ? sD[k * N + ma] : sD[ma * N + k];
+                    Rb[k] = cols ? sD[k * N + mb] : sD[mb * N + k];
+                }
+            }
+            pass(std::integral_constant<int, 0>{}, gb, 3 * mc + 0, mab, Ra, Rb);
+            pass(std::integral_constant<int, 1>{}, gb, 3 * mc + 1, mab, Ra, Rb);
+            pass(std::integral_constant<int, 2>{}, gb, 3 * mc + 2, mab, Ra, Rb);
         }
         for (int t = tid; t < NRL * N2; t += NT) {
-            const int rr = t / N2, p = t - rr * N2;
-            if (rr < T2) pass(std::integral_constant<int, 1>{}, gb, 3 * NC + rr, p);
-            else pass(std::integral_constant<int, 2>{}, gb, 3 * NC + rr, p);
+            const int rr = t / N2, p = t - rr * N2, a = p % N, b = p / N;
+            double Ra[N], Rb[N];
+            if (AFFINE) {
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    Ra[k] = cols ? sD[k * N + a] : sD[a * N + k];
+                    Rb[k] = cols ? sD[k * N + b] : sD[b * N + k];
+                }
+            }
+            if (rr < T2) pass(std::integral_constant<int, 1>{}, gb, 3 * NC + rr, p, Ra, Rb);
+            else pass(std::integral_constant<int, 2>{}, gb, 3 * NC + rr, p, Ra, Rb);
         }
     };
 
@@ -441,8 +478,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         gn::split<N>(v, xe, xo);
         double ulo, glo, uhi, ghi;
         gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
-        TR(f, side, 0)[p] = side ? ulo : uhi; // T- (ring below) faces the tile with its upper end
-        TR(f, side, 1)[p] = side ? glo : ghi;
+        TRp(f, side)[p] = side ? make_double2(ulo, glo) : make_double2(uhi, ghi); // T- faces the tile with its upper end
     };
     auto foreign = [&](const double* XN) {
         for (int t = tid; t < 2 * T2 * N2; t += NT) {
@@ -471,7 +507,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             if (AFFINE || COEFF) issue_geo(p_begin - 1, 1);
         }
         gn::mbar_wait(barA, 0);
-        cxcur = CX + NCG * CXSZ;
+        cxcur = CX + NC * CXSZ;
+        cfcur = CF + NCG * CFSZ;
         // T- upper-end traces (plane p_begin - 1) -> TR(3c, 0), T+ lower-end traces (plane p_begin) -> TR(3c, 1)
         for (int t = tid; t < NC * N2; t += NT) {
             const int c = t / N2, p = t - c * N2;
@@ -480,19 +517,28 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
         __syncthreads();
         const double* gb = GE + NCG * GREC;
+        double Ra[N], Rb[N], Ca[N], Cb[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            Ra[k] = sD[ma * N + k];
+            Rb[k] = sD[mb * N + k];
+            Ca[k] = sD[k * N + ma];
+            Cb[k] = sD[k * N + mb];
+        }
         if (AFFINE) {
-            if (act) passA(std::integral_constant<int, 0>{}, gb, 3 * mc, mab);
+            if (act) passA(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
             __syncthreads();
         }
-        if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab);
+        if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
         __syncthreads();
         if (AFFINE) {
-            if (act) passC(std::integral_constant<int, 0>{}, gb, 3 * mc, mab);
+            if (act) passC(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ca, Cb);
             __syncthreads();
         }
         if (act) {
-            pendV = TR(3 * mc, 1, 0)[mab];
-            pendG = TR(3 * mc, 1, 1)[mab];
+            const double2 vg = TRp(3 * mc, 1)[mab];
+            pendV = vg.x;
+            pendG = vg.y;
         }
         __syncthreads();
         if (tid == 0) {
@@ -529,26 +575,24 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
                 double y[N];
                 gn::sweep<N, false, false>(E, xe, xo, y);
-                TR(3 * mc + d, 0, 0)[mab] = uhi;
-                TR(3 * mc + d, 0, 1)[mab] = ghi;
+                TRp(3 * mc + d, 0)[mab] = make_double2(uhi, ghi);
                 if (d == 0) {
 #pragma unroll
                     for (int j = 0; j < N; ++j) G0[mc * N3 + pidx<N>(0, j, ma, mb)] = y[j];
                 } else if (d == 1) {
 #pragma unroll
                     for (int j = 0; j < N; ++j) G1[mc * N3 + pidx<N>(1, j, ma, mb)] = y[j];
-                    TR(flo1, 1, 0)[mab] = ulo;
-                    TR(flo1, 1, 1)[mab] = glo;
+                    TRp(flo1, 1)[mab] = make_double2(ulo, glo);
                 } else {
 #pragma unroll
                     for (int j = 0; j < N; ++j) g2[j] = y[j];
-                    TR(flo2, 1, 0)[mab] = ulo;
-                    TR(flo2, 1, 1)[mab] = glo;
+                    TRp(flo2, 1)[mab] = make_double2(ulo, glo);
                 }
             }
         }
         foreign(XN);
-        cxcur = CX + (s & 1) * NCG * CXSZ;
+        cxcur = CX + (s & 1) * NC * CXSZ;
+        cfcur = CF + (s & 1) * NCG * CFSZ;
         __syncthreads();
 
         // stream the next step's own blocks (plane lp + 2) and geometry (plane lp + 1) behind the compute
@@ -601,15 +645,15 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             }
         }
         if (AFFINE) {
-            all_faces(passA, gb);
+            all_faces(passA, std::false_type{}, gb);
             __syncthreads();
         }
         // ---------------- P3: face pass B (flux) ----------------
-        all_faces(passB, gb);
+        all_faces(passB, std::false_type{}, gb);
         __syncthreads();
         // ---------------- P4: face pass C (tangential back-projection) ----------------
         if (AFFINE) {
-            all_faces(passC, gb);
+            all_faces(passC, std::true_type{}, gb);
             __syncthreads();
         }
         // the ring buffer (aliased by W / CG) is free: stream the next plane's ring blocks
@@ -628,11 +672,13 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 double xe[HE], xo[H > 0 ? H : 1];
                 gn::split<N>(v, xe, xo);
                 double y[N];
-                gn::sweep<N, true, true>(E, xe, xo, y, pendV, pendG, TR(3 * mc, 0, 0)[mab], TR(3 * mc, 0, 1)[mab]);
+                const double2 hi = TRp(3 * mc, 0)[mab];
+                gn::sweep<N, true, true>(E, xe, xo, y, pendV, pendG, hi.x, hi.y);
 #pragma unroll
                 for (int j = 0; j < N; ++j) qd[pidx<N>(0, j, ma, mb)] = y[j];
-                pendV = TR(3 * mc, 1, 0)[mab]; // the T+ half of this face is the next plane's lower face
-                pendG = TR(3 * mc, 1, 1)[mab];
+                const double2 nx = TRp(3 * mc, 1)[mab]; // the T+ half of this face is the next plane's lower face
+                pendV = nx.x;
+                pendG = nx.y;
             }
             {
                 double* qd = G1 + mc * N3;
@@ -642,8 +688,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 double xe[HE], xo[H > 0 ? H : 1];
                 gn::split<N>(v, xe, xo);
                 double y[N];
-                gn::sweep<N, true, true>(E, xe, xo, y, TR(flo1, 1, 0)[mab], TR(flo1, 1, 1)[mab], TR(3 * mc + 1, 0, 0)[mab],
-                                         TR(3 * mc + 1, 0, 1)[mab]);
+                const double2 lo = TRp(flo1, 1)[mab], hi = TRp(3 * mc + 1, 0)[mab];
+                gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
 #pragma unroll
                 for (int j = 0; j < N; ++j) qd[pidx<N>(1, j, ma, mb)] = y[j];
             }
@@ -653,8 +699,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             double xe[HE], xo[H > 0 ? H : 1];
             gn::split<N>(q2, xe, xo);
             double y[N];
-            gn::sweep<N, true, true>(E, xe, xo, y, TR(flo2, 1, 0)[mab], TR(flo2, 1, 1)[mab], TR(3 * mc + 2, 0, 0)[mab],
-                                     TR(3 * mc + 2, 0, 1)[mab]);
+            const double2 lo = TRp(flo2, 1)[mab], hi = TRp(3 * mc + 2, 0)[mab];
+            gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
             const double* r0 = G0 + mc * N3;
             const double* r1 = G1 + mc * N3;
             double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;

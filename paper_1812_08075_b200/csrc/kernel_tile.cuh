@@ -33,8 +33,7 @@ namespace dg {
 constexpr int GREC = 36; // doubles per cell
 // [0..5]   G~ (00, 11, 22, 01, 02, 12)
 // [6..11]  J00 J01 J02 J10 J11 J12
-// [12 + 7 d .. 18 + 7 d]  upper face d: dS, a-[3], a+[3]
-// [33..35] unused
+// [12 + 8 d .. 19 + 8 d]  upper face d: dS, a-[3], a+[3], 0   (16-B aligned pairs)
 
 // One thread per cell of the L+2 planes plane_begin-1 .. plane_begin+L (same layout as jac).
 __global__ void k_geom(const double* __restrict__ jac, double* __restrict__ geo, long long ncell, int plane_cells,
@@ -52,7 +51,8 @@ __global__ void k_geom(const double* __restrict__ jac, double* __restrict__ geo,
     g[0] = gg(0, 0); g[1] = gg(1, 1); g[2] = gg(2, 2); g[3] = gg(0, 1); g[4] = gg(0, 2); g[5] = gg(1, 2);
     for (int i = 0; i < 6; ++i) g[6 + i] = J[i];
     for (int d = 0; d < 3; ++d) {
-        double* f = g + 12 + 7 * d;
+        double* f = g + 12 + 8 * d;
+        f[7] = 0.0;
         long long nb;
         if (d == 0) {
             if (pl + 1 >= nplanes_total) { for (int i = 0; i < 7; ++i) f[i] = 0.0; continue; }
@@ -75,7 +75,6 @@ __global__ void k_geom(const double* __restrict__ jac, double* __restrict__ geo,
             f[4 + e] = Jni[3 * e] * n0 + Jni[3 * e + 1] * n1 + Jni[3 * e + 2] * n2; // a+ = J_+^{-1} n_F
         }
     }
-    for (int i = 33; i < GREC; ++i) g[i] = 0.0;
 }
 
 namespace tl {
@@ -320,7 +319,7 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
             am_d = ap_d = 1.0 / hd;
             am_t1 = am_t2 = ap_t1 = ap_t2 = 0.0;
         } else {
-            const double* f = GEO + gs * GREC + 12 + 7 * d;
+            const double* f = GEO + gs * GREC + 12 + 8 * d;
             // components (d, t1, t2) of a- = f[1..3], a+ = f[4..6]
             am_d = d == 0 ? f[1] : (d == 1 ? f[2] : f[3]);
             am_t1 = d == 0 ? f[2] : f[1];
