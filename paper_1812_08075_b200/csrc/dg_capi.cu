@@ -252,7 +252,7 @@ GenInfo pick_gen(int n, bool aff, bool coef)
 // even/odd tables (kernel_gen.cuh, EOTab): D is centro-antisymmetric and e1, d1 are the mirrored
 // e0, -d0 on the symmetric Gauss nodes; the halves fold the factor 1/2 in.
 template <int N>
-void fill_eotab(const dg::HostTables& Ht, void* out)
+void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out)
 {
     dg::EOTab<N>* E = static_cast<dg::EOTab<N>*>(out);
     constexpr int H = N / 2;
@@ -291,6 +291,40 @@ void fill_eotab(const dg::HostTables& Ht, void* out)
         E->w[i] = Ht.w[i];
         E->xi[i] = Ht.xi[i];
     }
+    // line operator B^ (kernel_axis8.cuh) and its neighbour couplings aL = -d0/2 - P e0, bL = e0/2
+    // (aR_i = aL_{n-1-i}, bR_i = -bL_{n-1-i} by the mirror symmetry)
+    double B[N][N], aL[N], bL[N];
+    for (int i = 0; i < N; ++i) {
+        for (int j = 0; j < N; ++j) {
+            double s = 0.0;
+            for (int q = 0; q < N; ++q) s += Ht.D[q * N + i] * Ht.w[q] * Ht.D[q * N + j];
+            s += 0.5 * (Ht.e0[i] * Ht.d0[j] + Ht.d0[i] * Ht.e0[j] - Ht.e1[i] * Ht.d1[j] - Ht.d1[i] * Ht.e1[j]);
+            s += P * (Ht.e0[i] * Ht.e0[j] + Ht.e1[i] * Ht.e1[j]);
+            B[i][j] = s;
+        }
+        aL[i] = -0.5 * Ht.d0[i] - P * Ht.e0[i];
+        bL[i] = 0.5 * Ht.e0[i];
+    }
+    for (int i = 0; i < H; ++i) {
+        for (int j = 0; j < H; ++j) {
+            E->Lp[i][j] = 0.5 * (B[i][j] + B[i][N - 1 - j]);
+            E->Lm[i][j] = 0.5 * (B[i][j] - B[i][N - 1 - j]);
+        }
+        if (N & 1) E->Lp[i][H] = B[i][H];
+        E->Ae[i] = 0.5 * (aL[i] + aL[N - 1 - i]);
+        E->Be[i] = 0.5 * (bL[i] + bL[N - 1 - i]);
+        E->Ao[i] = 0.5 * (aL[i] - aL[N - 1 - i]);
+        E->Bo[i] = 0.5 * (bL[i] - bL[N - 1 - i]);
+    }
+    if (N & 1) {
+        for (int j = 0; j < H; ++j) E->Lmid[j] = B[H][j];
+        E->Lmid[H] = B[H][H];
+        E->Ae[H] = aL[H];
+        E->Be[H] = bL[H];
+    }
+    E->Sc[0] = h[1] * h[2] / h[0];
+    E->Sc[1] = h[0] * h[2] / h[1];
+    E->Sc[2] = h[0] * h[1] / h[2];
 }
 
 template <int N>
@@ -537,13 +571,13 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         }
         if (c->gen) {
             switch (n) {
-            case 2: fill_eotab<2>(H, c->eotab); break;
-            case 3: fill_eotab<3>(H, c->eotab); break;
-            case 4: fill_eotab<4>(H, c->eotab); break;
-            case 5: fill_eotab<5>(H, c->eotab); break;
-            case 6: fill_eotab<6>(H, c->eotab); break;
-            case 7: fill_eotab<7>(H, c->eotab); break;
-            case 8: fill_eotab<8>(H, c->eotab); break;
+            case 2: fill_eotab<2>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
+            case 3: fill_eotab<3>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
+            case 4: fill_eotab<4>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
+            case 5: fill_eotab<5>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
+            case 6: fill_eotab<6>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
+            case 7: fill_eotab<7>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
+            case 8: fill_eotab<8>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
             }
         }
         if ((c->tile || c->gen) && mesh->geom_kind == DG_GEOM_AFFINE) {
@@ -611,7 +645,8 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         const char* cl = getenv("DG_AX8_CHUNK");
         c->ax8_chunk = cl ? atoi(cl) : 12; // planes per work item (0: whole slab)
         c->ax8 = (n == 8 && mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE &&
-                  mesh->N[1] % T1 == 0 && mesh->N[2] % T2 == 0 && getenv("DG_FORCE_GENERAL") == nullptr);
+                  mesh->N[1] % T1 == 0 && mesh->N[2] % T2 == 0 && getenv("DG_FORCE_GENERAL") == nullptr &&
+                  getenv("DG_AX8_GEN") == nullptr);
     }
     if (c->ax8) {
         build_axis8(H, mesh->penalty_scale * k * (k + 1), M.h, &c->atab);

@@ -47,6 +47,13 @@ struct EOTab {
     double Es[HE], Ea[H], Ds[HE], Da[H];
     double D[N * N];   // plain D[q*N + j] (tangential face derivatives)
     double w[N], xi[N];
+    // line-operator form (axis-aligned, c = 1; LINEOP): the centro-symmetric 1D SIPG line operator
+    // B^ = D^T W D + 1/2 (e0 d0^T + d0 e0^T - e1 d1^T - d1 e1^T) + P (e0 e0^T + e1 e1^T) in even/odd form
+    // (Se_i = sum Lp[i][j] xe_j, So_i = sum Lm[i][j] xo_j, y_i = Se + So, y_{n-1-i} = Se - So; odd middle
+    // y_H = sum Lmid[j] xe_j) and its neighbour-trace couplings (Ae, Be on the sums, Ao, Bo on the differences)
+    double Lp[H][HE], Lm[H][H], Lmid[HE];
+    double Ae[HE], Be[HE], Ao[H], Bo[H];
+    double Sc[3]; // h_t1 h_t2 / h_d
 };
 
 namespace gn {
@@ -123,6 +130,33 @@ __device__ __forceinline__ void traces(const EOTab<N>& E, const double xe[EOTab<
     uhi = te - to;
     glo = qe + qo;
     ghi = qo - qe;
+}
+
+// y = B^ x + neighbour terms (line-operator form, LINEOP): uL, gL = (e1.x, d1.x) of the lower
+// neighbour's line, uR, gR = (e0.x, d0.x) of the upper neighbour's line
+template <int N>
+__device__ __forceinline__ void lineop(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
+                                       double y[N], double uL, double gL, double uR, double gR)
+{
+    constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
+    const double su = uL + uR, du = uL - uR, sg = gL + gR, dg = gL - gR;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+        double e = fma(E.Ae[i], su, E.Be[i] * dg);
+        double o = fma(E.Ao[i], du, E.Bo[i] * sg);
+#pragma unroll
+        for (int j = 0; j < HE; ++j) e = fma(E.Lp[i][j], xe[j], e);
+#pragma unroll
+        for (int j = 0; j < H; ++j) o = fma(E.Lm[i][j], xo[j], o);
+        y[i] = e + o;
+        y[N - 1 - i] = e - o;
+    }
+    if (N & 1) {
+        double m = fma(E.Ae[H], su, E.Be[H] * dg);
+#pragma unroll
+        for (int j = 0; j < HE; ++j) m = fma(E.Lmid[j], xe[j], m);
+        y[H] = m;
+    }
 }
 
 __device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double& cr, double& ci)
@@ -235,6 +269,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     constexpr int N2 = Y::N2, N3 = Y::N3, NC = Y::NC, NT = Y::NT, NRL = Y::NRL, NRH = Y::NRH, NF = Y::NF;
     constexpr int NCG = Y::NCG, CXSZ = Y::CXSZ, CFSZ = Y::CFSZ;
     constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
+    // axis-aligned with c = 1: stage 1 -> 2 -> 3 along a direction collapses into the 1D SIPG line
+    // operator B^ with neighbour-trace couplings (exact reordering, see kernel_axis8.cuh)
+    constexpr bool LINEOP = !AFFINE && !COEFF;
     extern __shared__ __align__(16) double sm[];
     double* const XS = sm + Y::XS;
     double* const RX = sm + Y::RX;
@@ -515,6 +552,18 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             trace_task(std::integral_constant<int, 0>{}, XS + NC * N3 + c * N3, p, 3 * c, 0);
             trace_task(std::integral_constant<int, 0>{}, XS + c * N3, p, 3 * c, 1);
         }
+        if (LINEOP) {
+            // the lower neighbour's (e1.x, d1.x) of the thread's d=0 line, from plane p_begin - 1
+            if (act) {
+                double v[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) v[j] = XS[NC * N3 + mc * N3 + pidx<N>(0, j, ma, mb)];
+                double xe[HE], xo[H > 0 ? H : 1];
+                gn::split<N>(v, xe, xo);
+                double ulo, glo;
+                gn::traces<N>(E, xe, xo, ulo, glo, pendV, pendG);
+            }
+        }
         __syncthreads();
         const double* gb = GE + NCG * GREC;
         double Ra[N], Rb[N], Ca[N], Cb[N];
@@ -529,13 +578,15 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             if (act) passA(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
             __syncthreads();
         }
-        if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
-        __syncthreads();
+        if (!LINEOP) {
+            if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
+            __syncthreads();
+        }
         if (AFFINE) {
             if (act) passC(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ca, Cb);
             __syncthreads();
         }
-        if (act) {
+        if (act && !LINEOP) {
             const double2 vg = TRp(3 * mc, 1)[mab];
             pendV = vg.x;
             pendG = vg.y;
@@ -559,6 +610,78 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         gn::mbar_wait(barB, s & 1);
         if (!D2BULK) gn::cp_async_wait_all();
         __syncthreads();
+
+        if constexpr (LINEOP) {
+            // ---- L1: own line traces (kept lines in registers) + foreign traces ----
+            double xe[3][HE], xo[3][H > 0 ? H : 1];
+            double nU = 0.0, nG = 0.0;
+            if (act) {
+                const double* xc = XC + mc * N3;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    double v[N];
+#pragma unroll
+                    for (int j = 0; j < N; ++j) v[j] = xc[pidx<N>(d, j, ma, mb)];
+                    gn::split<N>(v, xe[d], xo[d]);
+                    double ulo, glo, uhi, ghi;
+                    gn::traces<N>(E, xe[d], xo[d], ulo, glo, uhi, ghi);
+                    TRp(3 * mc + d, 0)[mab] = make_double2(uhi, ghi);
+                    if (d == 0) { nU = uhi; nG = ghi; }
+                    if (d == 1) TRp(flo1, 1)[mab] = make_double2(ulo, glo);
+                    if (d == 2) TRp(flo2, 1)[mab] = make_double2(ulo, glo);
+                }
+            }
+            foreign(XN);
+            __syncthreads();
+            if (s + 1 < nsteps) { // own plane buffer and ring buffer are free
+                if (tid == 0) {
+                    gn::mbar_expect_tx(barA, T1 * ROWB);
+                    issue_x(lp + 2, XS + (s & 1) * NC * N3);
+                    issue_ring_bulk(lp + 1);
+                }
+                issue_ring_cp(lp + 1);
+            }
+            // ---- L2: line operators; directions 0, 1 -> shared memory, 2 -> registers ----
+            double y2[N];
+            if (act) {
+                const double wab = sW[ma] * sW[mb];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    double uL, gL;
+                    if (d == 0) { uL = pendV; gL = pendG; }
+                    else { const double2 lo = TRp(d == 1 ? flo1 : flo2, 0)[mab]; uL = lo.x; gL = lo.y; }
+                    const double2 hi = TRp(3 * mc + d, 1)[mab];
+                    double y[N];
+                    gn::lineop<N>(E, xe[d], xo[d], y, uL, gL, hi.x, hi.y);
+                    const double S = wab * E.Sc[d];
+                    if (d == 0) {
+#pragma unroll
+                        for (int j = 0; j < N; ++j) G0[mc * N3 + pidx<N>(0, j, ma, mb)] = S * y[j];
+                    } else if (d == 1) {
+#pragma unroll
+                        for (int j = 0; j < N; ++j) G1[mc * N3 + pidx<N>(1, j, ma, mb)] = S * y[j];
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < N; ++j) y2[j] = S * y[j];
+                    }
+                }
+                pendV = nU;
+                pendG = nG;
+            }
+            __syncthreads();
+            // ---- L3: sum of the three directions, write r once ----
+            if (act) {
+                const double* r0 = G0 + mc * N3;
+                const double* r1 = G1 + mc * N3;
+                double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const int P = pidx<N>(2, j, ma, mb);
+                    dst[P] = y2[j] + r0[P] + r1[P];
+                }
+            }
+            continue;
+        }
 
         // ---------------- P1: stage 1 + own traces; foreign traces; c(x) tables ----------------
         double g2[N];

@@ -230,14 +230,13 @@ GEN_TILE = {2: (4, 4), 3: (2, 4), 4: (2, 4), 5: (2, 4), 6: (2, 2), 7: (2, 2), 8:
 
 @pytest.mark.parametrize("k", range(1, 8))
 @pytest.mark.parametrize("geom,coeff", [(0, 0), (0, 1), (1, 0), (1, 1)])
-def test_gen_all_degrees(k, geom, coeff):
+def test_gen_all_degrees(k, geom, coeff, monkeypatch):
     """k_gen (marching tiles with async staging) for every degree and geometry/coefficient
-    combination, on meshes of 1 and 2-3 tiles per direction (ring cells wrapping onto the tile
-    itself), against the oracle."""
+    combination (axis-aligned c = 1: the line-operator form), on meshes of 1 and 2-3 tiles per
+    direction (ring cells wrapping onto the tile itself), against the oracle."""
     T1, T2 = GEN_TILE[k + 1]
     N = (3, T1, 3 * T2) if k % 2 else (4, 2 * T1, T2)
-    if k == 7 and geom == 0 and coeff == 0:
-        pytest.skip("axis-aligned Q7 runs k_axis8")
+    monkeypatch.setenv("DG_AX8_GEN", "1")  # axis-aligned Q7 through k_gen instead of k_axis8
     w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=200 + k)
     op = _op(w)
     assert op.kernel_name == "k_gen"

@@ -53,7 +53,7 @@ def main():
         print(f"  {k:10s} {v:12d} {100 * v / T:5.1f}%  samples {ops_s[k]}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 2:
     main()
 
 
@@ -94,3 +94,37 @@ def by_line(rep, top=30):
 
 if __name__ == "__main__" and "--lines" in sys.argv:
     by_line(sys.argv[1])
+
+
+def smem_by_line(rep, top=30):
+    """Per CUDA source line: shared-memory wavefronts (actual / ideal) and executed instructions."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    res = []
+    fname = ""
+    hdr = None
+    for r in rows:
+        if r and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+            continue
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) < len(hdr):
+            continue
+        try:
+            wf = float(r[hdr.index("L1 Wavefronts Shared")])
+            wi = float(r[hdr.index("L1 Wavefronts Shared Ideal")])
+            ie = float(r[hdr.index("Instructions Executed")])
+        except (ValueError, IndexError):
+            continue
+        res.append((wf, wi, ie, f"{fname}:{r[0]}", r[1][:70]))
+    T = sum(x[0] for x in res) or 1
+    print(f"shared wavefronts total {T:.3e}")
+    for wf, wi, ie, loc, src in sorted(res, reverse=True)[:top]:
+        print(f"{100 * wf / T:5.1f}% wf {wf:.2e} ideal {wi:.2e} inst {ie:.2e} {loc:24s} {src}")
+
+
+if __name__ == "__main__" and "--smem" in sys.argv:
+    smem_by_line(sys.argv[1])

@@ -1,15 +1,38 @@
-# Full evidence run for profiles/: tests, smoke, default bench (with e2e + cpu baseline), ncu launch list and full capture of the top kernel
+# Full evidence run for profiles/: smoke, GPU tests, default bench (e2e + cpu baseline + clocks), reference
+# arm, per-config bench lines, ncu launch lists of the timed region (--profile-from-start off) and
+# one --set full capture per hot kernel (k_axis8 on cfg3, k_gen on cfg2 and cfg4), stall summaries.
 set -x
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
-nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv -lms 200 > gpurun_out/clocks.csv &
+O=gpurun_out/ev
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
+nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap --format=csv -lms 200 > $O/clocks.csv &
 SMI=$!
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 kill $SMI
-timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for C in 0 1 2 4; do timeout 600 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_cfg$C.json 2>&1; done
-C="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
-$C > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_launch.log 2>&1
-C2="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
-$C2 > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_axis8 -s 3 -c 1 -o gpurun_out/prof_top $C2 > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+for C in 0 1 2 4; do timeout 900 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_cfg$C.json 2> $O/bench_cfg$C.err; done
+for C in 3 2 4; do
+  B="python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
+  $B > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg$C.csv $B > /dev/null 2>&1
+done
+B3="python bench.py --config 3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_axis8 -s 3 -c 1 -o $O/prof_axis8_cfg3 $B3 > $O/ncu3.log 2>&1
+B2="python bench.py --config 2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg2 $B2 > $O/ncu2.log 2>&1
+B4="python bench.py --config 4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg4 $B4 > $O/ncu4.log 2>&1
+B1="python bench.py --config 1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg1 $B1 > $O/ncu1.log 2>&1
+# summaries on the box (the .ncu-rep files are ~20 MB each; gpurun returns <= 64 MiB)
+for R in axis8_cfg3 gen_cfg2 gen_cfg4 gen_cfg1; do
+  python tools/ncu_stalls.py $O/prof_$R.ncu-rep > $O/stalls_$R.txt 2>&1
+  python tools/ncu_stalls.py $O/prof_$R.ncu-rep --lines >> $O/stalls_$R.txt 2>&1
+done
+python tools/ncu_summary.py --launches $O/launches_cfg3.csv --rep $O/prof_axis8_cfg3.ncu-rep --out $O/ncu_axis8_cfg3 --title "k_axis8 on cfg3 (N=1)" > /dev/null 2>&1
+python tools/ncu_summary.py --launches $O/launches_cfg2.csv --rep $O/prof_gen_cfg2.ncu-rep --out $O/ncu_gen_cfg2 --title "k_gen on cfg2 (N=1)" > /dev/null 2>&1
+python tools/ncu_summary.py --launches $O/launches_cfg4.csv --rep $O/prof_gen_cfg4.ncu-rep --out $O/ncu_gen_cfg4 --title "k_gen on cfg4 (N=1)" > /dev/null 2>&1
+python tools/ncu_summary.py --rep $O/prof_gen_cfg1.ncu-rep --out $O/ncu_gen_cfg1 --title "k_gen on cfg1 (N=1)" > /dev/null 2>&1
+rm -f $O/prof_gen_cfg2.ncu-rep $O/prof_gen_cfg1.ncu-rep
+tail -2 $O/pytest_gpu.log
+cat $O/bench.json
