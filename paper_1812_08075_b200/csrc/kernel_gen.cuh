@@ -316,6 +316,12 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // TR face index of the own cell's lower faces d = 1, 2 (in-tile: upper face of the cell below)
     const int flo1 = mc1 > 0 ? 3 * (mc - T2) + 1 : 3 * NC + mc2;
     const int flo2 = mc2 > 0 ? 3 * (mc - 1) + 2 : 3 * NC + T2 + mc1;
+    // G0 / G1 layout [j2][cell][j0 + N j1]: the d = 2 line points of consecutive threads are consecutive
+    // (conflict-free stage 2 and final sum); index of point j on the thread's d-line of its cell
+    auto gix = [&](int d, int j) -> int {
+        return d == 0 ? mb * NC * N2 + mc * N2 + j + N * ma
+                      : (d == 1 ? mb * NC * N2 + mc * N2 + ma + N * j : j * NC * N2 + mc * N2 + mab);
+    };
 
     if (tid < N) { sXi[tid] = E.xi[tid]; sW[tid] = E.w[tid]; }
     for (int i = tid; i < N * N; i += NT) sD[i] = E.D[i];
@@ -399,16 +405,17 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         constexpr int d = decltype(DC)::value;
         FaceA A;
         if (AFFINE) {
+            // record pairs (a-_t1, a+_t1) (a-_t2, a+_t2) (a-_d, a+_d) (dS, 0): pass A reads the first two,
+            // pass B the last two, pass C the first three
             const double2* fr = reinterpret_cast<const double2*>(gb + face_rec(f) * GREC + 12 + 8 * d);
-            const double2 r0 = fr[0], r1 = fr[1], r2 = fr[2], r3 = fr[3]; // (dS, a-0) (a-1, a-2) (a+0, a+1) (a+2, 0)
-            const double am[3] = {r0.y, r1.x, r1.y}, ap[3] = {r2.x, r2.y, r3.x};
-            A.dS = r0.x;
-            A.mdn = am[d];
-            A.mt1 = am[d == 0 ? 1 : 0];
-            A.mt2 = am[d == 2 ? 1 : 2];
-            A.pdn = ap[d];
-            A.pt1 = ap[d == 0 ? 1 : 0];
-            A.pt2 = ap[d == 2 ? 1 : 2];
+            const double2 r0 = fr[0], r1 = fr[1], r2 = fr[2], r3 = fr[3];
+            A.mt1 = r0.x;
+            A.pt1 = r0.y;
+            A.mt2 = r1.x;
+            A.pt2 = r1.y;
+            A.mdn = r2.x;
+            A.pdn = r2.y;
+            A.dS = r3.x;
         } else {
             A.mdn = A.pdn = 1.0 / M.h[d];
             A.mt1 = A.mt2 = A.pt1 = A.pt2 = 0.0;
@@ -656,10 +663,10 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                     const double S = wab * E.Sc[d];
                     if (d == 0) {
 #pragma unroll
-                        for (int j = 0; j < N; ++j) G0[mc * N3 + pidx<N>(0, j, ma, mb)] = S * y[j];
+                        for (int j = 0; j < N; ++j) G0[gix(0, j)] = S * y[j];
                     } else if (d == 1) {
 #pragma unroll
-                        for (int j = 0; j < N; ++j) G1[mc * N3 + pidx<N>(1, j, ma, mb)] = S * y[j];
+                        for (int j = 0; j < N; ++j) G1[gix(1, j)] = S * y[j];
                     } else {
 #pragma unroll
                         for (int j = 0; j < N; ++j) y2[j] = S * y[j];
@@ -671,14 +678,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             __syncthreads();
             // ---- L3: sum of the three directions, write r once ----
             if (act) {
-                const double* r0 = G0 + mc * N3;
-                const double* r1 = G1 + mc * N3;
                 double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
 #pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    const int P = pidx<N>(2, j, ma, mb);
-                    dst[P] = y2[j] + r0[P] + r1[P];
-                }
+                for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y2[j] + G0[gix(2, j)] + G1[gix(2, j)];
             }
             continue;
         }
@@ -701,10 +703,10 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 TRp(3 * mc + d, 0)[mab] = make_double2(uhi, ghi);
                 if (d == 0) {
 #pragma unroll
-                    for (int j = 0; j < N; ++j) G0[mc * N3 + pidx<N>(0, j, ma, mb)] = y[j];
+                    for (int j = 0; j < N; ++j) G0[gix(0, j)] = y[j];
                 } else if (d == 1) {
 #pragma unroll
-                    for (int j = 0; j < N; ++j) G1[mc * N3 + pidx<N>(1, j, ma, mb)] = y[j];
+                    for (int j = 0; j < N; ++j) G1[gix(1, j)] = y[j];
                     TRp(flo1, 1)[mab] = make_double2(ulo, glo);
                 } else {
 #pragma unroll
@@ -740,11 +742,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                          cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
             }
             const double wab = sW[ma] * sW[mb];
-            double* g0 = G0 + mc * N3;
-            double* g1 = G1 + mc * N3;
 #pragma unroll
             for (int q = 0; q < N; ++q) {
-                const int P = mab + N2 * q;
+                const int P = gix(2, q);
                 double cW = wab * E.w[q];
                 if (COEFF) {
                     const double* cx = cxcur + mc * CXSZ;
@@ -754,15 +754,15 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                     const double c1 = fma(z1r, e1[0], -z1i * e1[1]); // Re(z1 e1) = cos(2 pi x1)
                     cW *= fma(0.5 * s0, c1, 1.0);
                 }
-                const double a0 = g0[P], a1 = g1[P], a2 = g2[q];
+                const double a0 = G0[P], a1 = G1[P], a2 = g2[q];
                 if (AFFINE) {
-                    g0[P] = cW * fma(gt[0], a0, fma(gt[3], a1, gt[4] * a2));
-                    g1[P] = cW * fma(gt[3], a0, fma(gt[1], a1, gt[5] * a2));
+                    G0[P] = cW * fma(gt[0], a0, fma(gt[3], a1, gt[4] * a2));
+                    G1[P] = cW * fma(gt[3], a0, fma(gt[1], a1, gt[5] * a2));
                     q2[q] = cW * fma(gt[4], a0, fma(gt[5], a1, gt[2] * a2));
                 } else {
                     const double adet = M.h[0] * M.h[1] * M.h[2];
-                    g0[P] = cW * (adet / (M.h[0] * M.h[0])) * a0;
-                    g1[P] = cW * (adet / (M.h[1] * M.h[1])) * a1;
+                    G0[P] = cW * (adet / (M.h[0] * M.h[0])) * a0;
+                    G1[P] = cW * (adet / (M.h[1] * M.h[1])) * a1;
                     q2[q] = cW * (adet / (M.h[2] * M.h[2])) * a2;
                 }
             }
@@ -788,33 +788,31 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         // ---------------- P5: stage 3 + face back-projection; d = 0, 1 in place, d = 2 -> r ----------------
         if (act) {
             {
-                double* qd = G0 + mc * N3;
                 double v[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) v[j] = qd[pidx<N>(0, j, ma, mb)];
+                for (int j = 0; j < N; ++j) v[j] = G0[gix(0, j)];
                 double xe[HE], xo[H > 0 ? H : 1];
                 gn::split<N>(v, xe, xo);
                 double y[N];
                 const double2 hi = TRp(3 * mc, 0)[mab];
                 gn::sweep<N, true, true>(E, xe, xo, y, pendV, pendG, hi.x, hi.y);
 #pragma unroll
-                for (int j = 0; j < N; ++j) qd[pidx<N>(0, j, ma, mb)] = y[j];
+                for (int j = 0; j < N; ++j) G0[gix(0, j)] = y[j];
                 const double2 nx = TRp(3 * mc, 1)[mab]; // the T+ half of this face is the next plane's lower face
                 pendV = nx.x;
                 pendG = nx.y;
             }
             {
-                double* qd = G1 + mc * N3;
                 double v[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) v[j] = qd[pidx<N>(1, j, ma, mb)];
+                for (int j = 0; j < N; ++j) v[j] = G1[gix(1, j)];
                 double xe[HE], xo[H > 0 ? H : 1];
                 gn::split<N>(v, xe, xo);
                 double y[N];
                 const double2 lo = TRp(flo1, 1)[mab], hi = TRp(3 * mc + 1, 0)[mab];
                 gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
 #pragma unroll
-                for (int j = 0; j < N; ++j) qd[pidx<N>(1, j, ma, mb)] = y[j];
+                for (int j = 0; j < N; ++j) G1[gix(1, j)] = y[j];
             }
         }
         __syncthreads();
@@ -824,14 +822,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             double y[N];
             const double2 lo = TRp(flo2, 1)[mab], hi = TRp(3 * mc + 2, 0)[mab];
             gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
-            const double* r0 = G0 + mc * N3;
-            const double* r1 = G1 + mc * N3;
             double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const int P = pidx<N>(2, j, ma, mb);
-                dst[P] = y[j] + r0[P] + r1[P];
-            }
+            for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y[j] + G0[gix(2, j)] + G1[gix(2, j)];
         }
         // (the barrier at the top of the next step orders these reads before the next writes)
     }

@@ -33,7 +33,9 @@ namespace dg {
 constexpr int GREC = 36; // doubles per cell
 // [0..5]   G~ (00, 11, 22, 01, 02, 12)
 // [6..11]  J00 J01 J02 J10 J11 J12
-// [12 + 8 d .. 19 + 8 d]  upper face d: dS, a-[3], a+[3], 0   (16-B aligned pairs)
+// [12 + 8 d .. 19 + 8 d]  upper face d: a-_t1, a+_t1, a-_t2, a+_t2, a-_d, a+_d, dS, 0  (a- = J_-^{-1} n_F,
+//                         a+ = J_+^{-1} n_F in (normal, tangential 1, tangential 2) order; 16-B pairs
+//                         grouped by the face pass that reads them)
 
 // One thread per cell of the L+2 planes plane_begin-1 .. plane_begin+L (same layout as jac).
 __global__ void k_geom(const double* __restrict__ jac, double* __restrict__ geo, long long ncell, int plane_cells,
@@ -69,11 +71,19 @@ __global__ void k_geom(const double* __restrict__ jac, double* __restrict__ geo,
         const double nu0 = Ji[3 * d], nu1 = Ji[3 * d + 1], nu2 = Ji[3 * d + 2];
         const double nn = sqrt(nu0 * nu0 + nu1 * nu1 + nu2 * nu2);
         const double n0 = nu0 / nn, n1 = nu1 / nn, n2 = nu2 / nn;
-        f[0] = adet * nn;
+        double am[3], ap[3];
         for (int e = 0; e < 3; ++e) {
-            f[1 + e] = Ji[3 * e] * n0 + Ji[3 * e + 1] * n1 + Ji[3 * e + 2] * n2;   // a- = J_-^{-1} n_F
-            f[4 + e] = Jni[3 * e] * n0 + Jni[3 * e + 1] * n1 + Jni[3 * e + 2] * n2; // a+ = J_+^{-1} n_F
+            am[e] = Ji[3 * e] * n0 + Ji[3 * e + 1] * n1 + Ji[3 * e + 2] * n2;   // a- = J_-^{-1} n_F
+            ap[e] = Jni[3 * e] * n0 + Jni[3 * e + 1] * n1 + Jni[3 * e + 2] * n2; // a+ = J_+^{-1} n_F
         }
+        const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+        f[0] = am[t1];
+        f[1] = ap[t1];
+        f[2] = am[t2];
+        f[3] = ap[t2];
+        f[4] = am[d];
+        f[5] = ap[d];
+        f[6] = adet * nn; // dS = |det J_-| |J_-^{-T} e_d| (Nanson)
     }
 }
 
@@ -320,17 +330,16 @@ k_tile(const double* __restrict__ x, const double* __restrict__ xb, const double
             am_t1 = am_t2 = ap_t1 = ap_t2 = 0.0;
         } else {
             const double* f = GEO + gs * GREC + 12 + 8 * d;
-            // components (d, t1, t2) of a- = f[1..3], a+ = f[4..6]
-            am_d = d == 0 ? f[1] : (d == 1 ? f[2] : f[3]);
-            am_t1 = d == 0 ? f[2] : f[1];
-            am_t2 = d == 2 ? f[2] : f[3];
-            ap_d = d == 0 ? f[4] : (d == 1 ? f[5] : f[6]);
-            ap_t1 = d == 0 ? f[5] : f[4];
-            ap_t2 = d == 2 ? f[5] : f[6];
+            am_t1 = f[0];
+            ap_t1 = f[1];
+            am_t2 = f[2];
+            ap_t2 = f[3];
+            am_d = f[4];
+            ap_d = f[5];
             const double gm = cF * (am_d * gmd + am_t1 * Q(2, sMinus)[ab] + am_t2 * Q(3, sMinus)[ab]);
             const double gp = cF * (ap_d * gpd + ap_t1 * Q(2, sPlus)[ab] + ap_t2 * Q(3, sPlus)[ab]);
             const double avg = 0.5 * (gm + gp);
-            const double W = sW[a] * sW[b] * f[0];
+            const double W = sW[a] * sW[b] * f[6];
             Cvm = W * (-avg + gam * jump);
             Cvp = W * (avg - gam * jump);
             Cg = -0.5 * W * jump * cF;
