@@ -70,9 +70,12 @@ typedef struct dg_mesh {
 /* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,
  * boundary vectors e0,e1,d0,d1), device copy of the slab's
  * geometry, kernel selection. k in [1,7]; quad = Gauss points per direction, must equal k+1
- * (collocation; other values -> DG_ERR_UNSUPPORTED). Allocates device memory (geometry:
- * 72 B per cell of L+2 planes for DG_GEOM_AFFINE, nothing for DG_GEOM_AXIS). *out owned by the
- * caller, release with dg_destroy. Synchronous. */
+ * (collocation; other values -> DG_ERR_UNSUPPORTED). Allocates device memory for the L+2 planes
+ * plane_begin-1 .. plane_begin+L: DG_GEOM_AFFINE: J (72 B/cell) and per-cell geometry records
+ * (288 B/cell: |det J| J^-1 J^-T, rows of J, upper-face normals / surface elements);
+ * DG_COEFF_SINCOS: c(x) factor tables (96 (n+1) B/cell) and c at the upper-face points
+ * (8 (3n^2 rounded up to even) B/cell); DG_GEOM_AXIS + DG_COEFF_ONE: nothing. *out owned by
+ * the caller, release with dg_destroy. Synchronous. */
 int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out);
 
 /* r = A x for a context owning the WHOLE mesh (nplanes == N[0]).
@@ -124,6 +127,19 @@ const char* dg_kernel_name(const dg_ctx* ctx);
  * DFMA chains per thread on every SM for `iters` x 128 DFMAs per thread and returns the achieved
  * FP64 TFLOP/s (2 flops per DFMA) and the kernel time. Synchronous. */
 int dg_bench_fp64(int device, int iters, double* tflops, double* ms);
+
+/* The kernels' 1D line algebra evaluated on the HOST with the same code (no device needed; a
+ * testing / inspection entry). For one line x[n], n = k+1, and four neighbour / face values
+ * nb = (a, b, c, d) writes out[3n + 4]:
+ *   out[0, n)     D x                                   (stage-1 sweep, D[q][j] = l_j'(xi_q))
+ *   out[n, 2n)    D^T x + e0 a + d0 b + e1 c + d1 d     (stage-3 sweep with the face back-projection
+ *                                                        at the two line ends)
+ *   out[2n, 3n)   B^ x + aL a + bL b + aR c + bR d      (axis-aligned line operator, DESIGN.md §4.1:
+ *                 B^ = D^T W D + (e0 d0^T + d0 e0^T - e1 d1^T - d1 e1^T)/2 + P (e0 e0^T + e1 e1^T),
+ *                 aL = -d0/2 - P e0, bL = e0/2, aR = d1/2 - P e1, bR = -e1/2, P = penalty_scale k(k+1))
+ *   out[3n, 3n+4) e0.x, d0.x, e1.x, d1.x                (face traces, 1-point tables)
+ * computed in the even/odd (centro-(anti)symmetric) form the kernels use. k in [1,7]. */
+int dg_line_ops(int k, double penalty_scale, const double* x, const double* nb, double* out);
 
 /* Thread-local description of the last error ("" if none). */
 const char* dg_last_error(void);

@@ -472,6 +472,28 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
     return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
 }
 
+namespace {
+template <int N>
+int host_line_ops(const dg::HostTables& Ht, double P, const double* x, const double* nb, double* out)
+{
+    alignas(16) unsigned char buf[sizeof(dg::EOTab<N>)];
+    const double h[3] = {1.0, 1.0, 1.0};
+    fill_eotab<N>(Ht, P, h, buf);
+    const dg::EOTab<N>& E = *reinterpret_cast<const dg::EOTab<N>*>(buf);
+    double v[N], xe[dg::EOTab<N>::HE], xo[dg::EOTab<N>::H], y[N];
+    for (int j = 0; j < N; ++j) v[j] = x[j];
+    dg::gn::split<N>(v, xe, xo);
+    dg::gn::sweep<N, false, false>(E, xe, xo, y);
+    for (int j = 0; j < N; ++j) out[j] = y[j];
+    dg::gn::sweep<N, true, true>(E, xe, xo, y, nb[0], nb[1], nb[2], nb[3]);
+    for (int j = 0; j < N; ++j) out[N + j] = y[j];
+    dg::gn::lineop<N>(E, xe, xo, y, nb[0], nb[1], nb[2], nb[3]);
+    for (int j = 0; j < N; ++j) out[2 * N + j] = y[j];
+    dg::gn::traces<N>(E, xe, xo, out[3 * N], out[3 * N + 1], out[3 * N + 2], out[3 * N + 3]);
+    return DG_OK;
+}
+} // namespace
+
 extern "C" {
 
 const char* dg_last_error(void) { return g_err.c_str(); }
@@ -709,6 +731,25 @@ int64_t dg_local_offset(const dg_ctx* c) { return c ? (int64_t)c->mesh.plane_beg
 int64_t dg_plane_ndofs(const dg_ctx* c) { return c ? c->plane_dofs : -1; }
 int dg_launches_per_apply(const dg_ctx* c) { return c ? 1 : -1; }
 const char* dg_kernel_name(const dg_ctx* c) { return c ? c->kname : ""; }
+
+int dg_line_ops(int k, double penalty_scale, const double* x, const double* nb, double* out)
+{
+    if (!x || !nb || !out) return fail(DG_ERR_INVALID, "dg_line_ops: NULL argument");
+    if (k < 1 || k > 7) return fail(DG_ERR_INVALID, "dg_line_ops: k=%d outside [1,7]", k);
+    const int n = k + 1;
+    dg::HostTables H;
+    if (dg::build_tables(n, &H)) return fail(DG_ERR_INVALID, "tables n=%d", n);
+    const double P = penalty_scale * k * (k + 1);
+    switch (n) {
+    case 2: return host_line_ops<2>(H, P, x, nb, out);
+    case 3: return host_line_ops<3>(H, P, x, nb, out);
+    case 4: return host_line_ops<4>(H, P, x, nb, out);
+    case 5: return host_line_ops<5>(H, P, x, nb, out);
+    case 6: return host_line_ops<6>(H, P, x, nb, out);
+    case 7: return host_line_ops<7>(H, P, x, nb, out);
+    default: return host_line_ops<8>(H, P, x, nb, out);
+    }
+}
 
 double dg_alg_flops(const dg_ctx* c)
 {

@@ -72,7 +72,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // split a line into even/odd halves
 template <int N>
-__device__ __forceinline__ void split(const double v[N], double xe[EOTab<N>::HE], double xo[EOTab<N>::H])
+__host__ __device__ __forceinline__ void split(const double v[N], double xe[EOTab<N>::HE], double xo[EOTab<N>::H])
 {
     constexpr int H = EOTab<N>::H;
 #pragma unroll
@@ -85,7 +85,7 @@ __device__ __forceinline__ void split(const double v[N], double xe[EOTab<N>::HE]
 
 // y = D x (TR = false) or y = D^T x (TR = true), plus optional stage-3 face terms at both ends
 template <int N, bool TR, bool FACE>
-__device__ __forceinline__ void sweep(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
+__host__ __device__ __forceinline__ void sweep(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
                                       double y[N], double Vl = 0, double Gl = 0, double Vh = 0, double Gh = 0)
 {
     constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
@@ -111,7 +111,7 @@ __device__ __forceinline__ void sweep(const EOTab<N>& E, const double xe[EOTab<N
 
 // traces of a line at both ends: u_lo = e0.x, u_hi = e1.x, g_lo = d0.x, g_hi = d1.x
 template <int N>
-__device__ __forceinline__ void traces(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
+__host__ __device__ __forceinline__ void traces(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
                                        double& ulo, double& glo, double& uhi, double& ghi)
 {
     constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;
@@ -135,7 +135,7 @@ __device__ __forceinline__ void traces(const EOTab<N>& E, const double xe[EOTab<
 // y = B^ x + neighbour terms (line-operator form, LINEOP): uL, gL = (e1.x, d1.x) of the lower
 // neighbour's line, uR, gR = (e0.x, d0.x) of the upper neighbour's line
 template <int N>
-__device__ __forceinline__ void lineop(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
+__host__ __device__ __forceinline__ void lineop(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
                                        double y[N], double uL, double gL, double uR, double gR)
 {
     constexpr int H = EOTab<N>::H, HE = EOTab<N>::HE;

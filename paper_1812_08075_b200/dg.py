@@ -49,7 +49,7 @@ class dg_mesh(ctypes.Structure):
 
 EXPORTS = ["dg_setup", "dg_apply", "dg_apply_planes", "dg_apply_host", "dg_destroy", "dg_set_stream",
            "dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs", "dg_alg_flops", "dg_alg_bytes",
-           "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64"]
+           "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops"]
 
 _lib = None
 
@@ -81,6 +81,7 @@ def load(path: str = LIB_PATH):
     L.dg_kernel_name.restype = ctypes.c_char_p
     L.dg_last_error.restype = ctypes.c_char_p
     L.dg_bench_fp64.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp]
+    L.dg_line_ops.argtypes = [ctypes.c_int, ctypes.c_double, vp, vp, vp]
     _lib = L
     return L
 
@@ -173,6 +174,18 @@ def dg_bench_fp64(device: int = 0, iters: int = 4000):
     tf, ms = ctypes.c_double(), ctypes.c_double()
     _check(load().dg_bench_fp64(device, iters, ctypes.byref(tf), ctypes.byref(ms)))
     return tf.value, ms.value
+
+
+def dg_line_ops(k: int, penalty_scale: float, x, nb) -> np.ndarray:
+    """The kernels' even/odd line algebra on the host (include/dg.h): returns [D x | D^T x + face terms |
+    B^ x + neighbour terms | e0.x, d0.x, e1.x, d1.x] for one line x (n = k+1) and nb = 4 values."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    nb = np.ascontiguousarray(nb, dtype=np.float64)
+    n = k + 1
+    assert x.shape == (n,) and nb.shape == (4,)
+    out = np.empty(3 * n + 4)
+    _check(load().dg_line_ops(k, float(penalty_scale), x.ctypes.data, nb.ctypes.data, out.ctypes.data))
+    return out
 
 
 def dg_last_error() -> str:
