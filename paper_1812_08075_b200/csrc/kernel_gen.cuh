@@ -179,7 +179,10 @@ struct Lay {
     // regions
     static constexpr int XS = 0;                                        // [2][NC][N3] own planes
     static constexpr int RXSZ = (NRL + NRH) * N3;                       // ring blocks: bd1[T2] bd2[T1] ad1[T2] ad2[T1]
-    static constexpr int WCSZ = AFFINE ? 3 * NF * N2 : 0;               // W (2 per face point) + CG (1)
+    // affine face passes: per face line (N points per thread, 2 buffers) for n <= 5, per face point
+    // (3 buffers) for n >= 6, where the NF n line tasks would leave too many of the NF n^2 threads idle
+    static constexpr bool FACE_LINES = N <= 5;
+    static constexpr int WCSZ = AFFINE ? (FACE_LINES ? 2 : 3) * NF * N2 : 0;
     static constexpr int RX = XS + 2 * NC * N3;                         // ring blocks, aliased by W / CG after P1
     static constexpr int RXEND = RX + (RXSZ > WCSZ ? RXSZ : WCSZ);
     static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
@@ -275,8 +278,11 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     extern __shared__ __align__(16) double sm[];
     double* const XS = sm + Y::XS;
     double* const RX = sm + Y::RX;
-    double* const WB = sm + Y::RX;              // W: [NF][2][N2] (AFFINE, after P1)
-    double* const CG = sm + Y::RX + 2 * NF * N2; // CG: [NF][N2]
+    double* const BX = sm + Y::RX;           // face buffers (AFFINE, after P1, aliasing the ring blocks):
+    double* const BY = sm + Y::RX + NF * N2; // BX: w2 -> Cg, BY: D_t1 w1 -> D_t2^T Cg, [NF][N2]
+    double* const PW = sm + Y::RX;              // point passes: W [NF][2][N2]
+    double* const PCG = sm + Y::RX + 2 * NF * N2; //              Cg [NF][N2]
+    constexpr bool FACE_LINES = Y::FACE_LINES;
     double* const GE = sm + Y::GE;
     double* const G0 = sm + Y::G01;
     double* const G1 = sm + Y::G01 + NC * N3;
@@ -423,16 +429,17 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
         return A;
     };
+    // ---- affine faces, one thread per face point (used when the line tasks would leave threads idle) ----
     // pass A (AFFINE): w1 = a-_t1 u- + a+_t1 u+, w2 = a-_t2 u- + a+_t2 u+
-    auto passA = [&](auto DC, const double* gb, int f, int p, const double*, const double*) {
+    auto ptA = [&](auto DC, const double* gb, int f, int p, const double*, const double*) {
         const FaceA A = face_a(DC, gb, f);
         const double um = TRp(f, 0)[p].x, up = TRp(f, 1)[p].x;
-        WB[(f * 2 + 0) * N2 + p] = fma(A.mt1, um, A.pt1 * up);
-        WB[(f * 2 + 1) * N2 + p] = fma(A.mt2, um, A.pt2 * up);
+        PW[(f * 2 + 0) * N2 + p] = fma(A.mt1, um, A.pt1 * up);
+        PW[(f * 2 + 1) * N2 + p] = fma(A.mt2, um, A.pt2 * up);
     };
     // pass B: flux. AFFINE: Cv- -> TR(f,0).x, Cg -> CG. Axis: (V, G) of both sides directly.
     // Ra, Rb: rows a, b of D (registers for the thread's own faces)
-    auto passB = [&](auto DC, const double* gb, int f, int p, const double* Ra, const double* Rb) {
+    auto ptB = [&](auto DC, const double* gb, int f, int p, const double* Ra, const double* Rb) {
         constexpr int d = decltype(DC)::value;
         const int a = p % N, b = p / N;
         const FaceA A = face_a(DC, gb, f);
@@ -440,8 +447,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const double2 m = TRp(f, 0)[p], pl = TRp(f, 1)[p];
         double s = fma(A.mdn, m.y, A.pdn * pl.y);
         if (AFFINE) {
-            const double* W1 = WB + (f * 2 + 0) * N2 + N * b;
-            const double* W2 = WB + (f * 2 + 1) * N2 + a;
+            const double* W1 = PW + (f * 2 + 0) * N2 + N * b;
+            const double* W2 = PW + (f * 2 + 1) * N2 + a;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
                 s = fma(Ra[k], W1[k], s);
@@ -455,7 +462,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const double Cg = -0.5 * Wt * jump * cF;
         if (AFFINE) {
             TRp(f, 0)[p].x = Cvm;
-            CG[f * N2 + p] = Cg;
+            PCG[f * N2 + p] = Cg;
         } else {
             TRp(f, 0)[p] = make_double2(Cvm, A.mdn * Cg);
             TRp(f, 1)[p] = make_double2(-Cvm, A.pdn * Cg);
@@ -463,24 +470,24 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     };
     // pass C (AFFINE): V+- = +-Cv- + a+-_t1 (D^T_t1 Cg) + a+-_t2 (D^T_t2 Cg), G+- = a+-_d Cg
     // Ca, Cb: columns a, b of D
-    auto passC = [&](auto DC, const double* gb, int f, int p, const double* Ca, const double* Cb) {
+    auto ptC = [&](auto DC, const double* gb, int f, int p, const double* Ca, const double* Cb) {
         const int a = p % N, b = p / N;
         const FaceA A = face_a(DC, gb, f);
-        const double* C1 = CG + f * N2 + N * b;
-        const double* C2 = CG + f * N2 + a;
+        const double* C1 = PCG + f * N2 + N * b;
+        const double* C2 = PCG + f * N2 + a;
         double t1 = 0.0, t2 = 0.0;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             t1 = fma(Ca[k], C1[k], t1);
             t2 = fma(Cb[k], C2[N * k], t2);
         }
-        const double Cvm = TRp(f, 0)[p].x, Cg = CG[f * N2 + p];
+        const double Cvm = TRp(f, 0)[p].x, Cg = PCG[f * N2 + p];
         TRp(f, 0)[p] = make_double2(fma(A.mt1, t1, fma(A.mt2, t2, Cvm)), A.mdn * Cg);
         TRp(f, 1)[p] = make_double2(fma(A.pt1, t1, fma(A.pt2, t2, -Cvm)), A.pdn * Cg);
     };
     // all faces of the plane step: the thread's 3 upper faces (fixed point, D rows / columns in
     // registers) + the tile-boundary lower faces. COLS: pass C wants columns of D, pass B rows.
-    auto all_faces = [&](auto pass, auto COLS, const double* gb) {
+    auto pt_faces = [&](auto pass, auto COLS, const double* gb) {
         constexpr bool cols = decltype(COLS)::value;
         if (act) {
             double Ra[N], Rb[N];
@@ -507,6 +514,115 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             }
             if (rr < T2) pass(std::integral_constant<int, 1>{}, gb, 3 * NC + rr, p, Ra, Rb);
             else pass(std::integral_constant<int, 2>{}, gb, 3 * NC + rr, p, Ra, Rb);
+        }
+    };
+
+    // ---- affine faces, one thread per face line (N points), tangential contractions as even/odd sweeps ----
+    // line A (t1-line b): w1 = a-_t1 u- + a+_t1 u+ -> BY = D_t1 w1;  w2 = a-_t2 u- + a+_t2 u+ -> BX
+    auto lineA = [&](auto DC, const double* gb, int f, int b) {
+        const FaceA A = face_a(DC, gb, f);
+        double w1[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            const int p = a + N * b;
+            const double um = TRp(f, 0)[p].x, up = TRp(f, 1)[p].x;
+            w1[a] = fma(A.mt1, um, A.pt1 * up);
+            BX[f * N2 + p] = fma(A.mt2, um, A.pt2 * up);
+        }
+        double xe[HE], xo[H > 0 ? H : 1], y[N];
+        gn::split<N>(w1, xe, xo);
+        gn::sweep<N, false, false>(E, xe, xo, y);
+#pragma unroll
+        for (int a = 0; a < N; ++a) BY[f * N2 + a + N * b] = y[a];
+    };
+    // line B (t2-line a): {c grad u . n} = c_F/2 (a-_d gn- + a+_d gn+ + D_t1 w1 + D_t2 w2), SIPG flux
+    // (Eq. diffreac_weak, theta = -1): Cv- -> TR(f,0).x, Cg -> BX, D_t2^T Cg -> BY
+    auto lineB = [&](auto DC, const double* gb, int f, int a) {
+        constexpr int d = decltype(DC)::value;
+        const FaceA A = face_a(DC, gb, f);
+        double w2[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) w2[k] = BX[f * N2 + a + N * k];
+        double xe[HE], xo[H > 0 ? H : 1], s2[N];
+        gn::split<N>(w2, xe, xo);
+        gn::sweep<N, false, false>(E, xe, xo, s2);
+        double cg[N];
+        const double wa = sW[a];
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            const int p = a + N * b;
+            const double2 m = TRp(f, 0)[p], pl = TRp(f, 1)[p];
+            const double s = fma(A.mdn, m.y, fma(A.pdn, pl.y, BY[f * N2 + p] + s2[b]));
+            const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0; // c at x_F on T- (R12)
+            const double Wt = wa * sW[b] * A.dS;
+            const double jump = m.x - pl.x;
+            TRp(f, 0)[p].x = Wt * fma(M.gamma[d], jump, -0.5 * cF * s);
+            cg[b] = -0.5 * Wt * jump * cF;
+        }
+        double t2[N];
+        gn::split<N>(cg, xe, xo);
+        gn::sweep<N, true, false>(E, xe, xo, t2);
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+            BX[f * N2 + a + N * b] = cg[b];
+            BY[f * N2 + a + N * b] = t2[b];
+        }
+    };
+    // line C (t1-line b): V+- = +-Cv- + a+-_t1 D_t1^T Cg + a+-_t2 D_t2^T Cg, G+- = a+-_d Cg
+    auto lineC = [&](auto DC, const double* gb, int f, int b) {
+        const FaceA A = face_a(DC, gb, f);
+        double cg[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) cg[k] = BX[f * N2 + k + N * b];
+        double xe[HE], xo[H > 0 ? H : 1], t1[N];
+        gn::split<N>(cg, xe, xo);
+        gn::sweep<N, true, false>(E, xe, xo, t1);
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            const int p = a + N * b;
+            const double Cvm = TRp(f, 0)[p].x, t2 = BY[f * N2 + p];
+            TRp(f, 0)[p] = make_double2(fma(A.mt1, t1[a], fma(A.mt2, t2, Cvm)), A.mdn * cg[a]);
+            TRp(f, 1)[p] = make_double2(fma(A.pt1, t1[a], fma(A.pt2, t2, -Cvm)), A.pdn * cg[a]);
+        }
+    };
+    // the plane step's faces as line tasks, grouped by direction (ordinal o: own d=0, d=1, d=2 faces,
+    // then the tile-boundary lower faces d=1, d=2); nf0 = NC restricts to the d=0 own faces (prologue)
+    auto face_lines = [&](auto line, const double* gb, int nfo) {
+        for (int t = tid; t < nfo * N; t += NT) {
+            const int o = t / N, l = t - o * N;
+            if (o < NC) line(std::integral_constant<int, 0>{}, gb, 3 * o, l);
+            else if (o < 2 * NC) line(std::integral_constant<int, 1>{}, gb, 3 * (o - NC) + 1, l);
+            else if (o < 3 * NC) line(std::integral_constant<int, 2>{}, gb, 3 * (o - 2 * NC) + 2, l);
+            else if (o < 3 * NC + T2) line(std::integral_constant<int, 1>{}, gb, o, l);
+            else line(std::integral_constant<int, 2>{}, gb, o, l);
+        }
+    };
+    // axis-aligned faces (no tangential terms): flux per point, (V, G) of both sides directly
+    auto passB = [&](auto DC, const double* gb, int f, int p, const double*, const double*) {
+        constexpr int d = decltype(DC)::value;
+        const int a = p % N, b = p / N;
+        const FaceA A = face_a(DC, gb, f);
+        const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0;
+        const double2 m = TRp(f, 0)[p], pl = TRp(f, 1)[p];
+        const double s = fma(A.mdn, m.y, A.pdn * pl.y);
+        const double Wt = sW[a] * sW[b] * A.dS;
+        const double jump = m.x - pl.x;
+        const double Cvm = Wt * fma(M.gamma[d], jump, -0.5 * cF * s);
+        const double Cg = -0.5 * Wt * jump * cF;
+        TRp(f, 0)[p] = make_double2(Cvm, A.mdn * Cg);
+        TRp(f, 1)[p] = make_double2(-Cvm, A.pdn * Cg);
+    };
+    // axis-aligned faces of the plane step: the thread's 3 upper faces + the tile-boundary lower faces
+    auto all_faces = [&](auto pass, const double* gb) {
+        if (act) {
+            pass(std::integral_constant<int, 0>{}, gb, 3 * mc + 0, mab, nullptr, nullptr);
+            pass(std::integral_constant<int, 1>{}, gb, 3 * mc + 1, mab, nullptr, nullptr);
+            pass(std::integral_constant<int, 2>{}, gb, 3 * mc + 2, mab, nullptr, nullptr);
+        }
+        for (int t = tid; t < NRL * N2; t += NT) {
+            const int rr = t / N2, p = t - rr * N2;
+            if (rr < T2) pass(std::integral_constant<int, 1>{}, gb, 3 * NC + rr, p, nullptr, nullptr);
+            else pass(std::integral_constant<int, 2>{}, gb, 3 * NC + rr, p, nullptr, nullptr);
         }
     };
 
@@ -573,24 +689,30 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
         __syncthreads();
         const double* gb = GE + NCG * GREC;
-        double Ra[N], Rb[N], Ca[N], Cb[N];
+        if (AFFINE && FACE_LINES) {
+            face_lines(lineA, gb, NC);
+            __syncthreads();
+            face_lines(lineB, gb, NC);
+            __syncthreads();
+            face_lines(lineC, gb, NC);
+            __syncthreads();
+        } else if (AFFINE) {
+            double Ra[N], Rb[N], Ca[N], Cb[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            Ra[k] = sD[ma * N + k];
-            Rb[k] = sD[mb * N + k];
-            Ca[k] = sD[k * N + ma];
-            Cb[k] = sD[k * N + mb];
-        }
-        if (AFFINE) {
-            if (act) passA(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
+            for (int k = 0; k < N; ++k) {
+                Ra[k] = sD[ma * N + k];
+                Rb[k] = sD[mb * N + k];
+                Ca[k] = sD[k * N + ma];
+                Cb[k] = sD[k * N + mb];
+            }
+            if (act) ptA(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
             __syncthreads();
-        }
-        if (!LINEOP) {
-            if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
+            if (act) ptB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ra, Rb);
             __syncthreads();
-        }
-        if (AFFINE) {
-            if (act) passC(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ca, Cb);
+            if (act) ptC(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, Ca, Cb);
+            __syncthreads();
+        } else if (!LINEOP) {
+            if (act) passB(std::integral_constant<int, 0>{}, gb, 3 * mc, mab, nullptr, nullptr);
             __syncthreads();
         }
         if (act && !LINEOP) {
@@ -767,19 +889,27 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 }
             }
         }
-        if (AFFINE) {
-            all_faces(passA, std::false_type{}, gb);
+        if (AFFINE && !FACE_LINES) {
+            pt_faces(ptA, std::false_type{}, gb);
+            __syncthreads();
+            pt_faces(ptB, std::false_type{}, gb);
+            __syncthreads();
+            pt_faces(ptC, std::true_type{}, gb);
+            __syncthreads();
+        } else if (AFFINE) {
+            face_lines(lineA, gb, NF);
+            __syncthreads();
+            // ---------------- P3: face line pass B (flux) ----------------
+            face_lines(lineB, gb, NF);
+            __syncthreads();
+            // ---------------- P4: face line pass C (tangential back-projection) ----------------
+            face_lines(lineC, gb, NF);
+            __syncthreads();
+        } else {
+            all_faces(passB, gb);
             __syncthreads();
         }
-        // ---------------- P3: face pass B (flux) ----------------
-        all_faces(passB, std::false_type{}, gb);
-        __syncthreads();
-        // ---------------- P4: face pass C (tangential back-projection) ----------------
-        if (AFFINE) {
-            all_faces(passC, std::true_type{}, gb);
-            __syncthreads();
-        }
-        // the ring buffer (aliased by W / CG) is free: stream the next plane's ring blocks
+        // the ring buffer (aliased by the face buffers) is free: stream the next plane's ring blocks
         if (s + 1 < nsteps) {
             if (tid == 0) issue_ring_bulk(lp + 1);
             issue_ring_cp(lp + 1);
