@@ -182,13 +182,19 @@ struct Lay {
     // affine face passes: per face line (N points per thread, 2 buffers) for n <= 5, per face point
     // (3 buffers) for n >= 6, where the NF n line tasks would leave too many of the NF n^2 threads idle
     static constexpr bool FACE_LINES = N <= 5;
-    static constexpr int WCSZ = AFFINE ? (FACE_LINES ? 2 : 3) * NF * N2 : 0;
+    // face-slot strides chosen against bank conflicts of the line tasks (16-B pairs: 3 FS = 5 mod 8, so
+    // both the t2-line (point-consecutive) and the t1-line (face-consecutive) task orders hit distinct
+    // banks; 8-B line buffers: odd FB)
+    static constexpr int pad_fs(int base) { return (3 * base) % 8 == 5 ? base : pad_fs(base + 1); }
+    static constexpr int FS = pad_fs(2 * N2);          // pairs per face (2 sides x N2 points + pad)
+    static constexpr int FB = (N2 % 2) ? N2 : N2 + 1;  // doubles per face in the line buffers
+    static constexpr int WCSZ = AFFINE ? (FACE_LINES ? 2 * NF * FB : 3 * NF * N2) : 0;
     static constexpr int RX = XS + 2 * NC * N3;                         // ring blocks, aliased by W / CG after P1
     static constexpr int RXEND = RX + (RXSZ > WCSZ ? RXSZ : WCSZ);
     static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
     static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // [2][NC][N3] grad0/1 -> Q0/1 -> R0/1
     static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][side][u|V, gn|G][N2]
-    static constexpr int CX = TRB + NF * 4 * N2;                        // [2][NC][CXSZ] c(x) factor tables (volume)
+    static constexpr int CX = TRB + NF * 2 * FS;                        // [2][NC][CXSZ] c(x) factor tables (volume)
     static constexpr int CF = CX + (COEFF ? 2 * NC * CXSZ : 0);         // [2][NCG][CFSZ] c(x) at upper-face points
     static constexpr int END = CF + (COEFF ? 2 * NCG * CFSZ : 0);
     static constexpr int BYTES = END * 8 + 64; // + 2 mbarriers
@@ -279,7 +285,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     double* const XS = sm + Y::XS;
     double* const RX = sm + Y::RX;
     double* const BX = sm + Y::RX;           // face buffers (AFFINE, after P1, aliasing the ring blocks):
-    double* const BY = sm + Y::RX + NF * N2; // BX: w2 -> Cg, BY: D_t1 w1 -> D_t2^T Cg, [NF][N2]
+    constexpr int FS = Y::FS, FB = Y::FB;
+    double* const BY = sm + Y::RX + NF * FB; // BX: w2 -> Cg, BY: D_t1 w1 -> D_t2^T Cg, [NF][FB]
     double* const PW = sm + Y::RX;              // point passes: W [NF][2][N2]
     double* const PCG = sm + Y::RX + 2 * NF * N2; //              Cg [NF][N2]
     constexpr bool FACE_LINES = Y::FACE_LINES;
@@ -313,7 +320,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto grec = [&](int lp, int i1, int i2) -> const double* { return geo + (cidx(lp + 1, i1, i2)) * GREC; };
     // face slots: (u, gn) -> (V, G) pairs per face f, side (0: T-, 1: T+), point p
     double2* const TR2 = reinterpret_cast<double2*>(TRB);
-    auto TRp = [&](int f, int side) -> double2* { return TR2 + (f * 2 + side) * N2; };
+    auto TRp = [&](int f, int side) -> double2* { return TR2 + f * FS + side * N2; };
 
     // fixed thread coordinates: cell mc of the tile, line position (ma, mb)
     const bool act = tid < Y::NACT;
@@ -527,13 +534,13 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             const int p = a + N * b;
             const double um = TRp(f, 0)[p].x, up = TRp(f, 1)[p].x;
             w1[a] = fma(A.mt1, um, A.pt1 * up);
-            BX[f * N2 + p] = fma(A.mt2, um, A.pt2 * up);
+            BX[f * FB + p] = fma(A.mt2, um, A.pt2 * up);
         }
         double xe[HE], xo[H > 0 ? H : 1], y[N];
         gn::split<N>(w1, xe, xo);
         gn::sweep<N, false, false>(E, xe, xo, y);
 #pragma unroll
-        for (int a = 0; a < N; ++a) BY[f * N2 + a + N * b] = y[a];
+        for (int a = 0; a < N; ++a) BY[f * FB + a + N * b] = y[a];
     };
     // line B (t2-line a): {c grad u . n} = c_F/2 (a-_d gn- + a+_d gn+ + D_t1 w1 + D_t2 w2), SIPG flux
     // (Eq. diffreac_weak, theta = -1): Cv- -> TR(f,0).x, Cg -> BX, D_t2^T Cg -> BY
@@ -542,7 +549,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const FaceA A = face_a(DC, gb, f);
         double w2[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) w2[k] = BX[f * N2 + a + N * k];
+        for (int k = 0; k < N; ++k) w2[k] = BX[f * FB + a + N * k];
         double xe[HE], xo[H > 0 ? H : 1], s2[N];
         gn::split<N>(w2, xe, xo);
         gn::sweep<N, false, false>(E, xe, xo, s2);
@@ -552,7 +559,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         for (int b = 0; b < N; ++b) {
             const int p = a + N * b;
             const double2 m = TRp(f, 0)[p], pl = TRp(f, 1)[p];
-            const double s = fma(A.mdn, m.y, fma(A.pdn, pl.y, BY[f * N2 + p] + s2[b]));
+            const double s = fma(A.mdn, m.y, fma(A.pdn, pl.y, BY[f * FB + p] + s2[b]));
             const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0; // c at x_F on T- (R12)
             const double Wt = wa * sW[b] * A.dS;
             const double jump = m.x - pl.x;
@@ -564,8 +571,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         gn::sweep<N, true, false>(E, xe, xo, t2);
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-            BX[f * N2 + a + N * b] = cg[b];
-            BY[f * N2 + a + N * b] = t2[b];
+            BX[f * FB + a + N * b] = cg[b];
+            BY[f * FB + a + N * b] = t2[b];
         }
     };
     // line C (t1-line b): V+- = +-Cv- + a+-_t1 D_t1^T Cg + a+-_t2 D_t2^T Cg, G+- = a+-_d Cg
@@ -573,23 +580,34 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const FaceA A = face_a(DC, gb, f);
         double cg[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) cg[k] = BX[f * N2 + k + N * b];
+        for (int k = 0; k < N; ++k) cg[k] = BX[f * FB + k + N * b];
         double xe[HE], xo[H > 0 ? H : 1], t1[N];
         gn::split<N>(cg, xe, xo);
         gn::sweep<N, true, false>(E, xe, xo, t1);
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             const int p = a + N * b;
-            const double Cvm = TRp(f, 0)[p].x, t2 = BY[f * N2 + p];
+            const double Cvm = TRp(f, 0)[p].x, t2 = BY[f * FB + p];
             TRp(f, 0)[p] = make_double2(fma(A.mt1, t1[a], fma(A.mt2, t2, Cvm)), A.mdn * cg[a]);
             TRp(f, 1)[p] = make_double2(fma(A.pt1, t1[a], fma(A.pt2, t2, -Cvm)), A.pdn * cg[a]);
         }
     };
     // the plane step's faces as line tasks, grouped by direction (ordinal o: own d=0, d=1, d=2 faces,
     // then the tile-boundary lower faces d=1, d=2); nf0 = NC restricts to the d=0 own faces (prologue)
-    auto face_lines = [&](auto line, const double* gb, int nfo) {
+    // OFAST: consecutive threads take the same line of consecutive faces (t1-line passes A, C);
+    // otherwise consecutive lines of one face (t2-line pass B) — both bank-conflict free with FS
+    auto face_lines = [&](auto line, auto OFAST, const double* gb, int nfo) {
+        constexpr bool of = decltype(OFAST)::value;
         for (int t = tid; t < nfo * N; t += NT) {
-            const int o = t / N, l = t - o * N;
+            int g0, G;
+            if (t < NC * N) { g0 = 0; G = NC; }
+            else if (t < 2 * NC * N) { g0 = NC; G = NC; }
+            else if (t < 3 * NC * N) { g0 = 2 * NC; G = NC; }
+            else if (t < (3 * NC + T2) * N) { g0 = 3 * NC; G = T2; }
+            else { g0 = 3 * NC + T2; G = T1; }
+            const int u = t - g0 * N;
+            const int oo = of ? u % G : u / N, l = of ? u / G : u % N;
+            const int o = g0 + oo;
             if (o < NC) line(std::integral_constant<int, 0>{}, gb, 3 * o, l);
             else if (o < 2 * NC) line(std::integral_constant<int, 1>{}, gb, 3 * (o - NC) + 1, l);
             else if (o < 3 * NC) line(std::integral_constant<int, 2>{}, gb, 3 * (o - 2 * NC) + 2, l);
@@ -690,11 +708,11 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         __syncthreads();
         const double* gb = GE + NCG * GREC;
         if (AFFINE && FACE_LINES) {
-            face_lines(lineA, gb, NC);
+            face_lines(lineA, std::true_type{}, gb, NC);
             __syncthreads();
-            face_lines(lineB, gb, NC);
+            face_lines(lineB, std::false_type{}, gb, NC);
             __syncthreads();
-            face_lines(lineC, gb, NC);
+            face_lines(lineC, std::true_type{}, gb, NC);
             __syncthreads();
         } else if (AFFINE) {
             double Ra[N], Rb[N], Ca[N], Cb[N];
@@ -897,13 +915,13 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             pt_faces(ptC, std::true_type{}, gb);
             __syncthreads();
         } else if (AFFINE) {
-            face_lines(lineA, gb, NF);
+            face_lines(lineA, std::true_type{}, gb, NF);
             __syncthreads();
             // ---------------- P3: face line pass B (flux) ----------------
-            face_lines(lineB, gb, NF);
+            face_lines(lineB, std::false_type{}, gb, NF);
             __syncthreads();
             // ---------------- P4: face line pass C (tangential back-projection) ----------------
-            face_lines(lineC, gb, NF);
+            face_lines(lineC, std::true_type{}, gb, NF);
             __syncthreads();
         } else {
             all_faces(passB, gb);
