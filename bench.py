@@ -182,12 +182,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--quad", type=int, default=-1,
+                    help="Gauss points per direction (default k+1; k+2 = overintegration, SURVEY §8(f2))")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
 
     import synth
     w = synth.CONFIGS[args.config]
+    if args.quad > 0 and args.quad != w.k + 1:
+        import dataclasses
+        w = dataclasses.replace(w, quad=args.quad, name=f"{w.name}_quad{args.quad}")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -209,7 +214,7 @@ def main():
         return synth.jac_planes_torch(w, pb, npl, device=dev).cpu().numpy()
 
     sop = slab.SlabOperator(w.N, w.k, rank, world, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
-                            penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank)
+                            penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank, quad=w.m)
     op = sop.op
     x = synth.x_torch(w, start=sop.offset, count=sop.ndofs, device=dev)
     r = torch.empty_like(x)

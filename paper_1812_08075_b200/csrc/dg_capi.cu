@@ -4,6 +4,7 @@
 #include "kernel_axis8.cuh"
 #include "kernel_cell.cuh"
 #include "kernel_gen.cuh"
+#include "kernel_quad.cuh"
 #include "kernel_tile.cuh"
 #include "tables.h"
 
@@ -327,6 +328,77 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
     E->Sc[2] = h[0] * h[1] / h[2];
 }
 
+// ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
+template <int N, bool AFF, bool COEF>
+cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
+                        double* r, long long c0, long long c1, cudaStream_t st, const double*)
+{
+    using L = dg::qd::QLay<N, N + 1>;
+    if (c1 <= c0) return cudaSuccess;
+    const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
+    dg::k_quad<N, N + 1, AFF, COEF><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
+        x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
+    return cudaGetLastError();
+}
+template <int N, bool AFF, bool COEF>
+cudaError_t attr_quad()
+{
+    return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dg::qd::QLay<N, N + 1>::BYTES);
+}
+template <int N>
+LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err)
+{
+    if (aff) {
+        *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
+        return coef ? launch_quad<N, true, true> : launch_quad<N, true, false>;
+    }
+    *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
+    return coef ? launch_quad<N, false, true> : launch_quad<N, false, false>;
+}
+LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err)
+{
+    switch (n) {
+    case 2: return pick_quad_n<2>(aff, coef, err);
+    case 3: return pick_quad_n<3>(aff, coef, err);
+    case 4: return pick_quad_n<4>(aff, coef, err);
+    case 5: return pick_quad_n<5>(aff, coef, err);
+    case 6: return pick_quad_n<6>(aff, coef, err);
+    case 7: return pick_quad_n<7>(aff, coef, err);
+    default: return pick_quad_n<8>(aff, coef, err);
+    }
+}
+// interpolation / derivative of the n-node Lagrange basis at the m = n+1 Gauss points (long double
+// product formulas, no division by (s - x_a): robust when a quadrature point is close to a node)
+template <int N>
+void fill_qtab(const dg::HostTables& Hn, const dg::HostTables& Hm, void* out)
+{
+    constexpr int M = N + 1;
+    dg::QTab<N, M>* Q = static_cast<dg::QTab<N, M>*>(out);
+    for (int q = 0; q < M; ++q) {
+        const long double s = Hm.xi[q];
+        for (int j = 0; j < N; ++j) {
+            long double v = 1.0L, dv = 0.0L;
+            for (int a = 0; a < N; ++a) {
+                if (a == j) continue;
+                const long double den = (long double)Hn.xi[j] - Hn.xi[a];
+                dv = dv * ((s - Hn.xi[a]) / den) + v / den; // product rule, accumulated
+                v *= (s - Hn.xi[a]) / den;
+            }
+            Q->A[q * N + j] = (double)v;
+            Q->Dq[q * N + j] = (double)dv;
+        }
+        Q->wq[q] = Hm.w[q];
+        Q->xq[q] = Hm.xi[q];
+    }
+    for (int j = 0; j < N; ++j) {
+        Q->e0[j] = Hn.e0[j];
+        Q->e1[j] = Hn.e1[j];
+        Q->d0[j] = Hn.d0[j];
+        Q->d1[j] = Hn.d1[j];
+    }
+}
+
 template <int N>
 void fill_tab(const dg::HostTables& H, void* out)
 {
@@ -417,6 +489,9 @@ struct dg_ctx {
     TileInfo tinfo;
     bool gen;
     GenInfo ginfo;
+    int m;     // Gauss points per direction
+    bool quad; // m = n + 1: k_quad
+    alignas(16) unsigned char qtab[sizeof(dg::QTab<dg::kMaxN, dg::kMaxN + 1>)];
     int gen_chunk;
     alignas(16) unsigned char eotab[sizeof(dg::EOTab<dg::kMaxN>)];
     int ax8_tile, ax8_T1, ax8_T2, ax8_chunk;
@@ -466,6 +541,10 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         }
         return cudaGetLastError();
     }
+    if (c->quad) {
+        const long long pcq = c->M.plane_cells;
+        return c->launch(c->qtab, c->M, x, xb, xa, r, (long long)p0 * pcq, (long long)p1 * pcq, st, nullptr);
+    }
     if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo, c->d_ctab, c->d_cface);
     if (c->tile) return c->tinfo.fn(c->tab, c->M, x, xb, xa, r, p0, p1, st, c->d_geo);
     const long long pc = c->M.plane_cells;
@@ -504,7 +583,8 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (!mesh || !out) return fail(DG_ERR_INVALID, "dg_setup: NULL argument");
     *out = nullptr;
     if (k < 1 || k > 7) return fail(DG_ERR_INVALID, "dg_setup: k=%d outside [1,7]", k);
-    if (quad != k + 1) return fail(DG_ERR_UNSUPPORTED, "dg_setup: quad=%d != k+1 (collocation only)", quad);
+    if (quad != k + 1 && quad != k + 2)
+        return fail(DG_ERR_UNSUPPORTED, "dg_setup: quad=%d (supported: k+1 collocation, k+2 overintegration)", quad);
     for (int d = 0; d < 3; ++d)
         if (mesh->N[d] < 2) return fail(DG_ERR_INVALID, "dg_setup: N[%d]=%d < 2", d, mesh->N[d]);
     if (mesh->plane_begin < 0 || mesh->plane_begin >= mesh->N[0] || mesh->nplanes < 1 || mesh->nplanes > mesh->N[0])
@@ -570,8 +650,36 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     }
     c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
     c->kname = "k_cell_general";
+    c->m = quad;
+    c->quad = quad == k + 2;
+    if (c->quad) {
+        // overintegration: m = n + 1 Gauss points, interpolation A != I -> k_quad
+        dg::HostTables Hm;
+        if (dg::build_tables(quad, &Hm)) {
+            if (c->d_jac) cudaFree(c->d_jac);
+            free(c);
+            return fail(DG_ERR_INVALID, "tables m=%d", quad);
+        }
+        switch (n) {
+        case 2: fill_qtab<2>(H, Hm, c->qtab); break;
+        case 3: fill_qtab<3>(H, Hm, c->qtab); break;
+        case 4: fill_qtab<4>(H, Hm, c->qtab); break;
+        case 5: fill_qtab<5>(H, Hm, c->qtab); break;
+        case 6: fill_qtab<6>(H, Hm, c->qtab); break;
+        case 7: fill_qtab<7>(H, Hm, c->qtab); break;
+        case 8: fill_qtab<8>(H, Hm, c->qtab); break;
+        }
+        cudaError_t e = cudaSuccess;
+        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e);
+        if (e != cudaSuccess) {
+            if (c->d_jac) cudaFree(c->d_jac);
+            free(c);
+            return fail(DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
+        }
+        c->kname = "k_quad";
+    }
     // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
-    {
+    if (!c->quad) {
         c->tinfo = pick_tile(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
         const int64_t rowb = (int64_t)c->tinfo.T2 * n3 * 8;
         const bool rows_aligned = (rowb % 16 == 0) && ((n3 * 8) % 16 == 0 || (mesh->N[2] % 2 == 0 && c->tinfo.T2 % 2 == 0));
@@ -654,7 +762,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         if (c->gen) c->kname = "k_gen";
     }
     // axis-aligned Q7 fast path: tile T1 x T2 (env DG_AX8_TILE picks an AX8_VARIANTS entry for experiments)
-    {
+    if (!c->quad) {
         const char* tv = getenv("DG_AX8_TILE");
         c->ax8_tile = 0;
         c->ax8_T1 = 2;
@@ -759,6 +867,16 @@ double dg_alg_flops(const dg_ctx* c)
     if (!c) return -1.0;
     const double n = c->n;
     double F;
+    if (c->quad) {
+        // general quadrature (k_quad, m points): the sum-factorisation contractions as executed (A != I):
+        // volume 2 (4 n^3 m + 6 n^2 m^2 + 6 n m^3) + (21 + Cc) m^3 per cell; each face once:
+        // 2 (8 n^3 + 9 n^2 m + 12 n m^2) + (40 + Cc) m^2 (traces both sides, interpolation / tangential
+        // derivatives to the m^2 points, flux, back-projection)
+        const double m = c->m, Cc = (c->mesh.coeff_kind == DG_COEFF_SINCOS) ? 16.0 : 0.0;
+        const double vol = 2.0 * (4 * n * n * n * m + 6 * n * n * m * m + 6 * n * m * m * m) + (21.0 + Cc) * m * m * m;
+        const double face = 2.0 * (8 * n * n * n + 9 * n * n * m + 12 * n * m * m) + (40.0 + Cc) * m * m;
+        return (vol + 3.0 * face) / (n * n * n) * (double)c->local_dofs;
+    }
     if (c->mesh.geom_kind == DG_GEOM_AXIS && c->mesh.coeff_kind == DG_COEFF_ONE)
         F = 12.0 * n + 51.0 + 30.0 / n;
     else {

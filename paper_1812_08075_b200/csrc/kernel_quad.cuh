@@ -1,0 +1,420 @@
+// K_quad: the SIPG operator with a general Gauss rule of M > n points per direction (SURVEY §8(f2):
+// overintegration, "quadrature with m points"), i.e. the paper's general sum factorisation
+// with interpolation A = [l_j(xi_q)] != I (Eq. lowcomplex, Alg. assembly):
+//
+//   stage 1  grad_hat U at the M^3 points:  d0 = D0 A1 A2 X,  d1 = A0 D1 A2 X,  d2 = A0 A1 D2 X
+//            (shared partial contractions: A2 X / D2 X along j2 first, then j1, then j0)
+//   stage 2  Q = w_q c(x_q) |det J| J^{-1} J^{-T} grad_hat U at the M^3 points
+//   stage 3  R = D0^T A1^T A2^T Q0 + A0^T D1^T A2^T Q1 + A0^T A1^T D2^T Q2  (transposes, reverse order)
+//   faces    traces along the face normal with the 1-point tables e, d (normal first
+//            P:L884), then A (values, normal derivative) and D (tangential derivatives) on the face to
+//            its M^2 points, SIPG flux (Eq. diffreac_weak, theta = -1, geometry of T- R11,
+//            c_F at the T- mapped points R12), back-projection with the transposed face contractions.
+//
+// Cell-centric (each cell evaluates its 6 faces with the neighbour's traces read from L2; r written
+// once); CPB cells per CTA, every contraction a 1D sweep over the lines of a shared-memory array,
+// distributed over the CTA's threads. A correctness-first path for the general case (no config of
+// BASELINE.json uses it); k_gen is the tuned collocation path.
+#pragma once
+
+#include "common.cuh"
+
+namespace dg {
+
+template <int N, int M>
+struct QTab {
+    double A[M * N];  // A[q*N + j] = l_j(xi_q) at the M Gauss points (basis: Lagrange on the N Gauss nodes)
+    double Dq[M * N]; // l_j'(xi_q)
+    double wq[M], xq[M];
+    double e0[N], e1[N], d0[N], d1[N];
+};
+
+namespace qd {
+
+// 1D contraction along dimension DIM of a 3D array with extents (E0, E1, E2) (dimension 0 fastest):
+// out[.., q, ..] (+)= sum_j T(q, j) in[.., j, ..]; T(q, j) = TRN ? T[j*LO + q] : T[q*LIN + j].
+template <int E0, int E1, int E2, int DIM, int LO, bool TRN, bool ACC>
+struct Sw3 {
+    static constexpr int LIN = DIM == 0 ? E0 : (DIM == 1 ? E1 : E2);
+    static constexpr int NL = (E0 * E1 * E2) / LIN; // lines
+    static constexpr int O0 = DIM == 0 ? LO : E0, O1 = DIM == 1 ? LO : E1;
+    __device__ static void line(const double* in, double* out, const double* T, int l)
+    {
+        int ib, ist, ob, ost;
+        if (DIM == 0) { ib = E0 * l; ist = 1; ob = O0 * l; ost = 1; }
+        else if (DIM == 1) { const int i0 = l % E0, i2 = l / E0; ib = i0 + E0 * E1 * i2; ist = E0; ob = i0 + O0 * O1 * i2; ost = O0; }
+        else { ib = l; ist = E0 * E1; ob = l; ost = O0 * O1; }
+        double v[LIN];
+#pragma unroll
+        for (int j = 0; j < LIN; ++j) v[j] = in[ib + ist * j];
+#pragma unroll
+        for (int q = 0; q < LO; ++q) {
+            double a = 0.0;
+#pragma unroll
+            for (int j = 0; j < LIN; ++j) a = fma(TRN ? T[j * LO + q] : T[q * LIN + j], v[j], a);
+            out[ob + ost * q] = ACC ? out[ob + ost * q] + a : a;
+        }
+    }
+};
+
+// the same for a 2D array with extents (E0, E1)
+template <int E0, int E1, int DIM, int LO, bool TRN, bool ACC>
+struct Sw2 {
+    static constexpr int LIN = DIM == 0 ? E0 : E1;
+    static constexpr int NL = (E0 * E1) / LIN;
+    static constexpr int O0 = DIM == 0 ? LO : E0;
+    __device__ static void line(const double* in, double* out, const double* T, int l)
+    {
+        const int ib = DIM == 0 ? E0 * l : l, ist = DIM == 0 ? 1 : E0;
+        const int ob = DIM == 0 ? O0 * l : l, ost = DIM == 0 ? 1 : O0;
+        double v[LIN];
+#pragma unroll
+        for (int j = 0; j < LIN; ++j) v[j] = in[ib + ist * j];
+#pragma unroll
+        for (int q = 0; q < LO; ++q) {
+            double a = 0.0;
+#pragma unroll
+            for (int j = 0; j < LIN; ++j) a = fma(TRN ? T[j * LO + q] : T[q * LIN + j], v[j], a);
+            out[ob + ost * q] = ACC ? out[ob + ost * q] + a : a;
+        }
+    }
+};
+
+template <int N, int M>
+struct QLay {
+    static constexpr int CPB = (N <= 5) ? 2 : 1;
+    static constexpr int NT = 256;
+    static constexpr int N2 = N * N, N3 = N * N * N, M2 = M * M, M3 = M * M * M, NM = N * M;
+    // per cell (doubles)
+    static constexpr int X = 0, R = X + N3, Y2 = R + N3, Y2d = Y2 + N2 * M, Z = Y2d + N2 * M, Zd1 = Z + N * M2,
+                         Zd2 = Zd1 + N * M2, G0 = Zd2 + N * M2, G1 = G0 + M3, G2 = G1 + M3;
+    // per face: FT [4][N2] (own u, own g, nb u, nb g) -> later FB2 [2][N2] (V2, G2)
+    //           F1 [6][NM] (own Ua1, Ud1, Ga1; nb Ua1, Ud1, Ga1) -> later FB1 [3][NM] (Pv, Pt, Pn)
+    //           F2 [8][M2] (U-, U+, Gn-, Gn+, Gt1-, Gt1+, Gt2-, Gt2+) -> coefficients [4][M2] (Cv, Ct1, Ct2, Cn)
+    static constexpr int FACE = 4 * N2 + 6 * NM + 8 * M2;
+    static constexpr int F = G2 + M3;
+    static constexpr int GEO = F + 6 * FACE; // per cell: Gt[6], J rows 0-1 [6], o[2]; per face 16: dS, a-[3], a+[3], Jm rows 0-1 [6], om[2], pad
+    static constexpr int CELL = GEO + 14 + 6 * 16;
+    static constexpr int CELLP = (CELL + 1) / 2 * 2;
+    static constexpr int TAB = CPB * CELLP;   // shared tables: A, Dq (M N each), wq, xq (M), e0, e1, d0, d1 (N)
+    static constexpr int END = TAB + 2 * M * N + 2 * M + 4 * N;
+    static constexpr int BYTES = END * 8;
+};
+
+} // namespace qd
+
+// grid: ceil(cells / CPB), block NT, dynamic smem QLay::BYTES. Cells [c_begin, c_end) of the slab
+// (local, canonical order).
+template <int N, int M, bool AFFINE, bool COEFF>
+__global__ void __launch_bounds__(256)
+k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
+       long long c_begin, long long c_end, const QTab<N, M> T, const MeshArgs M_)
+{
+    using L = qd::QLay<N, M>;
+    constexpr int CPB = L::CPB, NT = L::NT, N2 = L::N2, N3 = L::N3, M2 = L::M2, M3 = L::M3, NM = L::NM;
+    const MeshArgs& Ms = M_;
+    extern __shared__ __align__(16) double sm[];
+    double* const sA = sm + L::TAB;
+    double* const sDq = sA + M * N;
+    double* const sw = sDq + M * N;
+    double* const sxq = sw + M;
+    double* const se0 = sxq + M;
+    double* const se1 = se0 + N;
+    double* const sd0 = se1 + N;
+    double* const sd1 = sd0 + N;
+    const int tid = threadIdx.x;
+    const long long cfirst = c_begin + (long long)blockIdx.x * CPB;
+    const int ncell = (int)min((long long)CPB, c_end - cfirst);
+    auto cellp = [&](int c) { return sm + c * L::CELLP; };
+    auto facep = [&](int c, int f) { return cellp(c) + L::F + f * L::FACE; };
+
+    for (int i = tid; i < M * N; i += NT) { sA[i] = T.A[i]; sDq[i] = T.Dq[i]; }
+    for (int i = tid; i < M; i += NT) { sw[i] = T.wq[i]; sxq[i] = T.xq[i]; }
+    for (int i = tid; i < N; i += NT) { se0[i] = T.e0[i]; se1[i] = T.e1[i]; sd0[i] = T.d0[i]; sd1[i] = T.d1[i]; }
+    for (int c = 0; c < ncell; ++c)
+        for (int i = tid; i < N3; i += NT) cellp(c)[L::X + i] = __ldg(x + (cfirst + c) * N3 + i);
+
+    // cell coordinates
+    auto coords = [&](int c, int& lp, int& rem, int ig[3]) {
+        const long long lc = cfirst + c;
+        lp = (int)(lc / Ms.plane_cells);
+        rem = (int)(lc % Ms.plane_cells);
+        ig[0] = (Ms.plane_begin + lp) % Ms.N0;
+        ig[1] = rem / Ms.N2;
+        ig[2] = rem % Ms.N2;
+    };
+    auto jac_of = [&](int lp, int rem, double* J) {
+        const double* jp = Ms.jac + ((long long)(lp + 1) * Ms.plane_cells + rem) * 9;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) J[i] = __ldg(jp + i);
+    };
+    // neighbour (local plane, in-plane index, global coords) across face (d, side)
+    auto neighbour = [&](int lp, int rem, const int ig[3], int d, int side, int& nlp, int& nrem, int nig[3]) {
+        const int Nd = d == 0 ? Ms.N0 : (d == 1 ? Ms.N1 : Ms.N2);
+        nig[0] = ig[0]; nig[1] = ig[1]; nig[2] = ig[2];
+        nig[d] = (ig[d] + (side ? 1 : Nd - 1)) % Nd;
+        nlp = lp;
+        nrem = rem;
+        if (d == 0) nlp = lp + (side ? 1 : -1);
+        else nrem = nig[1] * Ms.N2 + nig[2];
+    };
+
+    // ---------------- P0: geometry (one thread per cell for the volume, per (cell, face) for the faces) --------
+    for (int t = tid; t < ncell * 7; t += NT) {
+        const int c = t / 7, f = t % 7;
+        int lp, rem, ig[3];
+        coords(c, lp, rem, ig);
+        double J[9], Ji[9];
+        if (AFFINE) jac_of(lp, rem, J);
+        else { for (int i = 0; i < 9; ++i) J[i] = 0.0; J[0] = Ms.h[0]; J[4] = Ms.h[1]; J[8] = Ms.h[2]; }
+        const double det = inv3(J, Ji);
+        double* g = cellp(c) + L::GEO;
+        if (f == 6) {
+            const double ad = fabs(det);
+            auto gg = [&](int a, int b) { return ad * (Ji[3 * a] * Ji[3 * b] + Ji[3 * a + 1] * Ji[3 * b + 1] + Ji[3 * a + 2] * Ji[3 * b + 2]); };
+            g[0] = gg(0, 0); g[1] = gg(1, 1); g[2] = gg(2, 2); g[3] = gg(0, 1); g[4] = gg(0, 2); g[5] = gg(1, 2);
+            for (int i = 0; i < 6; ++i) g[6 + i] = J[i];
+            g[12] = (double)ig[0] / Ms.N0;
+            g[13] = (double)ig[1] / Ms.N1;
+            continue;
+        }
+        const int d = f >> 1, side = f & 1; // face f = 2d + side; side 1: upper face (cell is T-)
+        int nlp, nrem, nig[3];
+        neighbour(lp, rem, ig, d, side, nlp, nrem, nig);
+        double Jn[9], Jni[9];
+        if (AFFINE) jac_of(nlp, d == 0 ? rem : nrem, Jn);
+        else for (int i = 0; i < 9; ++i) Jn[i] = J[i];
+        inv3(Jn, Jni);
+        const double* Jm = side ? J : Jn;   // T-
+        const double* Jmi = side ? Ji : Jni;
+        const double* Jpi = side ? Jni : Ji;
+        const double detm = side ? det : det3(Jn);
+        const double nu0 = Jmi[3 * d], nu1 = Jmi[3 * d + 1], nu2 = Jmi[3 * d + 2];
+        const double nn = sqrt(nu0 * nu0 + nu1 * nu1 + nu2 * nu2);
+        const double n0 = nu0 / nn, n1 = nu1 / nn, n2 = nu2 / nn;
+        double* fg = g + 14 + 16 * f;
+        fg[0] = fabs(detm) * nn; // dS (Nanson)
+        for (int e = 0; e < 3; ++e) {
+            fg[1 + e] = Jmi[3 * e] * n0 + Jmi[3 * e + 1] * n1 + Jmi[3 * e + 2] * n2; // a- = J_-^{-1} n_F
+            fg[4 + e] = Jpi[3 * e] * n0 + Jpi[3 * e + 1] * n1 + Jpi[3 * e + 2] * n2; // a+ = J_+^{-1} n_F
+        }
+        for (int i = 0; i < 6; ++i) fg[7 + i] = Jm[i];
+        const int* mig = side ? ig : nig;
+        fg[13] = (double)mig[0] / Ms.N0;
+        fg[14] = (double)mig[1] / Ms.N1;
+        fg[15] = 0.0;
+    }
+    __syncthreads();
+
+    // ---------------- P1: stage 1a (along j2); face traces along the normal (own from smem, neighbour from L2) ----
+    {
+        using S = qd::Sw3<N, N, N, 2, M, false, false>;
+        for (int t = tid; t < ncell * 2 * S::NL; t += NT) {
+            const int c = t / (2 * S::NL), k = (t / S::NL) % 2, l = t % S::NL;
+            double* b = cellp(c);
+            S::line(b + L::X, b + (k ? L::Y2d : L::Y2), k ? sDq : sA, l);
+        }
+        for (int t = tid; t < ncell * 6 * N2; t += NT) {
+            const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
+            const int d = f >> 1, side = f & 1;
+            int lp, rem, ig[3];
+            coords(c, lp, rem, ig);
+            int nlp, nrem, nig[3];
+            neighbour(lp, rem, ig, d, side, nlp, nrem, nig);
+            const double* nbx;
+            if (d == 0) nbx = nlp < 0 ? xb + (long long)rem * N3 : (nlp >= Ms.L ? xa + (long long)rem * N3 : x + ((long long)nlp * Ms.plane_cells + rem) * N3);
+            else nbx = x + ((long long)lp * Ms.plane_cells + nrem) * N3;
+            const double* xo = cellp(c) + L::X;
+            double uo = 0, go = 0, un = 0, gn = 0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double vo = xo[pidx<N>(d, j, a, bq)];
+                const double vn = __ldg(nbx + pidx<N>(d, j, a, bq));
+                uo = fma(side ? se1[j] : se0[j], vo, uo);
+                go = fma(side ? sd1[j] : sd0[j], vo, go);
+                un = fma(side ? se0[j] : se1[j], vn, un);
+                gn = fma(side ? sd0[j] : sd1[j], vn, gn);
+            }
+            double* FT = facep(c, f);
+            FT[p] = uo;
+            FT[N2 + p] = go;
+            FT[2 * N2 + p] = un;
+            FT[3 * N2 + p] = gn;
+        }
+    }
+    __syncthreads();
+    // ---------------- P2: stage 1b (along j1); face contraction along t1 ----------------
+    {
+        using SA = qd::Sw3<N, N, M, 1, M, false, false>;
+        for (int t = tid; t < ncell * 3 * SA::NL; t += NT) {
+            const int c = t / (3 * SA::NL), k = (t / SA::NL) % 3, l = t % SA::NL;
+            double* b = cellp(c);
+            if (k == 0) SA::line(b + L::Y2, b + L::Z, sA, l);
+            else if (k == 1) SA::line(b + L::Y2, b + L::Zd1, sDq, l);
+            else SA::line(b + L::Y2d, b + L::Zd2, sA, l);
+        }
+        using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
+        for (int t = tid; t < ncell * 6 * 6 * F::NL; t += NT) {
+            const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
+            double* FT = facep(c, f);
+            double* F1 = FT + 4 * N2;
+            // k: 0 own Ua1 = A u, 1 own Ud1 = D u, 2 own Ga1 = A g, 3..5 the same for the neighbour
+            const double* src = FT + ((k < 3) ? (k == 2 ? N2 : 0) : (k == 5 ? 3 * N2 : 2 * N2));
+            F::line(src, F1 + k * NM, (k % 3 == 1) ? sDq : sA, l);
+        }
+    }
+    __syncthreads();
+    // ---------------- P3: stage 1c (along j0); face contraction along t2 ----------------
+    {
+        using SB = qd::Sw3<N, M, M, 0, M, false, false>;
+        for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
+            const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
+            double* b = cellp(c);
+            if (k == 0) SB::line(b + L::Z, b + L::G0, sDq, l);
+            else if (k == 1) SB::line(b + L::Zd1, b + L::G1, sA, l);
+            else SB::line(b + L::Zd2, b + L::G2, sA, l);
+        }
+        using F = qd::Sw2<M, N, 1, M, false, false>; // M x N -> M x M
+        for (int t = tid; t < ncell * 6 * 8 * F::NL; t += NT) {
+            const int c = t / (48 * F::NL), f = (t / (8 * F::NL)) % 6, k = (t / F::NL) % 8, l = t % F::NL;
+            double* F1 = facep(c, f) + 4 * N2;
+            double* F2 = F1 + 6 * NM;
+            // outputs (side s = 0 own, 1 neighbour): U_s = A Ua1_s, Gn_s = A Ga1_s, Gt1_s = A Ud1_s, Gt2_s = D Ua1_s
+            const int s = k & 1, q = k >> 1; // q: 0 U, 1 Gn, 2 Gt1, 3 Gt2
+            const double* src = F1 + (3 * s + (q == 0 || q == 3 ? 0 : (q == 1 ? 2 : 1))) * NM;
+            F::line(src, F2 + k * M2, q == 3 ? sDq : sA, l);
+        }
+    }
+    __syncthreads();
+    // ---------------- P4: stage 2 (pointwise at the M^3 points); face fluxes at the M^2 points ----------------
+    for (int t = tid; t < ncell * M3; t += NT) {
+        const int c = t / M3, P = t % M3, q0 = P % M, q1 = (P / M) % M, q2 = P / M2;
+        double* b = cellp(c);
+        const double* g = b + L::GEO;
+        double cW = sw[q0] * sw[q1] * sw[q2];
+        if (COEFF) {
+            const double xi0 = sxq[q0], xi1 = sxq[q1], xi2 = sxq[q2];
+            cW *= coeff_sincos(g[12] + g[6] * xi0 + g[7] * xi1 + g[8] * xi2, g[13] + g[9] * xi0 + g[10] * xi1 + g[11] * xi2);
+        }
+        const double a0 = b[L::G0 + P], a1 = b[L::G1 + P], a2 = b[L::G2 + P];
+        b[L::G0 + P] = cW * fma(g[0], a0, fma(g[3], a1, g[4] * a2));
+        b[L::G1 + P] = cW * fma(g[3], a0, fma(g[1], a1, g[5] * a2));
+        b[L::G2 + P] = cW * fma(g[4], a0, fma(g[5], a1, g[2] * a2));
+    }
+    for (int t = tid; t < ncell * 6 * M2; t += NT) {
+        const int c = t / (6 * M2), f = (t / M2) % 6, p = t % M2, a = p % M, bq = p / M;
+        const int d = f >> 1, side = f & 1;
+        const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+        double* F2 = facep(c, f) + 4 * N2 + 6 * NM;
+        const double* fg = cellp(c) + L::GEO + 14 + 16 * f;
+        // own (s=0) and neighbour (s=1) -> T- / T+
+        const double Uo = F2[0 * M2 + p], Un = F2[1 * M2 + p], Gno = F2[2 * M2 + p], Gnn = F2[3 * M2 + p];
+        const double T1o = F2[4 * M2 + p], T1n = F2[5 * M2 + p], T2o = F2[6 * M2 + p], T2n = F2[7 * M2 + p];
+        const double um = side ? Uo : Un, up = side ? Un : Uo;
+        const double gnm = side ? Gno : Gnn, gnp = side ? Gnn : Gno;
+        const double t1m = side ? T1o : T1n, t1p = side ? T1n : T1o;
+        const double t2m = side ? T2o : T2n, t2p = side ? T2n : T2o;
+        const double* am = fg + 1;
+        const double* ap = fg + 4;
+        double cF = 1.0;
+        if (COEFF) {
+            double xi[3];
+            xi[d] = 1.0;
+            xi[t1] = sxq[a];
+            xi[t2] = sxq[bq];
+            cF = coeff_sincos(fg[13] + fg[7] * xi[0] + fg[8] * xi[1] + fg[9] * xi[2],
+                              fg[14] + fg[10] * xi[0] + fg[11] * xi[1] + fg[12] * xi[2]);
+        }
+        const double gm = cF * (am[d] * gnm + am[t1] * t1m + am[t2] * t2m);
+        const double gp = cF * (ap[d] * gnp + ap[t1] * t1p + ap[t2] * t2p);
+        const double W = sw[a] * sw[bq] * fg[0];
+        const double jump = um - up;
+        const double avg = 0.5 * (gm + gp);
+        const double gam = Ms.gamma[d];
+        const double Cvm = W * (-avg + gam * jump);
+        const double Cg = -0.5 * W * jump * cF;
+        const double* ao = side ? am : ap;
+        F2[0 * M2 + p] = side ? Cvm : -Cvm; // value coefficient of this cell's side
+        F2[1 * M2 + p] = ao[t1] * Cg;       // tangential-gradient coefficients (a_self . e_t Cg)
+        F2[2 * M2 + p] = ao[t2] * Cg;
+        F2[3 * M2 + p] = ao[d] * Cg;        // normal-gradient coefficient
+    }
+    __syncthreads();
+    // ---------------- P5: stage 3a (D0^T / A0^T along j0); face back-projection along t2 ----------------
+    {
+        using SB = qd::Sw3<M, M, M, 0, N, true, false>; // M^3 -> N x M x M
+        for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
+            const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
+            double* b = cellp(c);
+            if (k == 0) SB::line(b + L::G0, b + L::Z, sDq, l);       // V
+            else if (k == 1) SB::line(b + L::G1, b + L::Zd1, sA, l); // W1
+            else SB::line(b + L::G2, b + L::Zd2, sA, l);             // W2
+        }
+        // Pv = A^T_t2 Cv + D^T_t2 Ct2, Pt = A^T_t2 Ct1, Pn = A^T_t2 Cn   ([t1 = M][t2 = N])
+        using F = qd::Sw2<M, M, 1, N, true, false>;
+        using FA = qd::Sw2<M, M, 1, N, true, true>;
+        for (int t = tid; t < ncell * 6 * 3 * F::NL; t += NT) {
+            const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
+            double* F1 = facep(c, f) + 4 * N2;
+            const double* C = F1 + 6 * NM;
+            if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, sA, l); FA::line(C + 2 * M2, F1 + 0 * NM, sDq, l); }
+            else if (k == 1) F::line(C + 1 * M2, F1 + 1 * NM, sA, l);
+            else F::line(C + 3 * M2, F1 + 2 * NM, sA, l);
+        }
+    }
+    __syncthreads();
+    // ---------------- P6: stage 3b (along j1); face back-projection along t1 ----------------
+    {
+        using SA = qd::Sw3<N, M, M, 1, N, true, false>;  // N x M x M -> N x N x M
+        using SAa = qd::Sw3<N, M, M, 1, N, true, true>;
+        for (int t = tid; t < ncell * 2 * SA::NL; t += NT) {
+            const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
+            double* b = cellp(c);
+            if (k == 0) { SA::line(b + L::Z, b + L::Y2, sA, l); SAa::line(b + L::Zd1, b + L::Y2, sDq, l); } // Ya
+            else SA::line(b + L::Zd2, b + L::Y2d, sA, l);                                                   // Yb
+        }
+        // V2 = A^T_t1 Pv + D^T_t1 Pt, G2 = A^T_t1 Pn   ([t1 = N][t2 = N], into FT)
+        using F = qd::Sw2<M, N, 0, N, true, false>;
+        using FA = qd::Sw2<M, N, 0, N, true, true>;
+        for (int t = tid; t < ncell * 6 * 2 * F::NL; t += NT) {
+            const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
+            double* FT = facep(c, f);
+            const double* P = FT + 4 * N2;
+            if (k == 0) { F::line(P + 0 * NM, FT, sA, l); FA::line(P + 1 * NM, FT, sDq, l); }
+            else F::line(P + 2 * NM, FT + N2, sA, l);
+        }
+    }
+    __syncthreads();
+    // ---------------- P7: stage 3c (along j2) into R ----------------
+    {
+        using S = qd::Sw3<N, N, M, 2, N, true, false>;
+        using Sa = qd::Sw3<N, N, M, 2, N, true, true>;
+        for (int t = tid; t < ncell * S::NL; t += NT) {
+            const int c = t / S::NL, l = t % S::NL;
+            double* b = cellp(c);
+            S::line(b + L::Y2, b + L::R, sA, l);
+            Sa::line(b + L::Y2d, b + L::R, sDq, l);
+        }
+    }
+    __syncthreads();
+    // ---------------- P8: add the face back-projections along the normals, write r once ----------------
+    for (int t = tid; t < ncell * N3; t += NT) {
+        const int c = t / N3, P = t % N3;
+        const int j[3] = {P % N, (P / N) % N, P / N2};
+        double v = cellp(c)[L::R + P];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+            const int p = j[t1] + N * j[t2];
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                const double* FT = facep(c, 2 * d + side);
+                const double e = side ? se1[j[d]] : se0[j[d]], dd = side ? sd1[j[d]] : sd0[j[d]];
+                v = fma(e, FT[p], fma(dd, FT[N2 + p], v));
+            }
+        }
+        r[(cfirst + c) * N3 + P] = v;
+    }
+}
+
+} // namespace dg

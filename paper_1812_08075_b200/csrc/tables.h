@@ -8,7 +8,7 @@
 
 namespace dg {
 
-constexpr int kMaxN = 8;
+constexpr int kMaxN = 9; // n <= 8 basis functions; Gauss rules up to m = 9 points (overintegration)
 
 struct HostTables {
     int n;

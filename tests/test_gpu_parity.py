@@ -22,7 +22,7 @@ def _op(w, **kw):
     from paper_1812_08075_b200 import Operator
     jac = synth.jac_planes_torch(w, -1, w.N[0] + 2, device="cuda").cpu().numpy() if w.geom_kind else None
     return Operator(w.N, w.k, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind, penalty_scale=w.penalty_scale,
-                    jac=jac, **kw)
+                    jac=jac, quad=w.m, **kw)
 
 
 def _rel(a, b):
@@ -309,3 +309,78 @@ def test_gen_slab_loopback_bitwise(world):
         op.close()
     assert torch.equal(got, ref)
     full.close()
+
+
+@pytest.mark.parametrize("k", range(1, 8))
+@pytest.mark.parametrize("geom,coeff", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_quad_overintegration(k, geom, coeff):
+    """General quadrature: k+2 Gauss points per direction, A != I (k_quad), every
+    degree and geometry/coefficient combination, against the oracle evaluated with the same rule;
+    meshes with ragged CTA tails (odd cell counts)."""
+    N = (3, 2, 5) if k >= 5 else (3, 3, 5)
+    w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=500 + k, quad=k + 2)
+    op = _op(w)
+    assert op.kernel_name == "k_quad"
+    op.close()
+    assert _full_check(w) <= TOL
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_quad_equals_collocation_for_polynomial_integrands(k):
+    """With c = 1 both rules integrate exactly: the k+2-point operator (k_quad) equals the collocated
+    one (k_gen) to rounding on an affine mesh."""
+    w1 = synth.small(k, (4, 4, 4), geom_kind=1, coeff_kind=0, seed=77)
+    w2 = synth.small(k, (4, 4, 4), geom_kind=1, coeff_kind=0, seed=77, quad=k + 2)
+    x = synth.x_torch(w1, device="cuda")
+    a, b = _op(w1), _op(w2)
+    ra, rb = a.apply(x), b.apply(x)
+    assert b.kernel_name == "k_quad"
+    assert (ra - rb).abs().max().item() <= 1e-12 * ra.abs().max().item()
+    a.close()
+    b.close()
+
+
+def test_quad_rejects_unsupported_rules():
+    from paper_1812_08075_b200 import DgError, dg
+    with pytest.raises(DgError) as ei:
+        dg.dg_setup((4, 4, 4), 2, 5)
+    assert ei.value.code == dg.DG_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_quad_slab_loopback_bitwise(world):
+    """k_quad in the slab decomposition (halo planes from the neighbours) equals the whole-mesh apply."""
+    from paper_1812_08075_b200 import Operator, slab
+    w = synth.small(3, (6, 3, 4), geom_kind=1, coeff_kind=1, seed=43, quad=5)
+    full = _op(w)
+    x = synth.x_torch(w, device="cuda")
+    ref = full.apply(x)
+    pd = full.plane_ndofs
+    got = torch.full_like(x, float("nan"))
+    for q in range(world):
+        p = slab.plan(w.N[0], q, world)
+        jac = synth.jac_planes_torch(w, p.plane_begin - 1, p.nplanes + 2).numpy()
+        op = Operator(w.N, w.k, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind, penalty_scale=w.penalty_scale,
+                      jac=jac, plane_begin=p.plane_begin, nplanes=p.nplanes, quad=w.m)
+        xs = x[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        rs = got[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        hb = x[((p.plane_begin - 1) % w.N[0]) * pd:][:pd].clone()
+        ha = x[((p.plane_begin + p.nplanes) % w.N[0]) * pd:][:pd].clone()
+        a, b = p.interior
+        if b > a:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        for a, b in p.boundary:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        torch.cuda.synchronize()
+        op.close()
+    assert torch.equal(got, ref)
+    full.close()
+
+
+def test_quad_config_sampled():
+    """k_quad at the full size of cfg2 (Q5 on 64^3 affine cells, c(x)) with 7 Gauss points per direction,
+    on the deterministic cell sample (slab-boundary and wrap planes, random cells)."""
+    import dataclasses
+    w = dataclasses.replace(synth.CONFIGS[2], quad=7)
+    cells = synth.sample_cells(w, nrandom=1500, plane_cap=48, wrap_plane_cells=64)
+    assert _sampled_check(w, cells) <= TOL

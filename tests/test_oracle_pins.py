@@ -309,3 +309,33 @@ def test_cells_local_matches_full():
     # the listed-cells mode of oracle_apply too
     rs = oracle.apply(w, x, jac, cells=cells)
     np.testing.assert_array_equal(rs.reshape(w.ncells, -1)[cells], rl)
+
+
+@pytest.mark.parametrize("k,N,geom", [(1, (3, 2, 4), 0), (2, (2, 3, 3), 1), (3, (2, 2, 3), 1), (4, (2, 2, 2), 0)])
+def test_overintegration_exact_for_polynomial_integrands(k, N, geom):
+    """General quadrature m > k+1 (SURVEY §8(f2), P:L811 'quadrature with m points'): with c = 1 every
+    volume and face integrand is a polynomial of degree <= 2k per direction (affine: constant metric), so
+    the k+1- and k+2/k+3-point Gauss rules give the same operator to rounding — pins the oracle's
+    general-m path (interpolation A != I at the quadrature points) against the pinned m = k+1 path."""
+    w1 = synth.small(k, N, geom_kind=geom, coeff_kind=0, seed=9)
+    jac = synth.jac_cells_np(w1, np.arange(w1.ncells)) if geom else None
+    x = synth.x_np(w1)
+    r1 = oracle.apply(w1, x, jac)
+    for q in (k + 2, k + 3):
+        wq = synth.small(k, N, geom_kind=geom, coeff_kind=0, seed=9, quad=q)
+        rq = oracle.apply(wq, x, jac)
+        assert np.abs(rq - r1).max() <= 1e-12 * np.abs(r1).max()
+
+
+def test_overintegration_changes_nonpolynomial_coefficient():
+    """With c(x) = 1 + 0.5 sin cos the integrand is not polynomial: k+2 points give a different (more
+    accurate) operator, converging as m grows (the difference m = k+2 vs k+5 is below that of k+1 vs k+5)."""
+    k, N = 2, (3, 3, 2)
+    ws = [synth.small(k, N, geom_kind=1, coeff_kind=1, seed=4, quad=q) for q in (k + 1, k + 2, k + 5)]
+    jac = synth.jac_cells_np(ws[0], np.arange(ws[0].ncells))
+    x = synth.x_np(ws[0])
+    r = [oracle.apply(w, x, jac) for w in ws]
+    e1 = np.abs(r[0] - r[2]).max()
+    e2 = np.abs(r[1] - r[2]).max()
+    assert e1 > 1e-6 * np.abs(r[2]).max()
+    assert e2 < e1
