@@ -33,6 +33,8 @@ namespace qd {
 
 // 1D contraction along dimension DIM of a 3D array with extents (E0, E1, E2) (dimension 0 fastest):
 // out[.., q, ..] (+)= sum_j T(q, j) in[.., j, ..]; T(q, j) = TRN ? T[j*LO + q] : T[q*LIN + j].
+// T is a table of the kernel parameter (constant bank): the indices are compile-time after unrolling,
+// so the coefficients are uniform operands (no per-FMA shared-memory load).
 template <int E0, int E1, int E2, int DIM, int LO, bool TRN, bool ACC>
 struct Sw3 {
     static constexpr int LIN = DIM == 0 ? E0 : (DIM == 1 ? E1 : E2);
@@ -108,7 +110,7 @@ struct QLay {
 template <int N, int M, bool AFFINE, bool COEFF>
 __global__ void __launch_bounds__(256)
 k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
-       long long c_begin, long long c_end, const QTab<N, M> T, const MeshArgs M_)
+       long long c_begin, long long c_end, const __grid_constant__ QTab<N, M> T, const MeshArgs M_)
 {
     using L = qd::QLay<N, M>;
     constexpr int CPB = L::CPB, NT = L::NT, N2 = L::N2, N3 = L::N3, M2 = L::M2, M3 = L::M3, NM = L::NM;
@@ -212,7 +214,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * 2 * S::NL; t += NT) {
             const int c = t / (2 * S::NL), k = (t / S::NL) % 2, l = t % S::NL;
             double* b = cellp(c);
-            S::line(b + L::X, b + (k ? L::Y2d : L::Y2), k ? sDq : sA, l);
+            if (k) S::line(b + L::X, b + L::Y2d, T.Dq, l);
+            else S::line(b + L::X, b + L::Y2, T.A, l);
         }
         for (int t = tid; t < ncell * 6 * N2; t += NT) {
             const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
@@ -249,9 +252,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * 3 * SA::NL; t += NT) {
             const int c = t / (3 * SA::NL), k = (t / SA::NL) % 3, l = t % SA::NL;
             double* b = cellp(c);
-            if (k == 0) SA::line(b + L::Y2, b + L::Z, sA, l);
-            else if (k == 1) SA::line(b + L::Y2, b + L::Zd1, sDq, l);
-            else SA::line(b + L::Y2d, b + L::Zd2, sA, l);
+            if (k == 0) SA::line(b + L::Y2, b + L::Z, T.A, l);
+            else if (k == 1) SA::line(b + L::Y2, b + L::Zd1, T.Dq, l);
+            else SA::line(b + L::Y2d, b + L::Zd2, T.A, l);
         }
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
         for (int t = tid; t < ncell * 6 * 6 * F::NL; t += NT) {
@@ -260,7 +263,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             double* F1 = FT + 4 * N2;
             // k: 0 own Ua1 = A u, 1 own Ud1 = D u, 2 own Ga1 = A g, 3..5 the same for the neighbour
             const double* src = FT + ((k < 3) ? (k == 2 ? N2 : 0) : (k == 5 ? 3 * N2 : 2 * N2));
-            F::line(src, F1 + k * NM, (k % 3 == 1) ? sDq : sA, l);
+            if (k % 3 == 1) F::line(src, F1 + k * NM, T.Dq, l);
+            else F::line(src, F1 + k * NM, T.A, l);
         }
     }
     __syncthreads();
@@ -270,9 +274,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
             const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
-            if (k == 0) SB::line(b + L::Z, b + L::G0, sDq, l);
-            else if (k == 1) SB::line(b + L::Zd1, b + L::G1, sA, l);
-            else SB::line(b + L::Zd2, b + L::G2, sA, l);
+            if (k == 0) SB::line(b + L::Z, b + L::G0, T.Dq, l);
+            else if (k == 1) SB::line(b + L::Zd1, b + L::G1, T.A, l);
+            else SB::line(b + L::Zd2, b + L::G2, T.A, l);
         }
         using F = qd::Sw2<M, N, 1, M, false, false>; // M x N -> M x M
         for (int t = tid; t < ncell * 6 * 8 * F::NL; t += NT) {
@@ -282,7 +286,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             // outputs (side s = 0 own, 1 neighbour): U_s = A Ua1_s, Gn_s = A Ga1_s, Gt1_s = A Ud1_s, Gt2_s = D Ua1_s
             const int s = k & 1, q = k >> 1; // q: 0 U, 1 Gn, 2 Gt1, 3 Gt2
             const double* src = F1 + (3 * s + (q == 0 || q == 3 ? 0 : (q == 1 ? 2 : 1))) * NM;
-            F::line(src, F2 + k * M2, q == 3 ? sDq : sA, l);
+            if (q == 3) F::line(src, F2 + k * M2, T.Dq, l);
+            else F::line(src, F2 + k * M2, T.A, l);
         }
     }
     __syncthreads();
@@ -318,12 +323,12 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         const double* ap = fg + 4;
         double cF = 1.0;
         if (COEFF) {
-            double xi[3];
-            xi[d] = 1.0;
-            xi[t1] = sxq[a];
-            xi[t2] = sxq[bq];
-            cF = coeff_sincos(fg[13] + fg[7] * xi[0] + fg[8] * xi[1] + fg[9] * xi[2],
-                              fg[14] + fg[10] * xi[0] + fg[11] * xi[1] + fg[12] * xi[2]);
+            const double xa_ = sxq[a], xb_ = sxq[bq];
+            const double xi0 = d == 0 ? 1.0 : xa_;
+            const double xi1 = d == 1 ? 1.0 : (d == 0 ? xa_ : xb_);
+            const double xi2 = d == 2 ? 1.0 : xb_;
+            cF = coeff_sincos(fg[13] + fg[7] * xi0 + fg[8] * xi1 + fg[9] * xi2,
+                              fg[14] + fg[10] * xi0 + fg[11] * xi1 + fg[12] * xi2);
         }
         const double gm = cF * (am[d] * gnm + am[t1] * t1m + am[t2] * t2m);
         const double gp = cF * (ap[d] * gnp + ap[t1] * t1p + ap[t2] * t2p);
@@ -346,9 +351,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
             const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
-            if (k == 0) SB::line(b + L::G0, b + L::Z, sDq, l);       // V
-            else if (k == 1) SB::line(b + L::G1, b + L::Zd1, sA, l); // W1
-            else SB::line(b + L::G2, b + L::Zd2, sA, l);             // W2
+            if (k == 0) SB::line(b + L::G0, b + L::Z, T.Dq, l);       // V
+            else if (k == 1) SB::line(b + L::G1, b + L::Zd1, T.A, l); // W1
+            else SB::line(b + L::G2, b + L::Zd2, T.A, l);             // W2
         }
         // Pv = A^T_t2 Cv + D^T_t2 Ct2, Pt = A^T_t2 Ct1, Pn = A^T_t2 Cn   ([t1 = M][t2 = N])
         using F = qd::Sw2<M, M, 1, N, true, false>;
@@ -357,9 +362,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
             double* F1 = facep(c, f) + 4 * N2;
             const double* C = F1 + 6 * NM;
-            if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, sA, l); FA::line(C + 2 * M2, F1 + 0 * NM, sDq, l); }
-            else if (k == 1) F::line(C + 1 * M2, F1 + 1 * NM, sA, l);
-            else F::line(C + 3 * M2, F1 + 2 * NM, sA, l);
+            if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, T.A, l); FA::line(C + 2 * M2, F1 + 0 * NM, T.Dq, l); }
+            else if (k == 1) F::line(C + 1 * M2, F1 + 1 * NM, T.A, l);
+            else F::line(C + 3 * M2, F1 + 2 * NM, T.A, l);
         }
     }
     __syncthreads();
@@ -370,8 +375,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * 2 * SA::NL; t += NT) {
             const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
             double* b = cellp(c);
-            if (k == 0) { SA::line(b + L::Z, b + L::Y2, sA, l); SAa::line(b + L::Zd1, b + L::Y2, sDq, l); } // Ya
-            else SA::line(b + L::Zd2, b + L::Y2d, sA, l);                                                   // Yb
+            if (k == 0) { SA::line(b + L::Z, b + L::Y2, T.A, l); SAa::line(b + L::Zd1, b + L::Y2, T.Dq, l); } // Ya
+            else SA::line(b + L::Zd2, b + L::Y2d, T.A, l);                                                   // Yb
         }
         // V2 = A^T_t1 Pv + D^T_t1 Pt, G2 = A^T_t1 Pn   ([t1 = N][t2 = N], into FT)
         using F = qd::Sw2<M, N, 0, N, true, false>;
@@ -380,8 +385,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
             double* FT = facep(c, f);
             const double* P = FT + 4 * N2;
-            if (k == 0) { F::line(P + 0 * NM, FT, sA, l); FA::line(P + 1 * NM, FT, sDq, l); }
-            else F::line(P + 2 * NM, FT + N2, sA, l);
+            if (k == 0) { F::line(P + 0 * NM, FT, T.A, l); FA::line(P + 1 * NM, FT, T.Dq, l); }
+            else F::line(P + 2 * NM, FT + N2, T.A, l);
         }
     }
     __syncthreads();
@@ -392,8 +397,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * S::NL; t += NT) {
             const int c = t / S::NL, l = t % S::NL;
             double* b = cellp(c);
-            S::line(b + L::Y2, b + L::R, sA, l);
-            Sa::line(b + L::Y2d, b + L::R, sDq, l);
+            S::line(b + L::Y2, b + L::R, T.A, l);
+            Sa::line(b + L::Y2d, b + L::R, T.Dq, l);
         }
     }
     __syncthreads();
