@@ -43,6 +43,8 @@ def lib():
         L.oracle_apply_cells_local.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                                i64p, ctypes.c_int64, dp, dp, dp]
+        L.oracle_apply_diffreac.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_double, dp, dp, i64p, ctypes.c_int64]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -100,6 +102,25 @@ def apply(w, x: np.ndarray, jac: np.ndarray | None = None, cells=None) -> np.nda
                             float(w.penalty_scale), _dp(x), _dp(r), cp, nc)
     if rc != 0:
         raise ValueError("oracle_apply: invalid arguments")
+    return r
+
+
+def apply_diffreac(w, x: np.ndarray, cells=None) -> np.ndarray:
+    """The paper's diffusion-reaction residual on the non-periodic unit cube of
+    workload `w` (w.problem == 1; axiparallel, w.m Gauss points, alpha = w.penalty_scale): R(x), including the
+    f and g terms (R(0) != 0)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    assert x.size == w.ndofs
+    r = np.full(w.ndofs, np.nan)
+    if cells is None:
+        cp, nc = None, 0
+    else:
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        cp, nc = _i64p(cells), len(cells)
+    rc = lib().oracle_apply_diffreac(w.N[0], w.N[1], w.N[2], w.k, w.m, float(w.penalty_scale), _dp(x), _dp(r),
+                                     cp, nc)
+    if rc != 0:
+        raise ValueError("oracle_apply_diffreac: invalid arguments")
     return r
 
 

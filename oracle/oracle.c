@@ -355,6 +355,146 @@ static void cell_residual(const otab* T, int i0, int i1, int i2, const double* c
     }
 }
 
+/*
+ * The paper's own problem (Eq. diffreac / diffreac_weak): on the
+ * NON-periodic unit cube (0,1)^3 with an axiparallel mesh (h_d = 1/N_d),
+ *   -div(K grad u) + c u = f,  u = g on the boundary,
+ *   K(x) = x x^T + I, c = 10, f = -6, g = |x|^2 (g is a manufactured solution).
+ * Residual R_I(x) = r_h(sum_J x_J phi_J, phi_I) of Eq. diffreac_weak with theta = -1:
+ *   volume   (K grad u, grad v) + (c u, v) - (f, v)
+ *   interior -(n.{K grad u}, [v]) + theta([u], n.{K grad v}) + gamma_F([u], [v])
+ *   boundary the same with [v] = {v} = v|T and n the outer normal, plus
+ *            -theta(g, n.(K grad v)) - gamma_F(g, v)
+ *   gamma_F = alpha k (k+d-1) |F| / min(|T+|, |T-|) (interior), alpha k (k+d-1) |F| / |T| (boundary),
+ *   d = 3; alpha = the `alpha` argument (the paper: 3).
+ * Cell-centric like cell_residual; xs[1+2d] / xs[2+2d] may be NULL on boundary faces.
+ */
+static void Kmat(const double* x, double* K)
+{
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) K[3 * a + b] = x[a] * x[b] + (a == b ? 1.0 : 0.0);
+}
+
+static void cell_residual_dr(const otab* T, int i0, int i1, int i2, const double* const xs[7], double alpha, double* r)
+{
+    const int n = T->n, m = T->m, n3 = n * n * n;
+    const int ic[3] = {i0, i1, i2};
+    const double h[3] = {1.0 / T->N[0], 1.0 / T->N[1], 1.0 / T->N[2]};
+    const double vol = h[0] * h[1] * h[2];
+    const double cr = 10.0, f = -6.0;
+    for (int I = 0; I < n3; ++I) r[I] = 0.0;
+    /* volume: grad u = J^{-T} grad_hat u = grad_hat u / h componentwise */
+    for (int q2 = 0; q2 < m; ++q2)
+        for (int q1 = 0; q1 < m; ++q1)
+            for (int q0 = 0; q0 < m; ++q0) {
+                const double* tab = T->vphi + (size_t)point_index3(m, q0, q1, q2) * n3 * 4;
+                double u, gh[3], g[3], K[9], Kg[3];
+                eval_u(n3, xs[0], tab, &u, gh);
+                for (int a = 0; a < 3; ++a) g[a] = gh[a] / h[a];
+                const double xq[3] = {(ic[0] + T->qx[q0]) * h[0], (ic[1] + T->qx[q1]) * h[1], (ic[2] + T->qx[q2]) * h[2]};
+                Kmat(xq, K);
+                for (int a = 0; a < 3; ++a) Kg[a] = K[3 * a] * g[0] + K[3 * a + 1] * g[1] + K[3 * a + 2] * g[2];
+                const double W = T->qw[q0] * T->qw[q1] * T->qw[q2] * vol;
+                for (int I = 0; I < n3; ++I) {
+                    const double* ti = tab + 4 * I;
+                    const double gp0 = ti[1] / h[0], gp1 = ti[2] / h[1], gp2 = ti[3] / h[2];
+                    r[I] += W * (Kg[0] * gp0 + Kg[1] * gp1 + Kg[2] * gp2 + cr * u * ti[0] - f * ti[0]);
+                }
+            }
+    /* faces */
+    const double kk = (double)T->k * (T->k + 3 - 1);
+    for (int d = 0; d < 3; ++d) {
+        int t1, t2;
+        tangential(d, &t1, &t2);
+        const double area = h[t1] * h[t2];
+        const double gamma = alpha * kk * area / vol; /* |F| / |T| (all cells have the same volume) */
+        for (int side = 0; side < 2; ++side) {
+            const int boundary = side ? (ic[d] == T->N[d] - 1) : (ic[d] == 0);
+            const double* tabself = T->fphi[d][side];
+            for (int b = 0; b < m; ++b)
+                for (int a = 0; a < m; ++a) {
+                    const size_t off = (size_t)(a + m * b) * n3 * 4;
+                    double xi[3];
+                    xi[d] = (double)side; xi[t1] = T->qx[a]; xi[t2] = T->qx[b];
+                    double xF[3], K[9];
+                    for (int c = 0; c < 3; ++c) xF[c] = (ic[c] + xi[c]) * h[c];
+                    Kmat(xF, K);
+                    const double W = T->qw[a] * T->qw[b] * area;
+                    double us, ghs[3], gs[3];
+                    eval_u(n3, xs[0], tabself + off, &us, ghs);
+                    for (int c = 0; c < 3; ++c) gs[c] = ghs[c] / h[c];
+                    if (boundary) {
+                        /* outer normal n = +-e_d; [u] = u, {K grad u} = K grad u (one-sided) */
+                        const double sn = side ? 1.0 : -1.0;
+                        const double Kgn = sn * (K[3 * d] * gs[0] + K[3 * d + 1] * gs[1] + K[3 * d + 2] * gs[2]);
+                        const double g = xF[0] * xF[0] + xF[1] * xF[1] + xF[2] * xF[2];
+                        for (int I = 0; I < n3; ++I) {
+                            const double* ti = tabself + off + 4 * I;
+                            const double gp[3] = {ti[1] / h[0], ti[2] / h[1], ti[3] / h[2]};
+                            const double Kvn = sn * (K[3 * d] * gp[0] + K[3 * d + 1] * gp[1] + K[3 * d + 2] * gp[2]);
+                            /* -(n.K grad u) v + theta u (n.K grad v) + gamma u v - theta g (n.K grad v) - gamma g v */
+                            r[I] += W * (-Kgn * ti[0] - (us - g) * Kvn + gamma * (us - g) * ti[0]);
+                        }
+                    } else {
+                        const int self_is_minus = (side == 1);
+                        const double* xo = xs[self_is_minus ? 2 + 2 * d : 1 + 2 * d];
+                        const double* tabo = T->fphi[d][self_is_minus ? 0 : 1];
+                        double uo, gho[3], go[3];
+                        eval_u(n3, xo, tabo + off, &uo, gho);
+                        for (int c = 0; c < 3; ++c) go[c] = gho[c] / h[c];
+                        const double um = self_is_minus ? us : uo, up = self_is_minus ? uo : us;
+                        /* n = +e_d (T- -> T+): n.{K grad u} = 1/2 (K (grad u- + grad u+))_d */
+                        double gsum[3];
+                        for (int c = 0; c < 3; ++c) gsum[c] = (self_is_minus ? gs[c] + go[c] : go[c] + gs[c]);
+                        const double avg = 0.5 * (K[3 * d] * gsum[0] + K[3 * d + 1] * gsum[1] + K[3 * d + 2] * gsum[2]);
+                        const double jump = um - up;
+                        const double sv = self_is_minus ? 1.0 : -1.0;
+                        for (int I = 0; I < n3; ++I) {
+                            const double* ti = tabself + off + 4 * I;
+                            const double gp[3] = {ti[1] / h[0], ti[2] / h[1], ti[3] / h[2]};
+                            const double dphin = 0.5 * (K[3 * d] * gp[0] + K[3 * d + 1] * gp[1] + K[3 * d + 2] * gp[2]);
+                            r[I] += W * (-avg * sv * ti[0] - jump * dphin + gamma * jump * sv * ti[0]);
+                        }
+                    }
+                }
+        }
+    }
+}
+
+/*
+ * The paper's diffusion-reaction residual (cell_residual_dr) on the non-periodic unit cube; x, r global
+ * canonical vectors; cells == NULL => all cells. Returns 0 or -1.
+ */
+int oracle_apply_diffreac(int N0, int N1, int N2, int k, int m, double alpha, const double* x, double* r,
+                          const int64_t* cells, int64_t ncells)
+{
+    otab T;
+    if (N0 < 1 || N1 < 1 || N2 < 1) return -1;
+    if (otab_init(&T, N0, N1, N2, k, m, 0, alpha)) { otab_free(&T); return -1; }
+    const int n = k + 1;
+    const int64_t n3 = (int64_t)n * n * n;
+    const int64_t total = (int64_t)N0 * N1 * N2;
+    const int64_t cnt = cells ? ncells : total;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t s = 0; s < cnt; ++s) {
+        const int64_t c = cells ? cells[s] : s;
+        const int i2 = (int)(c % N2), i1 = (int)((c / N2) % N1), i0 = (int)(c / ((int64_t)N1 * N2));
+        const int ic[3] = {i0, i1, i2};
+        const double* xs[7];
+        xs[0] = x + c * n3;
+        for (int d = 0; d < 3; ++d)
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                int jc[3] = {ic[0], ic[1], ic[2]};
+                jc[d] = ic[d] + (sgn ? 1 : -1);
+                xs[1 + 2 * d + sgn] = (jc[d] < 0 || jc[d] >= T.N[d]) ? NULL
+                                                                     : x + (((int64_t)jc[0] * N1 + jc[1]) * N2 + jc[2]) * n3;
+            }
+        cell_residual_dr(&T, i0, i1, i2, xs, alpha, r + c * n3);
+    }
+    otab_free(&T);
+    return 0;
+}
+
 /* Geometry of a canonical cell: row-major J_T. geom_kind 0: diag(1/N); 1: from jac[9 c ..]. */
 static void cell_jac(int geom_kind, const int N[3], const double* jac, int64_t c, double* J)
 {

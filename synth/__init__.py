@@ -91,6 +91,9 @@ class Workload:
     penalty_scale: float = 10.0  # gamma = penalty_scale * k (k+1) / h  (BASELINE.json configs)
     quad: int = -1              # Gauss points per direction; -1 -> k + 1
     gpus: tuple = (1,)
+    problem: int = 0            # 0: periodic SIPG of the configs; 1: the paper's diffusion-reaction problem
+                                #    (non-periodic cube, Dirichlet g = |x|^2, K = xx^T + I, c = 10,
+                                #    f = -6; penalty_scale = alpha = 3, gamma = alpha k(k+2) |F|/|T|)
     text: str = ""
 
     @property
@@ -126,6 +129,14 @@ CONFIGS = [
     Workload("cfg4_diffusion_q4_256_affine", 4, (256, 256, 256), 1, 1, seed=4, gpus=(1, 2, 4, 8),
              text="diffusion SIPG as cfg2 with DG Q4 on 256^3 affine-perturbed cells (2.1B DOFs), 2/4/8 GPUs"),
 ]
+
+
+def diffreac(k: int, N, seed: int = 11, quad: int = -1, alpha: float = 3.0) -> Workload:
+    """The paper's diffusion-reaction problem on an axiparallel N0 x N1 x N2 mesh of (0,1)^3."""
+    if isinstance(N, int):
+        N = (N, N, N)
+    return Workload(f"diffreac_k{k}_N{N[0]}x{N[1]}x{N[2]}_m{k + 1 if quad < 0 else quad}", k, tuple(N), 0, 0,
+                    seed=seed, penalty_scale=alpha, quad=quad, problem=1)
 
 
 def small(k: int, N, geom_kind: int = 0, coeff_kind: int = 0, seed: int = 7, quad: int = -1) -> Workload:

@@ -339,3 +339,69 @@ def test_overintegration_changes_nonpolynomial_coefficient():
     e2 = np.abs(r[1] - r[2]).max()
     assert e1 > 1e-6 * np.abs(r[2]).max()
     assert e2 < e1
+
+
+# ------------------------------------------------------------------ the paper's diffusion-reaction problem
+def _interp_fn(w, fn):
+    """DOF vector interpolating fn(x0, x1, x2) at the GL nodes of every cell of the unit-cube mesh."""
+    n = w.n
+    xi, _ = _gl01(n)
+    N0, N1, N2 = w.N
+    c = np.arange(w.ncells)
+    i2, i1, i0 = c % N2, (c // N2) % N1, c // (N1 * N2)
+    j = np.arange(n ** 3)
+    j0, j1, j2 = j % n, (j // n) % n, j // (n * n)
+    X0 = (i0[:, None] + xi[j0][None, :]) / N0
+    X1 = (i1[:, None] + xi[j1][None, :]) / N1
+    X2 = (i2[:, None] + xi[j2][None, :]) / N2
+    return fn(X0, X1, X2).reshape(-1)
+
+
+@pytest.mark.parametrize("k,N", [(2, (2, 3, 2)), (3, (2, 2, 3)), (4, (2, 2, 2))])
+def test_diffreac_manufactured_solution(k, N):
+    """g = |x|^2 solves -div((xx^T + I) grad u) + 10 u = -6 with u = g on the boundary, and it
+    lies in Q_k for k >= 2; SIPG is consistent, so with quadrature exact for every term (m = k+2, SURVEY
+    §8(f1)) the residual of its interpolant vanishes on every cell (boundary cells included)."""
+    w = synth.diffreac(k, N, quad=k + 2)
+    x = _interp_fn(w, lambda a, b, c: a * a + b * b + c * c)
+    r = oracle.apply_diffreac(w, x)
+    r0 = oracle.apply_diffreac(w, np.zeros_like(x))
+    assert np.abs(r).max() <= 1e-11 * np.abs(r0).max()
+
+
+def test_diffreac_detects_a_wrong_solution():
+    """The same residual is far from zero for a perturbed solution (the pin above is not vacuous)."""
+    k, N = 2, (2, 2, 2)
+    w = synth.diffreac(k, N, quad=k + 2)
+    x = _interp_fn(w, lambda a, b, c: a * a + b * b + c * c + 0.01 * a * b)
+    r0 = oracle.apply_diffreac(w, np.zeros_like(x))
+    assert np.abs(oracle.apply_diffreac(w, x)).max() > 1e-4 * np.abs(r0).max()
+
+
+@pytest.mark.parametrize("k,N", [(1, (3, 2, 2)), (2, (2, 3, 2))])
+def test_diffreac_bilinear_part_symmetric_positive(k, N):
+    """a(u, v) = R(u) - R(0) is the SIPG bilinear form (theta = -1) plus the reaction mass: symmetric and
+    positive definite with Dirichlet boundary faces (no null space, unlike the periodic operator)."""
+    w = synth.diffreac(k, N, quad=k + 2)
+    nd = w.ndofs
+    r0 = oracle.apply_diffreac(w, np.zeros(nd))
+    A = np.zeros((nd, nd))
+    for j in range(nd):
+        e = np.zeros(nd)
+        e[j] = 1.0
+        A[:, j] = oracle.apply_diffreac(w, e) - r0
+    assert np.abs(A - A.T).max() <= 1e-12 * np.abs(A).max()
+    assert np.linalg.eigvalsh(0.5 * (A + A.T)).min() > 0
+
+
+def test_diffreac_rhs_terms():
+    """R(0) = -(f, v) + boundary terms in g only: with alpha -> 2 alpha the penalty parts of R(0) and of a
+    double (the g-penalty term -gamma (g, v) and gamma(u, v) are linear in alpha)."""
+    k, N = 2, (2, 2, 2)
+    w1 = synth.diffreac(k, N, quad=k + 2, alpha=3.0)
+    w2 = synth.diffreac(k, N, quad=k + 2, alpha=6.0)
+    w0 = synth.diffreac(k, N, quad=k + 2, alpha=0.0)
+    z = np.zeros(w1.ndofs)
+    p1 = oracle.apply_diffreac(w1, z) - oracle.apply_diffreac(w0, z)
+    p2 = oracle.apply_diffreac(w2, z) - oracle.apply_diffreac(w0, z)
+    assert np.abs(p2 - 2 * p1).max() <= 1e-12 * np.abs(p2).max()
