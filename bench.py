@@ -113,6 +113,11 @@ def oracle_sample_rate(w, budget_s: float, seed: int = 2024):
 
     def run(ncell):
         cells = np.sort(rng.choice(w.ncells, ncell, replace=False)).astype(np.int64)
+        if w.problem == 1:  # the paper's problem: the oracle on the whole (small) host vector, sampled rows
+            x = synth.x_np(w)
+            t0 = time.perf_counter()
+            oracle.apply_diffreac(w, x, cells)
+            return time.perf_counter() - t0
         nb = oracle.neighbours(w, cells)
         x7 = synth.x_cells_np(w, nb.reshape(-1)).reshape(len(cells), 7, n3)
         j7 = synth.jac_cells_np(w, nb.reshape(-1)).reshape(len(cells), 7, 9) if w.geom_kind else None
@@ -165,7 +170,9 @@ def _config(w, ngpu):
     return {"workload": w.name, "mesh": list(w.N), "k": w.k, "quad_points": w.m, "dofs": w.ndofs,
             "geometry": "axis-aligned" if w.geom_kind == 0 else "per-cell affine",
             "coefficient": "1" if w.coeff_kind == 0 else "1+0.5sin(2pi x0)cos(2pi x1)",
-            "penalty": f"{w.penalty_scale:g}*k(k+1)/h", "parallelism": f"x0-slab{ngpu}",
+            "penalty": (f"{w.penalty_scale:g}*k(k+1)/h" if w.problem == 0 else f"alpha={w.penalty_scale:g}: alpha*k(k+2)|F|/|T|"),
+            "problem": "periodic SIPG (configs)" if w.problem == 0 else "diffusion-reaction, Dirichlet g=|x|^2 (P:L945-1003)",
+            "parallelism": f"x0-slab{ngpu}",
             "l2": f"inputs larger than L2 ({8 * w.ndofs / 1e9:.2f} GB per vector vs 126 MB L2)"
             if 8 * w.ndofs > 2 * 126e6 else "L2 flushed between steps"}
 
@@ -182,6 +189,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--problem", default="config", choices=["config", "diffreac"],
+                    help="diffreac: the paper's diffusion-reaction problem (SURVEY §8(f1)) with --k / --N, k+2 points")
+    ap.add_argument("--k", type=int, default=3)
+    ap.add_argument("--N", type=int, default=64)
     ap.add_argument("--quad", type=int, default=-1,
                     help="Gauss points per direction (default k+1; k+2 = overintegration, SURVEY §8(f2))")
     args = ap.parse_args()
@@ -190,6 +201,8 @@ def main():
 
     import synth
     w = synth.CONFIGS[args.config]
+    if args.problem == "diffreac":
+        w = synth.diffreac(args.k, args.N, quad=args.k + 2)
     if args.quad > 0 and args.quad != w.k + 1:
         import dataclasses
         w = dataclasses.replace(w, quad=args.quad, name=f"{w.name}_quad{args.quad}")
@@ -214,7 +227,8 @@ def main():
         return synth.jac_planes_torch(w, pb, npl, device=dev).cpu().numpy()
 
     sop = slab.SlabOperator(w.N, w.k, rank, world, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
-                            penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank, quad=w.m)
+                            penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank, quad=w.m,
+                            problem=w.problem)
     op = sop.op
     x = synth.x_torch(w, start=sop.offset, count=sop.ndofs, device=dev)
     r = torch.empty_like(x)

@@ -49,6 +49,13 @@ extern "C" {
 #define DG_COEFF_ONE 0   /* c = 1 (Poisson) */
 #define DG_COEFF_SINCOS 1 /* c(x) = 1 + 0.5 sin(2 pi x0) cos(2 pi x1), at the mapped quadrature points */
 
+#define DG_PROBLEM_PERIODIC 0 /* the configs: periodic cube, -div(c grad u), f = 0: r = A x */
+#define DG_PROBLEM_DIFFREAC 1 /* the paper's problem: non-periodic (0,1)^3,
+                                 -div(K grad u) + 10 u = -6, K = x x^T + I, u = |x|^2 on the boundary;
+                                 r = R(x) = A x - b (Eq. diffreac_weak incl. the f and g terms); axiparallel
+                                 (DG_GEOM_AXIS) only, coeff_kind ignored, quad = k+2 (k_quad);
+                                 gamma_F = penalty_scale k (k+2) |F| / |T| (the paper: penalty_scale = alpha = 3) */
+
 typedef struct dg_ctx dg_ctx;
 
 typedef struct dg_mesh {
@@ -65,6 +72,7 @@ typedef struct dg_mesh {
     double penalty_scale;  /* gamma_F = penalty_scale * k (k+1) * N[d] on faces with normal d (> 0) */
     int32_t device;        /* CUDA device ordinal */
     void* stream;          /* cudaStream_t on which dg_apply* enqueue work (NULL: legacy default stream) */
+    int32_t problem;       /* DG_PROBLEM_PERIODIC (default, 0) or DG_PROBLEM_DIFFREAC */
 } dg_mesh;
 
 /* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,

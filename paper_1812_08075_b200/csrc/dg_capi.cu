@@ -329,26 +329,30 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
 }
 
 // ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
-template <int N, bool AFF, bool COEF>
+template <int N, bool AFF, bool COEF, bool DR = false>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                         double* r, long long c0, long long c1, cudaStream_t st, const double*)
 {
     using L = dg::qd::QLay<N, N + 1>;
     if (c1 <= c0) return cudaSuccess;
     const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
-    dg::k_quad<N, N + 1, AFF, COEF><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
+    dg::k_quad<N, N + 1, AFF, COEF, DR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
         x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
     return cudaGetLastError();
 }
-template <int N, bool AFF, bool COEF>
+template <int N, bool AFF, bool COEF, bool DR = false>
 cudaError_t attr_quad()
 {
-    return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 dg::qd::QLay<N, N + 1>::BYTES);
 }
 template <int N>
-LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err)
+LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, bool dr = false)
 {
+    if (dr) {
+        *err = attr_quad<N, false, false, true>();
+        return launch_quad<N, false, false, true>;
+    }
     if (aff) {
         *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
         return coef ? launch_quad<N, true, true> : launch_quad<N, true, false>;
@@ -356,16 +360,16 @@ LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err)
     *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
     return coef ? launch_quad<N, false, true> : launch_quad<N, false, false>;
 }
-LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err)
+LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, bool dr = false)
 {
     switch (n) {
-    case 2: return pick_quad_n<2>(aff, coef, err);
-    case 3: return pick_quad_n<3>(aff, coef, err);
-    case 4: return pick_quad_n<4>(aff, coef, err);
-    case 5: return pick_quad_n<5>(aff, coef, err);
-    case 6: return pick_quad_n<6>(aff, coef, err);
-    case 7: return pick_quad_n<7>(aff, coef, err);
-    default: return pick_quad_n<8>(aff, coef, err);
+    case 2: return pick_quad_n<2>(aff, coef, err, dr);
+    case 3: return pick_quad_n<3>(aff, coef, err, dr);
+    case 4: return pick_quad_n<4>(aff, coef, err, dr);
+    case 5: return pick_quad_n<5>(aff, coef, err, dr);
+    case 6: return pick_quad_n<6>(aff, coef, err, dr);
+    case 7: return pick_quad_n<7>(aff, coef, err, dr);
+    default: return pick_quad_n<8>(aff, coef, err, dr);
     }
 }
 // interpolation / derivative of the n-node Lagrange basis at the m = n+1 Gauss points (long double
@@ -597,6 +601,10 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (mesh->coeff_kind != DG_COEFF_ONE && mesh->coeff_kind != DG_COEFF_SINCOS)
         return fail(DG_ERR_INVALID, "dg_setup: coeff_kind=%d", mesh->coeff_kind);
     if (!(mesh->penalty_scale > 0.0)) return fail(DG_ERR_INVALID, "dg_setup: penalty_scale must be > 0");
+    if (mesh->problem != DG_PROBLEM_PERIODIC && mesh->problem != DG_PROBLEM_DIFFREAC)
+        return fail(DG_ERR_INVALID, "dg_setup: problem=%d", mesh->problem);
+    if (mesh->problem == DG_PROBLEM_DIFFREAC && (mesh->geom_kind != DG_GEOM_AXIS || quad != k + 2))
+        return fail(DG_ERR_UNSUPPORTED, "dg_setup: the diffusion-reaction problem needs DG_GEOM_AXIS and quad = k+2");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -634,6 +642,8 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     for (int d = 0; d < 3; ++d) {
         M.h[d] = 1.0 / mesh->N[d];
         M.gamma[d] = mesh->penalty_scale * k * (k + 1) * (double)mesh->N[d];
+        // the paper's problem: gamma_F = alpha k (k+d-1) |F| / |T| = alpha k (k+2) / h_d
+        if (mesh->problem == DG_PROBLEM_DIFFREAC) M.gamma[d] = mesh->penalty_scale * k * (k + 2) * (double)mesh->N[d];
     }
     M.jac = nullptr;
     const int64_t n3 = (int64_t)n * n * n;
@@ -670,13 +680,14 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         case 8: fill_qtab<8>(H, Hm, c->qtab); break;
         }
         cudaError_t e = cudaSuccess;
-        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e);
+        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e,
+                              mesh->problem == DG_PROBLEM_DIFFREAC);
         if (e != cudaSuccess) {
             if (c->d_jac) cudaFree(c->d_jac);
             free(c);
             return fail(DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
         }
-        c->kname = "k_quad";
+        c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? "k_quad_diffreac" : "k_quad";
     }
     // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
     if (!c->quad) {
@@ -875,7 +886,10 @@ double dg_alg_flops(const dg_ctx* c)
         const double m = c->m, Cc = (c->mesh.coeff_kind == DG_COEFF_SINCOS) ? 16.0 : 0.0;
         const double vol = 2.0 * (4 * n * n * n * m + 6 * n * n * m * m + 6 * n * m * m * m) + (21.0 + Cc) * m * m * m;
         const double face = 2.0 * (8 * n * n * n + 9 * n * n * m + 12 * n * m * m) + (40.0 + Cc) * m * m;
-        return (vol + 3.0 * face) / (n * n * n) * (double)c->local_dofs;
+        // the diffusion-reaction problem adds u at the M^3 points (2 n m^3), its back-projection (2 n m^3),
+        // the full K (12 m^3) and the reaction / source term (3 m^3)
+        const double dr = (c->mesh.problem == DG_PROBLEM_DIFFREAC) ? 4 * n * m * m * m + 15 * m * m * m : 0.0;
+        return (vol + dr + 3.0 * face) / (n * n * n) * (double)c->local_dofs;
     }
     if (c->mesh.geom_kind == DG_GEOM_AXIS && c->mesh.coeff_kind == DG_COEFF_ONE)
         F = 12.0 * n + 51.0 + 30.0 / n;

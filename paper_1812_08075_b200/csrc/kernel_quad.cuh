@@ -94,7 +94,8 @@ struct QLay {
     //           F1 [6][NM] (own Ua1, Ud1, Ga1; nb Ua1, Ud1, Ga1) -> later FB1 [3][NM] (Pv, Pt, Pn)
     //           F2 [8][M2] (U-, U+, Gn-, Gn+, Gt1-, Gt1+, Gt2-, Gt2+) -> coefficients [4][M2] (Cv, Ct1, Ct2, Cn)
     static constexpr int FACE = 4 * N2 + 6 * NM + 8 * M2;
-    static constexpr int F = G2 + M3;
+    static constexpr int GU = G2 + M3;      // u at the M^3 points (diffusion-reaction: reaction / source terms)
+    static constexpr int F = GU + M3;
     static constexpr int GEO = F + 6 * FACE; // per cell: Gt[6], J rows 0-1 [6], o[2]; per face 16: dS, a-[3], a+[3], Jm rows 0-1 [6], om[2], pad
     static constexpr int CELL = GEO + 14 + 6 * 16;
     static constexpr int CELLP = (CELL + 1) / 2 * 2;
@@ -107,7 +108,12 @@ struct QLay {
 
 // grid: ceil(cells / CPB), block NT, dynamic smem QLay::BYTES. Cells [c_begin, c_end) of the slab
 // (local, canonical order).
-template <int N, int M, bool AFFINE, bool COEFF>
+// DR: the paper's diffusion-reaction problem (axiparallel mesh of the
+// non-periodic unit cube): K(x) = x x^T + I in place of c I, reaction c = 10 and source f = -6 in the
+// volume (u at the quadrature points: the 4th quantity of the stacked stage 1, Eq. fusedtensor),
+// boundary faces with the Dirichlet data g = |x|^2 (one-sided flux, [u] -> u - g), penalty
+// alpha k (k+2) |F| / |T| (alpha = penalty_scale, set in M.gamma by dg_setup).
+template <int N, int M, bool AFFINE, bool COEFF, bool DR = false>
 __global__ void __launch_bounds__(256)
 k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
        long long c_begin, long long c_end, const __grid_constant__ QTab<N, M> T, const MeshArgs M_)
@@ -204,7 +210,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         const int* mig = side ? ig : nig;
         fg[13] = (double)mig[0] / Ms.N0;
         fg[14] = (double)mig[1] / Ms.N1;
-        fg[15] = 0.0;
+        // DR: 1 on the boundary of the (non-periodic) cube
+        const int Nd = d == 0 ? Ms.N0 : (d == 1 ? Ms.N1 : Ms.N2);
+        fg[15] = (DR && (side ? ig[d] == Nd - 1 : ig[d] == 0)) ? 1.0 : 0.0;
     }
     __syncthreads();
 
@@ -228,11 +236,12 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             if (d == 0) nbx = nlp < 0 ? xb + (long long)rem * N3 : (nlp >= Ms.L ? xa + (long long)rem * N3 : x + ((long long)nlp * Ms.plane_cells + rem) * N3);
             else nbx = x + ((long long)lp * Ms.plane_cells + nrem) * N3;
             const double* xo = cellp(c) + L::X;
+            const bool bnd = DR && cellp(c)[L::GEO + 14 + 16 * f + 15] != 0.0;
             double uo = 0, go = 0, un = 0, gn = 0;
 #pragma unroll
             for (int j = 0; j < N; ++j) {
                 const double vo = xo[pidx<N>(d, j, a, bq)];
-                const double vn = __ldg(nbx + pidx<N>(d, j, a, bq));
+                const double vn = bnd ? 0.0 : __ldg(nbx + pidx<N>(d, j, a, bq));
                 uo = fma(side ? se1[j] : se0[j], vo, uo);
                 go = fma(side ? sd1[j] : sd0[j], vo, go);
                 un = fma(side ? se0[j] : se1[j], vn, un);
@@ -271,12 +280,14 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     // ---------------- P3: stage 1c (along j0); face contraction along t2 ----------------
     {
         using SB = qd::Sw3<N, M, M, 0, M, false, false>;
-        for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
-            const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
+        constexpr int NQ = DR ? 4 : 3;
+        for (int t = tid; t < ncell * NQ * SB::NL; t += NT) {
+            const int c = t / (NQ * SB::NL), k = (t / SB::NL) % NQ, l = t % SB::NL;
             double* b = cellp(c);
             if (k == 0) SB::line(b + L::Z, b + L::G0, T.Dq, l);
             else if (k == 1) SB::line(b + L::Zd1, b + L::G1, T.A, l);
-            else SB::line(b + L::Zd2, b + L::G2, T.A, l);
+            else if (k == 2) SB::line(b + L::Zd2, b + L::G2, T.A, l);
+            else SB::line(b + L::Z, b + L::GU, T.A, l); // u = A0 A1 A2 X
         }
         using F = qd::Sw2<M, N, 1, M, false, false>; // M x N -> M x M
         for (int t = tid; t < ncell * 6 * 8 * F::NL; t += NT) {
@@ -302,6 +313,21 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             cW *= coeff_sincos(g[12] + g[6] * xi0 + g[7] * xi1 + g[8] * xi2, g[13] + g[9] * xi0 + g[10] * xi1 + g[11] * xi2);
         }
         const double a0 = b[L::G0 + P], a1 = b[L::G1 + P], a2 = b[L::G2 + P];
+        if (DR) {
+            // (K grad u, grad v) + (c u - f, v), K = x x^T + I, c = 10, f = -6
+            const double h0 = Ms.h[0], h1 = Ms.h[1], h2 = Ms.h[2];
+            const double W = sw[q0] * sw[q1] * sw[q2] * h0 * h1 * h2;
+            int lp_, rem_, ig_[3];
+            coords(c, lp_, rem_, ig_);
+            const double x0 = (ig_[0] + sxq[q0]) * h0, x1 = (ig_[1] + sxq[q1]) * h1, x2 = (ig_[2] + sxq[q2]) * h2;
+            const double p0 = a0 / h0, p1 = a1 / h1, p2 = a2 / h2; // physical gradient
+            const double xg = x0 * p0 + x1 * p1 + x2 * p2;        // K grad u = x (x . grad u) + grad u
+            b[L::G0 + P] = W * fma(x0, xg, p0) / h0;
+            b[L::G1 + P] = W * fma(x1, xg, p1) / h1;
+            b[L::G2 + P] = W * fma(x2, xg, p2) / h2;
+            b[L::GU + P] = W * (10.0 * b[L::GU + P] + 6.0);
+            continue;
+        }
         b[L::G0 + P] = cW * fma(g[0], a0, fma(g[3], a1, g[4] * a2));
         b[L::G1 + P] = cW * fma(g[3], a0, fma(g[1], a1, g[5] * a2));
         b[L::G2 + P] = cW * fma(g[4], a0, fma(g[5], a1, g[2] * a2));
@@ -321,6 +347,43 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         const double t2m = side ? T2o : T2n, t2p = side ? T2n : T2o;
         const double* am = fg + 1;
         const double* ap = fg + 4;
+        if (DR) {
+            // physical face point (own cell, xi_d = side) and K = x x^T + I
+            int lp_, rem_, ig_[3];
+            coords(c, lp_, rem_, ig_);
+            const double xa_ = sxq[a], xb_ = sxq[bq];
+            const double xi0 = d == 0 ? (double)side : xa_;
+            const double xi1 = d == 1 ? (double)side : (d == 0 ? xa_ : xb_);
+            const double xi2 = d == 2 ? (double)side : xb_;
+            const double X0 = (ig_[0] + xi0) * Ms.h[0], X1 = (ig_[1] + xi1) * Ms.h[1], X2 = (ig_[2] + xi2) * Ms.h[2];
+            const double Xd = d == 0 ? X0 : (d == 1 ? X1 : X2);
+            const double Xt1 = d == 0 ? X1 : X0, Xt2 = d == 2 ? X1 : X2;
+            const double hd = Ms.h[d], ht1 = Ms.h[t1], ht2 = Ms.h[t2];
+            // (K e)_d for e = d, t1, t2 (K symmetric), scaled to reference derivatives (1/h_e)
+            const double kd = (Xd * Xd + 1.0) / hd, kt1 = Xd * Xt1 / ht1, kt2 = Xd * Xt2 / ht2;
+            const double W = sw[a] * sw[bq] * ht1 * ht2;
+            const double gam = Ms.gamma[d];
+            const double Kgo = kd * Gno + kt1 * T1o + kt2 * T2o; // (K grad u)_d of the own side
+            double Cv, s;
+            if (fg[15] != 0.0) {
+                // boundary face: outer normal sn e_d, [u] = u - g (theta and penalty terms), one-sided flux
+                const double sn = side ? 1.0 : -1.0;
+                const double jmp = Uo - (X0 * X0 + X1 * X1 + X2 * X2);
+                Cv = W * (-sn * Kgo + gam * jmp);
+                s = -W * jmp * sn;
+            } else {
+                const double Kgn = kd * Gnn + kt1 * T1n + kt2 * T2n;
+                const double jmp = um - up;
+                const double Cvm = W * (-0.5 * (Kgo + Kgn) + gam * jmp);
+                Cv = side ? Cvm : -Cvm;
+                s = -0.5 * W * jmp;
+            }
+            F2[0 * M2 + p] = Cv;
+            F2[1 * M2 + p] = s * kt1;
+            F2[2 * M2 + p] = s * kt2;
+            F2[3 * M2 + p] = s * kd;
+            continue;
+        }
         double cF = 1.0;
         if (COEFF) {
             const double xa_ = sxq[a], xb_ = sxq[bq];
@@ -351,7 +414,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
             const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
-            if (k == 0) SB::line(b + L::G0, b + L::Z, T.Dq, l);       // V
+            if (k == 0) {
+                SB::line(b + L::G0, b + L::Z, T.Dq, l); // V
+                if (DR) qd::Sw3<M, M, M, 0, N, true, true>::line(b + L::GU, b + L::Z, T.A, l); // + A0^T (c u - f)
+            }
             else if (k == 1) SB::line(b + L::G1, b + L::Zd1, T.A, l); // W1
             else SB::line(b + L::G2, b + L::Zd2, T.A, l);             // W2
         }

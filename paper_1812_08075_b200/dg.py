@@ -44,6 +44,7 @@ class dg_mesh(ctypes.Structure):
         ("penalty_scale", ctypes.c_double),
         ("device", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("problem", ctypes.c_int32),
     ]
 
 
@@ -101,7 +102,7 @@ def _ptr(t) -> int:
 # ------------------------------------------------------------------ C-ABI with the same names
 def dg_setup(N, k: int, quad: int, *, plane_begin: int = 0, nplanes: int | None = None, geom_kind: int = 0,
              jac: np.ndarray | None = None, coeff_kind: int = 0, penalty_scale: float = 10.0, device: int = 0,
-             stream: int | None = None) -> int:
+             stream: int | None = None, problem: int = 0) -> int:
     """Returns an opaque context handle (int). jac: host float64 array [(L+2) N1 N2, 9] for affine."""
     L = load()
     m = dg_mesh()
@@ -116,6 +117,7 @@ def dg_setup(N, k: int, quad: int, *, plane_begin: int = 0, nplanes: int | None 
     m.penalty_scale = float(penalty_scale)
     m.device = device
     m.stream = stream
+    m.problem = problem
     h = ctypes.c_void_p()
     _check(L.dg_setup(ctypes.byref(m), k, quad, ctypes.byref(h)))
     return h.value
@@ -198,7 +200,7 @@ class Operator:
 
     def __init__(self, N, k: int, *, geom_kind: int = 0, coeff_kind: int = 0, penalty_scale: float = 10.0,
                  jac: np.ndarray | None = None, plane_begin: int = 0, nplanes: int | None = None, device: int = 0,
-                 stream=None, quad: int | None = None):
+                 stream=None, quad: int | None = None, problem: int = 0):
         import torch
         self.N = tuple(int(v) for v in N)
         self.k = k
@@ -208,7 +210,7 @@ class Operator:
         self._stream = stream
         self.ctx = dg_setup(self.N, k, k + 1 if quad is None else quad, plane_begin=plane_begin, nplanes=nplanes,
                             geom_kind=geom_kind, jac=jac, coeff_kind=coeff_kind, penalty_scale=penalty_scale,
-                            device=device, stream=stream.cuda_stream)
+                            device=device, stream=stream.cuda_stream, problem=problem)
         self.ndofs = dg_local_ndofs(self.ctx)
         self.offset = dg_local_offset(self.ctx)
         self.plane_ndofs = dg_plane_ndofs(self.ctx)

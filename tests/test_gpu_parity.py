@@ -384,3 +384,77 @@ def test_quad_config_sampled():
     w = dataclasses.replace(synth.CONFIGS[2], quad=7)
     cells = synth.sample_cells(w, nrandom=1500, plane_cap=48, wrap_plane_cells=64)
     assert _sampled_check(w, cells) <= TOL
+
+
+# ------------------------------------------------------------------ the paper's diffusion-reaction problem
+def _dr_op(w, **kw):
+    from paper_1812_08075_b200 import Operator
+    return Operator(w.N, w.k, penalty_scale=w.penalty_scale, quad=w.m, problem=1, **kw)
+
+
+@pytest.mark.parametrize("k", range(1, 8))
+def test_diffreac_parity(k):
+    """R(x) of Eq. diffreac_weak (K = xx^T + I, c = 10, f = -6, Dirichlet g = |x|^2 on the
+    non-periodic cube, alpha = 3) on the GPU (k_quad, k+2 points) against the oracle, boundary cells on
+    every side, anisotropic meshes with ragged CTA tails."""
+    N = (3, 4, 5) if k <= 4 else (2, 3, 3)
+    w = synth.diffreac(k, N, quad=k + 2)
+    op = _dr_op(w)
+    assert op.kernel_name == "k_quad_diffreac"
+    x = synth.x_torch(w, device="cuda")
+    r = op.apply(x)
+    torch.cuda.synchronize()
+    ref = oracle.apply_diffreac(w, x.cpu().numpy())
+    op.close()
+    assert _rel(r.cpu().numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_diffreac_manufactured_solution_gpu(k):
+    """The interpolant of g = |x|^2 (in Q_k for k >= 2) has a vanishing residual on the GPU too."""
+    w = synth.diffreac(k, (4, 3, 5), quad=k + 2)
+    xi, _ = np.polynomial.legendre.leggauss(w.n)
+    xi = 0.5 * (xi + 1.0)
+    N0, N1, N2 = w.N
+    c = np.arange(w.ncells)
+    i2, i1, i0 = c % N2, (c // N2) % N1, c // (N1 * N2)
+    j = np.arange(w.n ** 3)
+    j0, j1, j2 = j % w.n, (j // w.n) % w.n, j // (w.n * w.n)
+    X0 = (i0[:, None] + xi[j0][None, :]) / N0
+    X1 = (i1[:, None] + xi[j1][None, :]) / N1
+    X2 = (i2[:, None] + xi[j2][None, :]) / N2
+    x = torch.from_numpy((X0 ** 2 + X1 ** 2 + X2 ** 2).reshape(-1)).cuda()
+    op = _dr_op(w)
+    r = op.apply(x)
+    r0 = op.apply(torch.zeros_like(x))
+    assert r.abs().max().item() <= 1e-11 * r0.abs().max().item()
+    op.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_diffreac_slab_loopback_bitwise(world):
+    """The diffusion-reaction residual in the x0-slab decomposition equals the whole-mesh apply (the
+    boundary planes of the cube ignore the halos)."""
+    from paper_1812_08075_b200 import slab
+    w = synth.diffreac(3, (6, 3, 4), quad=5)
+    full = _dr_op(w)
+    x = synth.x_torch(w, device="cuda")
+    ref = full.apply(x)
+    pd = full.plane_ndofs
+    got = torch.full_like(x, float("nan"))
+    for q in range(world):
+        p = slab.plan(w.N[0], q, world)
+        op = _dr_op(w, plane_begin=p.plane_begin, nplanes=p.nplanes)
+        xs = x[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        rs = got[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        hb = x[((p.plane_begin - 1) % w.N[0]) * pd:][:pd].clone()
+        ha = x[((p.plane_begin + p.nplanes) % w.N[0]) * pd:][:pd].clone()
+        a, b = p.interior
+        if b > a:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        for a, b in p.boundary:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        torch.cuda.synchronize()
+        op.close()
+    assert torch.equal(got, ref)
+    full.close()
