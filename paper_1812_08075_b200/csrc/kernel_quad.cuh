@@ -102,6 +102,10 @@ struct QLay {
     static constexpr int TAB = CPB * CELLP;   // shared tables: A, Dq (M N each), wq, xq (M), e0, e1, d0, d1 (N)
     static constexpr int END = TAB + 2 * M * N + 2 * M + 4 * N;
     static constexpr int BYTES = END * 8;
+    // resident CTAs per SM the shared memory allows (the register cap follows from it)
+    // (at most 2 for n >= 6: their sweeps need ~128 registers; 85 spill heavily)
+    static constexpr int MINB_SMEM = (BYTES + 2048) * 4 <= 228 * 1024 ? 4 : ((BYTES + 2048) * 3 <= 228 * 1024 ? 3 : ((BYTES + 2048) * 2 <= 228 * 1024 ? 2 : 1));
+    static constexpr int MINB = (N >= 6 && MINB_SMEM > 2) ? 2 : MINB_SMEM;
 };
 
 } // namespace qd
@@ -114,7 +118,7 @@ struct QLay {
 // boundary faces with the Dirichlet data g = |x|^2 (one-sided flux, [u] -> u - g), penalty
 // alpha k (k+2) |F| / |T| (alpha = penalty_scale, set in M.gamma by dg_setup).
 template <int N, int M, bool AFFINE, bool COEFF, bool DR = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, qd::QLay<N, M>::MINB) // as many CTAs / SM as shared memory allows
 k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
        long long c_begin, long long c_end, const __grid_constant__ QTab<N, M> T, const MeshArgs M_)
 {
@@ -142,14 +146,24 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     for (int c = 0; c < ncell; ++c)
         for (int i = tid; i < N3; i += NT) cellp(c)[L::X + i] = __ldg(x + (cfirst + c) * N3 + i);
 
-    // cell coordinates
+    // cell coordinates, computed once per cell (32-bit: a slab has < 2^31 cells)
+    __shared__ int s_co[CPB][5]; // lp, rem, i0, i1, i2
+    if (tid < ncell) {
+        const int lc = (int)(cfirst + tid);
+        const int lp = lc / Ms.plane_cells, rem = lc - lp * Ms.plane_cells;
+        s_co[tid][0] = lp;
+        s_co[tid][1] = rem;
+        s_co[tid][2] = (Ms.plane_begin + lp) % Ms.N0;
+        s_co[tid][3] = rem / Ms.N2;
+        s_co[tid][4] = rem - (rem / Ms.N2) * Ms.N2;
+    }
+    __syncthreads();
     auto coords = [&](int c, int& lp, int& rem, int ig[3]) {
-        const long long lc = cfirst + c;
-        lp = (int)(lc / Ms.plane_cells);
-        rem = (int)(lc % Ms.plane_cells);
-        ig[0] = (Ms.plane_begin + lp) % Ms.N0;
-        ig[1] = rem / Ms.N2;
-        ig[2] = rem % Ms.N2;
+        lp = s_co[c][0];
+        rem = s_co[c][1];
+        ig[0] = s_co[c][2];
+        ig[1] = s_co[c][3];
+        ig[2] = s_co[c][4];
     };
     auto jac_of = [&](int lp, int rem, double* J) {
         const double* jp = Ms.jac + ((long long)(lp + 1) * Ms.plane_cells + rem) * 9;
@@ -172,11 +186,33 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         const int c = t / 7, f = t % 7;
         int lp, rem, ig[3];
         coords(c, lp, rem, ig);
-        double J[9], Ji[9];
-        if (AFFINE) jac_of(lp, rem, J);
-        else { for (int i = 0; i < 9; ++i) J[i] = 0.0; J[0] = Ms.h[0]; J[4] = Ms.h[1]; J[8] = Ms.h[2]; }
-        const double det = inv3(J, Ji);
         double* g = cellp(c) + L::GEO;
+        if (!AFFINE) {
+            // axis-aligned: J = diag(h), no inverse needed
+            const double h0 = Ms.h[0], h1 = Ms.h[1], h2 = Ms.h[2], ad = h0 * h1 * h2;
+            if (f == 6) {
+                g[0] = ad / (h0 * h0); g[1] = ad / (h1 * h1); g[2] = ad / (h2 * h2); g[3] = g[4] = g[5] = 0.0;
+                g[6] = h0; g[7] = 0.0; g[8] = 0.0; g[9] = 0.0; g[10] = h1; g[11] = 0.0;
+                g[12] = (double)ig[0] / Ms.N0;
+                g[13] = (double)ig[1] / Ms.N1;
+                continue;
+            }
+            const int d = f >> 1, side = f & 1;
+            const int Nd = d == 0 ? Ms.N0 : (d == 1 ? Ms.N1 : Ms.N2);
+            double* fg = g + 14 + 16 * f;
+            fg[0] = ad / Ms.h[d];
+            for (int e = 0; e < 3; ++e) fg[1 + e] = fg[4 + e] = (e == d) ? 1.0 / Ms.h[d] : 0.0;
+            fg[7] = h0; fg[8] = 0.0; fg[9] = 0.0; fg[10] = 0.0; fg[11] = h1; fg[12] = 0.0;
+            const int mi0 = (d == 0 && !side) ? (ig[0] + Ms.N0 - 1) % Ms.N0 : ig[0];
+            const int mi1 = (d == 1 && !side) ? (ig[1] + Ms.N1 - 1) % Ms.N1 : ig[1];
+            fg[13] = (double)mi0 / Ms.N0;
+            fg[14] = (double)mi1 / Ms.N1;
+            fg[15] = (DR && (side ? ig[d] == Nd - 1 : ig[d] == 0)) ? 1.0 : 0.0;
+            continue;
+        }
+        double J[9], Ji[9];
+        jac_of(lp, rem, J);
+        const double det = inv3(J, Ji);
         if (f == 6) {
             const double ad = fabs(det);
             auto gg = [&](int a, int b) { return ad * (Ji[3 * a] * Ji[3 * b] + Ji[3 * a + 1] * Ji[3 * b + 1] + Ji[3 * a + 2] * Ji[3 * b + 2]); };
