@@ -12,6 +12,10 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 kill $SMI
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
 for C in 0 1 2 4; do timeout 900 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_cfg$C.json 2> $O/bench_cfg$C.err; done
+# SURVEY §8(f2) general quadrature (cfg2 with 7 points) and §8(f1) the paper's diffusion-reaction problem
+timeout 900 python bench.py --config 2 --quad 7 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_cfg2_quad7.json 2> $O/bench_cfg2_quad7.err
+timeout 900 python bench.py --problem diffreac --k 3 --N 64 --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > $O/bench_diffreac_k3_64.json 2> $O/bench_diffreac.err
+timeout 900 python bench.py --problem diffreac --k 5 --N 48 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_diffreac_k5_48.json 2>> $O/bench_diffreac.err
 for C in 3 2 4; do
   B="python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
   $B > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg$C.csv $B > /dev/null 2>&1
