@@ -37,6 +37,6 @@ python tools/ncu_summary.py --launches $O/launches_cfg3.csv --rep $O/prof_axis8_
 python tools/ncu_summary.py --launches $O/launches_cfg2.csv --rep $O/prof_gen_cfg2.ncu-rep --out $O/ncu_gen_cfg2 --title "k_gen on cfg2 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --launches $O/launches_cfg4.csv --rep $O/prof_gen_cfg4.ncu-rep --out $O/ncu_gen_cfg4 --title "k_gen on cfg4 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --rep $O/prof_gen_cfg1.ncu-rep --out $O/ncu_gen_cfg1 --title "k_gen on cfg1 (N=1)" > /dev/null 2>&1
-rm -f $O/prof_gen_cfg2.ncu-rep $O/prof_gen_cfg1.ncu-rep
+rm -f $O/*.ncu-rep  # summaries only: gpurun returns <= 64 MiB
 tail -2 $O/pytest_gpu.log
 cat $O/bench.json
