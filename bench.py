@@ -271,6 +271,17 @@ def main():
         torch.cuda.profiler.stop()
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    warm_ms = None
+    if flush is not None:
+        # L2-resident vectors: also the warm number (no flush between applies; SURVEY §8(d) timing protocol)
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        w0.record(stream)
+        for _ in range(K):
+            sop.apply(x, r)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        warm_ms = w0.elapsed_time(w1) / K
     total_ms = t_start.elapsed_time(t_end) if flush is None else sum(step_ms)
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -365,6 +376,7 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * sop.launches_per_apply,
         "clocks": clk.summary(), "result_finite": ok,
         "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
+        "warm_ms_per_step": warm_ms,
     }
     if world > 1:
         dist.barrier()

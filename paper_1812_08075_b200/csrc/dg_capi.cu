@@ -771,6 +771,16 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         }
         if (c->tile) c->kname = "k_tile";
         if (c->gen) c->kname = "k_gen";
+#ifdef DG_GEN_TRACE
+        if (c->gen && getenv("DG_TRACE") && !c->dbg) {
+            if (cudaMalloc(&c->dbg, sizeof(long long) * 1024 * 16 * 8) == cudaSuccess) {
+                cudaMemset(c->dbg, 0, sizeof(long long) * 1024 * 16 * 8);
+                cudaMemcpyToSymbol(dg::g_gen_dbg, &c->dbg, sizeof(long long*));
+            } else {
+                c->dbg = nullptr;
+            }
+        }
+#endif
     }
     // axis-aligned Q7 fast path: tile T1 x T2 (env DG_AX8_TILE picks an AX8_VARIANTS entry for experiments)
     if (!c->quad) {

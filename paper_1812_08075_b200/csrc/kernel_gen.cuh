@@ -267,6 +267,17 @@ __global__ void k_cface(const double* __restrict__ jac, double* __restrict__ out
     out[t] = 1.0 + 0.5 * sinpi(2.0 * x0) * cospi(2.0 * x1);
 }
 
+#ifdef DG_GEN_TRACE
+// phase timestamps (experiments only): [block < 1024][step < 16][8] clock64 values, thread 0
+__device__ long long* g_gen_dbg = nullptr;
+#define GEN_STAMP(ph)                                                                                              \
+    do {                                                                                                           \
+        if (tid == 0 && g_gen_dbg && blockIdx.x < 1024 && s < 16) g_gen_dbg[(blockIdx.x * 16 + s) * 8 + (ph)] = clock64(); \
+    } while (0)
+#else
+#define GEN_STAMP(ph) do { } while (0)
+#endif
+
 // grid: ntiles * nchunks CTAs (chunk-major), block Lay::NT, dynamic smem Lay::BYTES
 template <int N, bool AFFINE, bool COEFF, int T1, int T2, int MINB>
 __global__ void __launch_bounds__(gn::Lay<N, AFFINE, COEFF, T1, T2>::NT, MINB)
@@ -753,10 +764,12 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const double* XC = XS + (s & 1) * NC * N3;     // own plane lp
         const double* XN = XS + ((s + 1) & 1) * NC * N3; // next plane lp + 1
         const double* gb = GE + (s & 1) * NCG * GREC;
+        GEN_STAMP(0);
         gn::mbar_wait(barA, (s + 1) & 1);
         gn::mbar_wait(barB, s & 1);
         if (!D2BULK) gn::cp_async_wait_all();
         __syncthreads();
+        GEN_STAMP(1);
 
         if constexpr (LINEOP) {
             // ---- L1: own line traces (kept lines in registers) + foreign traces ----
@@ -859,6 +872,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         cxcur = CX + (s & 1) * NC * CXSZ;
         cfcur = CF + (s & 1) * NCG * CFSZ;
         __syncthreads();
+        GEN_STAMP(2);
 
         // stream the next step's own blocks (plane lp + 2) and geometry (plane lp + 1) behind the compute
         if (tid == 0 && s + 1 < nsteps) {
@@ -917,12 +931,15 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         } else if (AFFINE) {
             face_lines(lineA, std::true_type{}, gb, NF);
             __syncthreads();
+            GEN_STAMP(3);
             // ---------------- P3: face line pass B (flux) ----------------
             face_lines(lineB, std::false_type{}, gb, NF);
             __syncthreads();
+            GEN_STAMP(4);
             // ---------------- P4: face line pass C (tangential back-projection) ----------------
             face_lines(lineC, std::true_type{}, gb, NF);
             __syncthreads();
+            GEN_STAMP(5);
         } else {
             all_faces(passB, gb);
             __syncthreads();
@@ -964,6 +981,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             }
         }
         __syncthreads();
+        GEN_STAMP(6);
         if (act) {
             double xe[HE], xo[H > 0 ? H : 1];
             gn::split<N>(q2, xe, xo);
@@ -974,6 +992,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
 #pragma unroll
             for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y[j] + G0[gix(2, j)] + G1[gix(2, j)];
         }
+        GEN_STAMP(7);
         // (the barrier at the top of the next step orders these reads before the next writes)
     }
 }

@@ -23,6 +23,8 @@ def main():
     tot = Counter()
     S = 0
     ops, ops_s = Counter(), Counter()
+    thr = Counter()  # predicated-on thread instructions per opcode (exact lane counts)
+    ti = idx.get("Predicated-On Thread Instructions Executed")
     for r in data:
         for s in stalls:
             try:
@@ -43,12 +45,21 @@ def main():
             ops[op] += int(r[idx["Instructions Executed"]])
         except ValueError:
             pass
+        if ti is not None:
+            try:
+                thr[op] += int(r[ti])
+            except ValueError:
+                pass
         ops_s[op] += ns
     print(f"samples {S}")
     for s, v in tot.most_common(12):
         print(f"  {s:28s} {v:9d} {100 * v / max(S, 1):5.1f}%")
     T = sum(ops.values())
     print(f"warp instructions executed {T}")
+    if thr:
+        f64 = 2 * thr["DFMA"] + thr["DADD"] + thr["DMUL"]
+        print(f"issued FP64 flops (2 DFMA + DADD + DMUL, predicated-on lanes) {f64:.4e}  "
+              f"[DFMA {thr['DFMA']:.3e}, DADD {thr['DADD']:.3e}, DMUL {thr['DMUL']:.3e} thread-instructions]")
     for k, v in ops.most_common(22):
         print(f"  {k:10s} {v:12d} {100 * v / T:5.1f}%  samples {ops_s[k]}")
 
