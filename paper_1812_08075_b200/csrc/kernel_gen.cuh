@@ -58,6 +58,10 @@ struct EOTab {
 
 namespace gn {
 
+struct RunD { // a face direction known only at run time (the warp-local face phase)
+    int value;
+};
+
 using tl::bulk_g2s;
 using tl::mbar_expect_tx;
 using tl::mbar_init;
@@ -426,7 +430,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         double mdn, mt1, mt2, pdn, pt1, pt2, dS;
     };
     auto face_a = [&](auto DC, const double* gb, int f) -> FaceA {
-        constexpr int d = decltype(DC)::value;
+        const int d = DC.value; // compile-time for integral_constant, runtime for RunD
         FaceA A;
         if (AFFINE) {
             // record pairs (a-_t1, a+_t1) (a-_t2, a+_t2) (a-_d, a+_d) (dS, 0): pass A reads the first two,
@@ -458,7 +462,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // pass B: flux. AFFINE: Cv- -> TR(f,0).x, Cg -> CG. Axis: (V, G) of both sides directly.
     // Ra, Rb: rows a, b of D (registers for the thread's own faces)
     auto ptB = [&](auto DC, const double* gb, int f, int p, const double* Ra, const double* Rb) {
-        constexpr int d = decltype(DC)::value;
+        const int d = DC.value; // compile-time for integral_constant, runtime for RunD
         const int a = p % N, b = p / N;
         const FaceA A = face_a(DC, gb, f);
         const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0; // c at x_F on T- (R12)
@@ -556,7 +560,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // line B (t2-line a): {c grad u . n} = c_F/2 (a-_d gn- + a+_d gn+ + D_t1 w1 + D_t2 w2), SIPG flux
     // (Eq. diffreac_weak, theta = -1): Cv- -> TR(f,0).x, Cg -> BX, D_t2^T Cg -> BY
     auto lineB = [&](auto DC, const double* gb, int f, int a) {
-        constexpr int d = decltype(DC)::value;
+        const int d = DC.value; // compile-time for integral_constant, runtime for RunD
         const FaceA A = face_a(DC, gb, f);
         double w2[N];
 #pragma unroll
@@ -574,7 +578,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0; // c at x_F on T- (R12)
             const double Wt = wa * sW[b] * A.dS;
             const double jump = m.x - pl.x;
-            TRp(f, 0)[p].x = Wt * fma(M.gamma[d], jump, -0.5 * cF * s);
+            TRp(f, 0)[p].x = Wt * fma(d == 0 ? M.gamma[0] : (d == 1 ? M.gamma[1] : M.gamma[2]), jump, -0.5 * cF * s);
             cg[b] = -0.5 * Wt * jump * cF;
         }
         double t2[N];
@@ -626,9 +630,36 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             else line(std::integral_constant<int, 2>{}, gb, o, l);
         }
     };
+    // warp-local face phase (affine, n <= 5): the N lines of a face are N consecutive lanes of one warp, so
+    // passes A -> B -> C of a face need only __syncwarp (no CTA barriers between them); the face direction
+    // is a run-time value (faces of several directions share a warp)
+    auto face_warp = [&](const double* gb) {
+        constexpr int FPW = 32 / N;          // faces per warp and round
+        constexpr int NWARP = NT / 32;
+        const int warp = tid >> 5, lane = tid & 31;
+        const int fo = lane / N, l = lane - fo * N;
+        for (int base = 0; base < NF; base += FPW * NWARP) {
+            const int o = base + warp * FPW + fo;
+            const bool on = lane < FPW * N && o < NF;
+            int f = 0, d = 0;
+            if (on) {
+                if (o < NC) { f = 3 * o; d = 0; }
+                else if (o < 2 * NC) { f = 3 * (o - NC) + 1; d = 1; }
+                else if (o < 3 * NC) { f = 3 * (o - 2 * NC) + 2; d = 2; }
+                else { f = o; d = (o < 3 * NC + T2) ? 1 : 2; }
+            }
+            const gn::RunD DC{d};
+            if (on) lineA(DC, gb, f, l);
+            __syncwarp();
+            if (on) lineB(DC, gb, f, l);
+            __syncwarp();
+            if (on) lineC(DC, gb, f, l);
+            __syncwarp();
+        }
+    };
     // axis-aligned faces (no tangential terms): flux per point, (V, G) of both sides directly
     auto passB = [&](auto DC, const double* gb, int f, int p, const double*, const double*) {
-        constexpr int d = decltype(DC)::value;
+        const int d = DC.value; // compile-time for integral_constant, runtime for RunD
         const int a = p % N, b = p / N;
         const FaceA A = face_a(DC, gb, f);
         const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0;
@@ -658,7 +689,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // foreign traces: ring cells (their ends facing the tile) and the next plane's lower ends,
     // grouped by line direction (d = 1: rings along i1, d = 2: rings along i2, d = 0: next plane)
     auto trace_task = [&](auto DC, const double* blk, int p, int f, int side) {
-        constexpr int d = decltype(DC)::value;
+        const int d = DC.value; // compile-time for integral_constant, runtime for RunD
         const int a = p % N, b = p / N;
         double v[N];
 #pragma unroll
@@ -929,6 +960,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             pt_faces(ptC, std::true_type{}, gb);
             __syncthreads();
         } else if (AFFINE) {
+#ifdef DG_GEN_CTA_FACES
             face_lines(lineA, std::true_type{}, gb, NF);
             __syncthreads();
             GEN_STAMP(3);
@@ -940,6 +972,12 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             face_lines(lineC, std::true_type{}, gb, NF);
             __syncthreads();
             GEN_STAMP(5);
+#else
+            // ---------------- P3: face passes A -> B -> C, warp-local ----------------
+            face_warp(gb);
+            __syncthreads();
+            GEN_STAMP(3);
+#endif
         } else {
             all_faces(passB, gb);
             __syncthreads();
