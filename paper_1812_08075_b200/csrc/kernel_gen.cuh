@@ -183,9 +183,9 @@ struct Lay {
     // regions
     static constexpr int XS = 0;                                        // [2][NC][N3] own planes
     static constexpr int RXSZ = (NRL + NRH) * N3;                       // ring blocks: bd1[T2] bd2[T1] ad1[T2] ad2[T1]
-    // affine face passes: per face line (N points per thread, 2 buffers) for n <= 5, per face point
-    // (3 buffers) for n >= 6, where the NF n line tasks would leave too many of the NF n^2 threads idle
-    static constexpr bool FACE_LINES = N <= 5;
+    // affine face passes: per face line (N points per thread, 2 buffers, warp-local A -> B -> C) for n <= 6,
+    // per face point (3 buffers, CTA barriers between the passes) for n >= 7
+    static constexpr bool FACE_LINES = N <= 6;
     // face-slot strides chosen against bank conflicts of the line tasks (16-B pairs: 3 FS = 5 mod 8, so
     // both the t2-line (point-consecutive) and the t1-line (face-consecutive) task orders hit distinct
     // banks; 8-B line buffers: odd FB)
