@@ -5,6 +5,7 @@
 #include "kernel_cell.cuh"
 #include "kernel_gen.cuh"
 #include "kernel_quad.cuh"
+#include "kernel_quadw.cuh"
 #include "kernel_tile.cuh"
 #include "tables.h"
 
@@ -329,29 +330,52 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
 }
 
 // ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
-template <int N, bool AFF, bool COEF, bool DR = false>
+// n = 5: one warp per cell (k_quadw, measured faster) unless WARP = false; n <= 4 (too few lines per warp
+// phase) and n >= 6 (per-cell buffers beyond a warp's share of shared memory): k_quad
+template <int N, bool AFF, bool COEF, bool DR = false, bool WARP = true>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                         double* r, long long c0, long long c1, cudaStream_t st, const double*)
 {
-    using L = dg::qd::QLay<N, N + 1>;
     if (c1 <= c0) return cudaSuccess;
-    const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
-    dg::k_quad<N, N + 1, AFF, COEF, DR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
-        x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
-    return cudaGetLastError();
+    if constexpr (N == 5 && WARP) {
+        using W = dg::qw::WLay<N, N + 1>;
+        const long long grid = (c1 - c0 + W::WPB - 1) / W::WPB;
+        dg::k_quadw<N, N + 1, AFF, COEF, DR><<<(unsigned)grid, W::WPB * 32, W::BYTES, st>>>(
+            x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
+        return cudaGetLastError();
+    } else {
+        using L = dg::qd::QLay<N, N + 1>;
+        const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
+        dg::k_quad<N, N + 1, AFF, COEF, DR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
+            x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
+        return cudaGetLastError();
+    }
 }
 template <int N, bool AFF, bool COEF, bool DR = false>
 cudaError_t attr_quad()
 {
+    if constexpr (N == 5) {
+        cudaError_t e = cudaFuncSetAttribute(dg::k_quadw<N, N + 1, AFF, COEF, DR>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, dg::qw::WLay<N, N + 1>::BYTES);
+        if (e != cudaSuccess) return e;
+    }
     return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 dg::qd::QLay<N, N + 1>::BYTES);
 }
 template <int N>
-LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, bool dr = false)
+LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, bool dr = false, bool cta = false)
 {
     if (dr) {
         *err = attr_quad<N, false, false, true>();
-        return launch_quad<N, false, false, true>;
+        return cta ? launch_quad<N, false, false, true, false> : launch_quad<N, false, false, true>;
+    }
+    if (cta) {
+        if (aff) {
+            *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
+            return coef ? launch_quad<N, true, true, false, false> : launch_quad<N, true, false, false, false>;
+        }
+        *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
+        return coef ? launch_quad<N, false, true, false, false> : launch_quad<N, false, false, false, false>;
     }
     if (aff) {
         *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
@@ -360,16 +384,16 @@ LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, bool dr = false)
     *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
     return coef ? launch_quad<N, false, true> : launch_quad<N, false, false>;
 }
-LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, bool dr = false)
+LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, bool dr = false, bool cta = false)
 {
     switch (n) {
-    case 2: return pick_quad_n<2>(aff, coef, err, dr);
-    case 3: return pick_quad_n<3>(aff, coef, err, dr);
-    case 4: return pick_quad_n<4>(aff, coef, err, dr);
-    case 5: return pick_quad_n<5>(aff, coef, err, dr);
-    case 6: return pick_quad_n<6>(aff, coef, err, dr);
-    case 7: return pick_quad_n<7>(aff, coef, err, dr);
-    default: return pick_quad_n<8>(aff, coef, err, dr);
+    case 2: return pick_quad_n<2>(aff, coef, err, dr, cta);
+    case 3: return pick_quad_n<3>(aff, coef, err, dr, cta);
+    case 4: return pick_quad_n<4>(aff, coef, err, dr, cta);
+    case 5: return pick_quad_n<5>(aff, coef, err, dr, cta);
+    case 6: return pick_quad_n<6>(aff, coef, err, dr, cta);
+    case 7: return pick_quad_n<7>(aff, coef, err, dr, cta);
+    default: return pick_quad_n<8>(aff, coef, err, dr, cta);
     }
 }
 // interpolation / derivative of the n-node Lagrange basis at the m = n+1 Gauss points (long double
@@ -680,14 +704,17 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         case 8: fill_qtab<8>(H, Hm, c->qtab); break;
         }
         cudaError_t e = cudaSuccess;
+        const bool cta = getenv("DG_QUAD_CTA") != nullptr; // experiments / tests: the CTA-synchronous k_quad
         c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e,
-                              mesh->problem == DG_PROBLEM_DIFFREAC);
+                              mesh->problem == DG_PROBLEM_DIFFREAC, cta);
         if (e != cudaSuccess) {
             if (c->d_jac) cudaFree(c->d_jac);
             free(c);
             return fail(DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
         }
-        c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? "k_quad_diffreac" : "k_quad";
+        const bool warp = n == 5 && !cta;
+        c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? (warp ? "k_quadw_diffreac" : "k_quad_diffreac")
+                                                        : (warp ? "k_quadw" : "k_quad");
     }
     // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
     if (!c->quad) {
