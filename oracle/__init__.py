@@ -45,6 +45,8 @@ def lib():
                                                i64p, ctypes.c_int64, dp, dp, dp]
         L.oracle_apply_diffreac.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_double, dp, dp, i64p, ctypes.c_int64]
+        L.oracle_apply_nlreac.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_int, dp, dp, dp, i64p, ctypes.c_int64]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -121,6 +123,28 @@ def apply_diffreac(w, x: np.ndarray, cells=None) -> np.ndarray:
                                      cp, nc)
     if rc != 0:
         raise ValueError("oracle_apply_diffreac: invalid arguments")
+    return r
+
+
+def apply_nlreac(w, x: np.ndarray, u0: np.ndarray | None = None, cells=None) -> np.ndarray:
+    """The nonlinear variant of the paper's problem (reading R26: reaction c u^2, source
+    f = c|x|^4 - 10|x|^2 - 6, same K, g, penalty as apply_diffreac). u0 is None: the residual R(x);
+    else the Jacobian action J(u0) x at the linearization point u0."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    assert x.size == w.ndofs
+    r = np.full(w.ndofs, np.nan)
+    if u0 is not None:
+        u0 = np.ascontiguousarray(u0, dtype=np.float64)
+        assert u0.size == w.ndofs
+    if cells is None:
+        cp, nc = None, 0
+    else:
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        cp, nc = _i64p(cells), len(cells)
+    rc = lib().oracle_apply_nlreac(w.N[0], w.N[1], w.N[2], w.k, w.m, float(w.penalty_scale), int(u0 is not None),
+                                   None if u0 is None else _dp(u0), _dp(x), _dp(r), cp, nc)
+    if rc != 0:
+        raise ValueError("oracle_apply_nlreac: invalid arguments")
     return r
 
 

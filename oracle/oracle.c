@@ -375,7 +375,19 @@ static void Kmat(const double* x, double* K)
         for (int b = 0; b < 3; ++b) K[3 * a + b] = x[a] * x[b] + (a == b ? 1.0 : 0.0);
 }
 
-static void cell_residual_dr(const otab* T, int i0, int i1, int i2, const double* const xs[7], double alpha, double* r)
+/*
+ * mode 0: the paper's linear problem above.
+ * mode 1: its nonlinear variant (reading R26): reaction c u^2 in place of c u, source
+ *         f = c |x|^4 - 10 |x|^2 - 6 so that u = |x|^2 stays the exact solution (-div(K grad |x|^2) = -10|x|^2 - 6);
+ *         residual R(x) with the volume term (c u^2 - f, v).
+ * mode 2: the action of its Jacobian at the linearization point u0:
+ *         J(u0) z = d/de R(u0 + e z) at e = 0: volume (K grad z, grad v) + (2 c u0 z, v); the face terms
+ *         are those of R with z in place of u and g = 0 (they are affine in u; g does not depend on it).
+ *         xs[] hold z; u0s is the cell's block of u0 (the linearization point, evaluated with the same
+ *         basis at the same quadrature points).
+ */
+static void cell_residual_dr(const otab* T, int i0, int i1, int i2, const double* const xs[7], double alpha, double* r,
+                             int mode, const double* u0s)
 {
     const int n = T->n, m = T->m, n3 = n * n * n;
     const int ic[3] = {i0, i1, i2};
@@ -395,10 +407,23 @@ static void cell_residual_dr(const otab* T, int i0, int i1, int i2, const double
                 Kmat(xq, K);
                 for (int a = 0; a < 3; ++a) Kg[a] = K[3 * a] * g[0] + K[3 * a + 1] * g[1] + K[3 * a + 2] * g[2];
                 const double W = T->qw[q0] * T->qw[q1] * T->qw[q2] * vol;
+                /* the zeroth-order term q(u) - f, multiplied by v */
+                double react;
+                if (mode == 0) {
+                    react = cr * u - f;
+                } else if (mode == 1) {
+                    const double s = xq[0] * xq[0] + xq[1] * xq[1] + xq[2] * xq[2];
+                    const double fnl = cr * s * s - 10.0 * s - 6.0;
+                    react = cr * u * u - fnl;
+                } else {
+                    double u0, gh0[3];
+                    eval_u(n3, u0s, tab, &u0, gh0);
+                    react = 2.0 * cr * u0 * u;
+                }
                 for (int I = 0; I < n3; ++I) {
                     const double* ti = tab + 4 * I;
                     const double gp0 = ti[1] / h[0], gp1 = ti[2] / h[1], gp2 = ti[3] / h[2];
-                    r[I] += W * (Kg[0] * gp0 + Kg[1] * gp1 + Kg[2] * gp2 + cr * u * ti[0] - f * ti[0]);
+                    r[I] += W * (Kg[0] * gp0 + Kg[1] * gp1 + Kg[2] * gp2 + react * ti[0]);
                 }
             }
     /* faces */
@@ -427,7 +452,7 @@ static void cell_residual_dr(const otab* T, int i0, int i1, int i2, const double
                         /* outer normal n = +-e_d; [u] = u, {K grad u} = K grad u (one-sided) */
                         const double sn = side ? 1.0 : -1.0;
                         const double Kgn = sn * (K[3 * d] * gs[0] + K[3 * d + 1] * gs[1] + K[3 * d + 2] * gs[2]);
-                        const double g = xF[0] * xF[0] + xF[1] * xF[1] + xF[2] * xF[2];
+                        const double g = (mode == 2) ? 0.0 : xF[0] * xF[0] + xF[1] * xF[1] + xF[2] * xF[2];
                         for (int I = 0; I < n3; ++I) {
                             const double* ti = tabself + off + 4 * I;
                             const double gp[3] = {ti[1] / h[0], ti[2] / h[1], ti[3] / h[2]};
@@ -465,8 +490,8 @@ static void cell_residual_dr(const otab* T, int i0, int i1, int i2, const double
  * The paper's diffusion-reaction residual (cell_residual_dr) on the non-periodic unit cube; x, r global
  * canonical vectors; cells == NULL => all cells. Returns 0 or -1.
  */
-int oracle_apply_diffreac(int N0, int N1, int N2, int k, int m, double alpha, const double* x, double* r,
-                          const int64_t* cells, int64_t ncells)
+static int apply_dr(int N0, int N1, int N2, int k, int m, double alpha, int mode, const double* u0, const double* x,
+                    double* r, const int64_t* cells, int64_t ncells)
 {
     otab T;
     if (N0 < 1 || N1 < 1 || N2 < 1) return -1;
@@ -489,10 +514,27 @@ int oracle_apply_diffreac(int N0, int N1, int N2, int k, int m, double alpha, co
                 xs[1 + 2 * d + sgn] = (jc[d] < 0 || jc[d] >= T.N[d]) ? NULL
                                                                      : x + (((int64_t)jc[0] * N1 + jc[1]) * N2 + jc[2]) * n3;
             }
-        cell_residual_dr(&T, i0, i1, i2, xs, alpha, r + c * n3);
+        cell_residual_dr(&T, i0, i1, i2, xs, alpha, r + c * n3, mode, u0 ? u0 + c * n3 : NULL);
     }
     otab_free(&T);
     return 0;
+}
+
+int oracle_apply_diffreac(int N0, int N1, int N2, int k, int m, double alpha, const double* x, double* r,
+                          const int64_t* cells, int64_t ncells)
+{
+    return apply_dr(N0, N1, N2, k, m, alpha, 0, NULL, x, r, cells, ncells);
+}
+
+/*
+ * The nonlinear variant (cell_residual_dr modes 1 and 2): jacobian == 0 -> R(x); jacobian == 1 -> J(u0) x.
+ * u0: global canonical vector (jacobian == 1 only, else may be NULL). Returns 0 or -1.
+ */
+int oracle_apply_nlreac(int N0, int N1, int N2, int k, int m, double alpha, int jacobian, const double* u0,
+                        const double* x, double* r, const int64_t* cells, int64_t ncells)
+{
+    if (jacobian && !u0) return -1;
+    return apply_dr(N0, N1, N2, k, m, alpha, jacobian ? 2 : 1, jacobian ? u0 : NULL, x, r, cells, ncells);
 }
 
 /* Geometry of a canonical cell: row-major J_T. geom_kind 0: diag(1/N); 1: from jac[9 c ..]. */

@@ -91,7 +91,7 @@ class Workload:
     penalty_scale: float = 10.0  # gamma = penalty_scale * k (k+1) / h  (BASELINE.json configs)
     quad: int = -1              # Gauss points per direction; -1 -> k + 1
     gpus: tuple = (1,)
-    problem: int = 0            # 0: periodic SIPG of the configs; 1: the paper's diffusion-reaction problem
+    problem: int = 0            # 0: periodic SIPG of the configs; 1: the paper's diffusion-reaction problem; 2: its nonlinear variant
                                 #    (non-periodic cube, Dirichlet g = |x|^2, K = xx^T + I, c = 10,
                                 #    f = -6; penalty_scale = alpha = 3, gamma = alpha k(k+2) |F|/|T|)
     text: str = ""
@@ -137,6 +137,15 @@ def diffreac(k: int, N, seed: int = 11, quad: int = -1, alpha: float = 3.0) -> W
         N = (N, N, N)
     return Workload(f"diffreac_k{k}_N{N[0]}x{N[1]}x{N[2]}_m{k + 1 if quad < 0 else quad}", k, tuple(N), 0, 0,
                     seed=seed, penalty_scale=alpha, quad=quad, problem=1)
+
+
+def nlreac(k: int, N, seed: int = 13, alpha: float = 3.0) -> Workload:
+    """The nonlinear variant of the paper's problem (reading R26: reaction c u^2)
+    on an axiparallel N0 x N1 x N2 mesh of (0,1)^3, k+2 Gauss points per direction."""
+    if isinstance(N, int):
+        N = (N, N, N)
+    return Workload(f"nlreac_k{k}_N{N[0]}x{N[1]}x{N[2]}_m{k + 2}", k, tuple(N), 0, 0,
+                    seed=seed, penalty_scale=alpha, quad=k + 2, problem=2)
 
 
 def small(k: int, N, geom_kind: int = 0, coeff_kind: int = 0, seed: int = 7, quad: int = -1) -> Workload:

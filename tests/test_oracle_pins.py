@@ -405,3 +405,60 @@ def test_diffreac_rhs_terms():
     p1 = oracle.apply_diffreac(w1, z) - oracle.apply_diffreac(w0, z)
     p2 = oracle.apply_diffreac(w2, z) - oracle.apply_diffreac(w0, z)
     assert np.abs(p2 - 2 * p1).max() <= 1e-12 * np.abs(p2).max()
+
+
+# ---------------------------------------------------------------- the nonlinear variant
+@pytest.mark.parametrize("k,N", [(2, (2, 3, 2)), (3, (2, 2, 3))])
+def test_nlreac_manufactured_solution(k, N):
+    """Reading R26: -div(K grad u) + c u^2 = f with f = c|x|^4 - 10|x|^2 - 6 is solved by u = |x|^2 = g
+    (-div((xx^T + I) 2x) = -10|x|^2 - 6); every term is a polynomial the k+2 point rule integrates exactly
+    (u^2 v: degree 4 + k <= 2k + 3 per direction), so the residual of the interpolant vanishes."""
+    w = synth.nlreac(k, N)
+    x = _interp_fn(w, lambda a, b, c: a * a + b * b + c * c)
+    r = oracle.apply_nlreac(w, x)
+    r0 = oracle.apply_nlreac(w, np.zeros_like(x))
+    assert np.abs(r).max() <= 1e-11 * np.abs(r0).max()
+    # not vacuous: a perturbed function has a residual far from zero
+    y = _interp_fn(w, lambda a, b, c: a * a + b * b + c * c + 0.01 * a * b)
+    assert np.abs(oracle.apply_nlreac(w, y)).max() > 1e-4 * np.abs(r0).max()
+
+
+@pytest.mark.parametrize("k,N", [(1, (3, 2, 2)), (2, (2, 2, 3)), (3, (2, 2, 2))])
+def test_nlreac_jacobian_is_the_exact_derivative(k, N):
+    """R is quadratic in x, so the central difference is exact for any step:
+    J(u) z = (R(u + s z) - R(u - s z)) / (2 s) (the action of dR/dc on z). A dropped factor 2 in
+    the reaction term, a g-term left in the Jacobian or a wrong linearization point fails it."""
+    w = synth.nlreac(k, N)
+    rng = np.random.default_rng(5)
+    u = rng.standard_normal(w.ndofs)
+    z = rng.standard_normal(w.ndofs)
+    J = oracle.apply_nlreac(w, z, u0=u)
+    for s in (1.0, 0.37):
+        fd = (oracle.apply_nlreac(w, u + s * z) - oracle.apply_nlreac(w, u - s * z)) / (2 * s)
+        assert np.abs(J - fd).max() <= 1e-11 * np.abs(J).max()
+
+
+def test_nlreac_jacobian_at_constant_half_is_the_linear_operator():
+    """At u0 = 1/2 the reaction derivative 2 c u0 = c: J(1/2) z = a(z, .) of the paper's linear problem, i.e.
+    apply_diffreac(z) - apply_diffreac(0) (itself pinned by its manufactured solution)."""
+    k, N = 2, (3, 2, 2)
+    wn = synth.nlreac(k, N)
+    wl = synth.diffreac(k, N, quad=k + 2)
+    z = np.random.default_rng(9).standard_normal(wn.ndofs)
+    J = oracle.apply_nlreac(wn, z, u0=np.full(wn.ndofs, 0.5))
+    A = oracle.apply_diffreac(wl, z) - oracle.apply_diffreac(wl, np.zeros_like(z))
+    assert np.abs(J - A).max() <= 1e-12 * np.abs(A).max()
+
+
+def test_nlreac_jacobian_symmetric():
+    """J(u0) = SIPG (theta = -1) + the mass matrix weighted by 2 c u0: symmetric for any u0."""
+    k, N = 1, (2, 2, 3)
+    w = synth.nlreac(k, N)
+    u0 = np.random.default_rng(3).standard_normal(w.ndofs)
+    nd = w.ndofs
+    J = np.zeros((nd, nd))
+    for j in range(nd):
+        e = np.zeros(nd)
+        e[j] = 1.0
+        J[:, j] = oracle.apply_nlreac(w, e, u0=u0)
+    assert np.abs(J - J.T).max() <= 1e-12 * np.abs(J).max()
