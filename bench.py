@@ -101,7 +101,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
-def oracle_sample_rate(w, budget_s: float, seed: int = 2024):
+def oracle_sample_rate(w, budget_s: float, seed: int = 2024, jacobian: bool = False):
     """Time the oracle (as it stands) on a deterministic random sample of cells of workload w,
     sized to roughly budget_s seconds of host CPU work. Returns (DOF/s, cells, seconds, threads)."""
     import numpy as np
@@ -113,10 +113,15 @@ def oracle_sample_rate(w, budget_s: float, seed: int = 2024):
 
     def run(ncell):
         cells = np.sort(rng.choice(w.ncells, ncell, replace=False)).astype(np.int64)
-        if w.problem == 1:  # the paper's problem: the oracle on the whole (small) host vector, sampled rows
+        if w.problem in (1, 2):  # the paper's problem: the oracle on the whole (small) host vector, sampled rows
             x = synth.x_np(w)
             t0 = time.perf_counter()
-            oracle.apply_diffreac(w, x, cells)
+            if w.problem == 1:
+                oracle.apply_diffreac(w, x, cells)
+            elif jacobian:
+                oracle.apply_nlreac(w, x, u0=np.sin(x), cells=cells)
+            else:
+                oracle.apply_nlreac(w, x, cells=cells)
             return time.perf_counter() - t0
         nb = oracle.neighbours(w, cells)
         x7 = synth.x_cells_np(w, nb.reshape(-1)).reshape(len(cells), 7, n3)
@@ -144,11 +149,11 @@ def run_reference(args, w, rank):
         return 0
     budget = max(0.5, min(5.0, 150.0 / (args.steps + args.warmup)))
     for _ in range(args.warmup):
-        oracle_sample_rate(w, budget)
+        oracle_sample_rate(w, budget, jacobian=args.jacobian)
     rates, cells, secs = [], 0, 0.0
     th = 1
     for _ in range(args.steps):
-        v, c, t, th = oracle_sample_rate(w, budget)
+        v, c, t, th = oracle_sample_rate(w, budget, jacobian=args.jacobian)
         rates.append(v)
         cells, secs = c, t
     value = statistics.median(rates)
@@ -171,7 +176,8 @@ def _config(w, ngpu):
             "geometry": "axis-aligned" if w.geom_kind == 0 else "per-cell affine",
             "coefficient": "1" if w.coeff_kind == 0 else "1+0.5sin(2pi x0)cos(2pi x1)",
             "penalty": (f"{w.penalty_scale:g}*k(k+1)/h" if w.problem == 0 else f"alpha={w.penalty_scale:g}: alpha*k(k+2)|F|/|T|"),
-            "problem": "periodic SIPG (configs)" if w.problem == 0 else "diffusion-reaction, Dirichlet g=|x|^2 (P:L945-1003)",
+            "problem": ("periodic SIPG (configs)", "diffusion-reaction, Dirichlet g=|x|^2 (P:L945-1003)",
+                        "nonlinear diffusion-reaction c u^2 (R26), Dirichlet g=|x|^2")[w.problem],
             "parallelism": f"x0-slab{ngpu}",
             "l2": f"inputs larger than L2 ({8 * w.ndofs / 1e9:.2f} GB per vector vs 126 MB L2)"
             if 8 * w.ndofs > 2 * 126e6 else "L2 flushed between steps"}
@@ -189,8 +195,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--problem", default="config", choices=["config", "diffreac"],
-                    help="diffreac: the paper's diffusion-reaction problem (SURVEY §8(f1)) with --k / --N, k+2 points")
+    ap.add_argument("--problem", default="config", choices=["config", "diffreac", "nlreac"],
+                    help="diffreac: the paper's diffusion-reaction problem (SURVEY §8(f1)) with --k / --N, k+2 points; "
+                         "nlreac: its nonlinear variant (SURVEY §8(f3), R26)")
+    ap.add_argument("--jacobian", action="store_true",
+                    help="nlreac: time the Jacobian action J(u0) z (dg_apply_jacobian) instead of the residual")
     ap.add_argument("--k", type=int, default=3)
     ap.add_argument("--N", type=int, default=64)
     ap.add_argument("--quad", type=int, default=-1,
@@ -203,6 +212,10 @@ def main():
     w = synth.CONFIGS[args.config]
     if args.problem == "diffreac":
         w = synth.diffreac(args.k, args.N, quad=args.k + 2)
+    if args.problem == "nlreac":
+        w = synth.nlreac(args.k, args.N)
+    if args.jacobian and w.problem != 2:
+        raise SystemExit("--jacobian needs --problem nlreac")
     if args.quad > 0 and args.quad != w.k + 1:
         import dataclasses
         w = dataclasses.replace(w, quad=args.quad, name=f"{w.name}_quad{args.quad}")
@@ -232,6 +245,13 @@ def main():
     op = sop.op
     x = synth.x_torch(w, start=sop.offset, count=sop.ndofs, device=dev)
     r = torch.empty_like(x)
+    u0 = torch.sin(x) if args.jacobian else None  # linearization point (same distribution scale as x)
+
+    def step(xin, rout):
+        if args.jacobian:
+            sop.apply_jacobian(u0, xin, rout)
+        else:
+            sop.apply(xin, rout)
     torch.cuda.synchronize()
 
     def barrier():
@@ -241,7 +261,7 @@ def main():
 
     # ---- warm-up
     for _ in range(args.warmup):
-        sop.apply(x, r)
+        step(x, r)
     barrier()
 
     # ---- timed region: K steps, events on the launching stream; per-step event pairs give the
@@ -264,7 +284,7 @@ def main():
             if flush is not None:
                 flush.fill_(float(i))
             ev[i][0].record(stream)
-            sop.apply(x, r)
+            step(x, r)
             ev[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
@@ -278,7 +298,7 @@ def main():
         barrier()
         w0.record(stream)
         for _ in range(K):
-            sop.apply(x, r)
+            step(x, r)
         w1.record(stream)
         torch.cuda.synchronize()
         warm_ms = w0.elapsed_time(w1) / K
@@ -298,6 +318,11 @@ def main():
     fp64_meas, _ = dg.dg_bench_fp64(local_rank, 4000)
     kern_ms = statistics.mean(step_ms)
     F = op.alg_flops
+    if args.jacobian:
+        # J(u0) z: + u0 at the m^3 points (2 (n^3 m + n^2 m^2 + n m^3) per cell), reaction 2 c u0 z without f
+        # (6 flops per point fewer than the residual's c u^2 - f(x)); DESIGN.md §5
+        nn, mm = w.n, w.m
+        F += (2.0 * (nn ** 3 * mm + nn ** 2 * mm ** 2 + nn * mm ** 3) - 6.0 * mm ** 3) * (sop.ndofs / nn ** 3)
     B = op.alg_bytes
     t_flop = F / (fp64_nominal * 1e12)
     t_byte = B / (pk["hbm_gbs"] * 1e9)
@@ -329,7 +354,8 @@ def main():
         xh = x.cpu().pin_memory()
         rh = torch.empty_like(xh).pin_memory()
         KE = max(1, args.e2e_steps)
-        if world == 1:
+        uh = u0.cpu().pin_memory() if args.jacobian else None
+        if world == 1 and not args.jacobian:
             op.apply_host(xh, rh)  # warm-up (allocates staging buffers)
             barrier()
             t0 = time.perf_counter()
@@ -340,9 +366,15 @@ def main():
             xd = torch.empty_like(x)
             rd = torch.empty_like(x)
 
+            ud = torch.empty_like(x) if args.jacobian else None
+
             def host_step():
                 xd.copy_(xh, non_blocking=True)
-                sop.apply(xd, rd)
+                if args.jacobian:
+                    ud.copy_(uh, non_blocking=True)
+                    sop.apply_jacobian(ud, xd, rd)
+                else:
+                    sop.apply(xd, rd)
                 rh.copy_(rd, non_blocking=True)
                 torch.cuda.synchronize()
             host_step()
@@ -351,19 +383,22 @@ def main():
             for _ in range(KE):
                 host_step()
             te = time.perf_counter() - t0
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = tt.item()
-        e2e = {"value": w.ndofs / (te / KE), "unit": UNIT, "h2d_bytes_per_step": 8 * w.ndofs,
+            if world > 1:
+                tt = torch.tensor([te], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te = tt.item()
+        e2e = {"value": w.ndofs / (te / KE), "unit": UNIT,
+               "h2d_bytes_per_step": (16 if args.jacobian else 8) * w.ndofs,
                "d2h_bytes_per_step": 8 * w.ndofs, "steps": KE,
-               "how": "dg_apply_host (pinned host x -> H2D -> kernels -> D2H r, plane-chunk pipelined)"
-               if world == 1 else "per rank: pinned H2D of the slab, halo exchange + kernels, D2H of r"}
-        del xh, rh
+               "how": "pinned H2D of u0 and z, dg_apply_jacobian, D2H of r" if args.jacobian else
+               ("dg_apply_host (pinned host x -> H2D -> kernels -> D2H r, plane-chunk pipelined)"
+                if world == 1 else "per rank: pinned H2D of the slab, halo exchange + kernels, D2H of r")}
+        del xh, rh, uh
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        v, cells, secs, th = oracle_sample_rate(w, args.cpu_seconds)
+        v, cells, secs, th = oracle_sample_rate(w, args.cpu_seconds, jacobian=args.jacobian)
         cpu = {"value": v, "unit": UNIT, "cores": th, "kind": "oracle",
                "sample": f"{cells} random cells ({cells * w.n ** 3} DOFs) of {w.name}, {secs:.1f} s"}
 
@@ -378,6 +413,9 @@ def main():
         "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
         "warm_ms_per_step": warm_ms,
     }
+    if args.jacobian:
+        line["config"]["operator"] = "Jacobian action J(u0) z (dg_apply_jacobian), u0 = sin(x)"
+        line["roofline"]["kernel"] = op.kernel_name + " (mode 3: Jacobian)"
     if world > 1:
         dist.barrier()
     if rank == 0:

@@ -55,6 +55,10 @@ extern "C" {
                                  r = R(x) = A x - b (Eq. diffreac_weak incl. the f and g terms); axiparallel
                                  (DG_GEOM_AXIS) only, coeff_kind ignored, quad = k+2 (k_quad);
                                  gamma_F = penalty_scale k (k+2) |F| / |T| (the paper: penalty_scale = alpha = 3) */
+#define DG_PROBLEM_NLREAC 2   /* its nonlinear variant (reading R26): reaction 10 u^2 in
+                                 place of 10 u, f = 10|x|^4 - 10|x|^2 - 6 (u = |x|^2 stays the exact solution),
+                                 K, g, penalty, restrictions as DG_PROBLEM_DIFFREAC; dg_apply returns the
+                                 nonlinear residual R(x), dg_apply_jacobian* the action J(u0) z of its Jacobian */
 
 typedef struct dg_ctx dg_ctx;
 
@@ -72,7 +76,7 @@ typedef struct dg_mesh {
     double penalty_scale;  /* gamma_F = penalty_scale * k (k+1) * N[d] on faces with normal d (> 0) */
     int32_t device;        /* CUDA device ordinal */
     void* stream;          /* cudaStream_t on which dg_apply* enqueue work (NULL: legacy default stream) */
-    int32_t problem;       /* DG_PROBLEM_PERIODIC (default, 0) or DG_PROBLEM_DIFFREAC */
+    int32_t problem;       /* DG_PROBLEM_PERIODIC (default, 0), DG_PROBLEM_DIFFREAC or DG_PROBLEM_NLREAC */
 } dg_mesh;
 
 /* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,
@@ -103,6 +107,19 @@ int dg_apply(dg_ctx* ctx, const double* x, double* r);
  * Asynchronous on the context stream. */
 int dg_apply_planes(dg_ctx* ctx, const double* x, const double* x_below, const double* x_above, double* r,
                     int p_begin, int p_end);
+
+/* The action of the Jacobian of a DG_PROBLEM_NLREAC residual at the linearization point u0
+ * ("not only the solution needs to be evaluated in step 1 ... but also the given
+ * linearization point"; A_i(c, z) = (J z)_i, depending on both c and z):
+ *   r = J(u0) z = (K grad z, grad v) + (20 u0 z, v) + the SIPG face terms of z with g = 0.
+ * u0 and z are evaluated at the quadrature points by the same sum-factorisation sweeps in one
+ * kernel (k_quad mode 3). Arguments as dg_apply / dg_apply_planes (z takes x's place, z_below /
+ * z_above its halo planes); u0: DEVICE, dg_local_ndofs() doubles of the owned planes only (the
+ * Jacobian's u0-dependence is cell-local), 8-byte aligned, must not overlap r.
+ * DG_ERR_UNSUPPORTED unless the context's problem is DG_PROBLEM_NLREAC. Asynchronous. */
+int dg_apply_jacobian(dg_ctx* ctx, const double* u0, const double* z, double* r);
+int dg_apply_jacobian_planes(dg_ctx* ctx, const double* u0, const double* z, const double* z_below,
+                             const double* z_above, double* r, int p_begin, int p_end);
 
 /* End-to-end form with HOST buffers (whole-mesh context): copies x host->device, applies A,
  * copies r device->host, pipelined over x0-plane chunks on three streams (H2D, compute, D2H)

@@ -332,50 +332,54 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
 // ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
 // n = 5: one warp per cell (k_quadw, measured faster) unless WARP = false; n <= 4 (too few lines per warp
 // phase) and n >= 6 (per-cell buffers beyond a warp's share of shared memory): k_quad
-template <int N, bool AFF, bool COEF, bool DR = false, bool WARP = true>
+template <int N, bool AFF, bool COEF, int PR = 0, bool WARP = true>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                        double* r, long long c0, long long c1, cudaStream_t st, const double*)
+                        double* r, long long c0, long long c1, cudaStream_t st, const double* u0)
 {
     if (c1 <= c0) return cudaSuccess;
-    if constexpr (N == 5 && WARP) {
+    if constexpr (N == 5 && WARP && PR <= 1) {
         using W = dg::qw::WLay<N, N + 1>;
         const long long grid = (c1 - c0 + W::WPB - 1) / W::WPB;
-        dg::k_quadw<N, N + 1, AFF, COEF, DR><<<(unsigned)grid, W::WPB * 32, W::BYTES, st>>>(
+        dg::k_quadw<N, N + 1, AFF, COEF, PR == 1><<<(unsigned)grid, W::WPB * 32, W::BYTES, st>>>(
             x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
         return cudaGetLastError();
     } else {
-        using L = dg::qd::QLay<N, N + 1>;
+        using L = dg::qd::QLay<N, N + 1, PR == 3>;
         const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
-        dg::k_quad<N, N + 1, AFF, COEF, DR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
-            x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
+        dg::k_quad<N, N + 1, AFF, COEF, PR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
+            x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M, u0);
         return cudaGetLastError();
     }
 }
-template <int N, bool AFF, bool COEF, bool DR = false>
+template <int N, bool AFF, bool COEF, int PR = 0>
 cudaError_t attr_quad()
 {
-    if constexpr (N == 5) {
-        cudaError_t e = cudaFuncSetAttribute(dg::k_quadw<N, N + 1, AFF, COEF, DR>,
+    if constexpr (N == 5 && PR <= 1) {
+        cudaError_t e = cudaFuncSetAttribute(dg::k_quadw<N, N + 1, AFF, COEF, PR == 1>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, dg::qw::WLay<N, N + 1>::BYTES);
         if (e != cudaSuccess) return e;
     }
-    return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF, DR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                dg::qd::QLay<N, N + 1>::BYTES);
+    return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dg::qd::QLay<N, N + 1, PR == 3>::BYTES);
 }
+// pr: the problem mode of k_quad (0 periodic, 1 diffusion-reaction, 2 its nonlinear variant, 3 the Jacobian
+// action of the nonlinear variant; 2 and 3 always use the CTA kernel)
 template <int N>
-LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, bool dr = false, bool cta = false)
+LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0, bool cta = false)
 {
-    if (dr) {
-        *err = attr_quad<N, false, false, true>();
-        return cta ? launch_quad<N, false, false, true, false> : launch_quad<N, false, false, true>;
+    if (pr == 1) {
+        *err = attr_quad<N, false, false, 1>();
+        return cta ? launch_quad<N, false, false, 1, false> : launch_quad<N, false, false, 1>;
     }
+    if (pr == 2) { *err = attr_quad<N, false, false, 2>(); return launch_quad<N, false, false, 2, false>; }
+    if (pr == 3) { *err = attr_quad<N, false, false, 3>(); return launch_quad<N, false, false, 3, false>; }
     if (cta) {
         if (aff) {
             *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
-            return coef ? launch_quad<N, true, true, false, false> : launch_quad<N, true, false, false, false>;
+            return coef ? launch_quad<N, true, true, 0, false> : launch_quad<N, true, false, 0, false>;
         }
         *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
-        return coef ? launch_quad<N, false, true, false, false> : launch_quad<N, false, false, false, false>;
+        return coef ? launch_quad<N, false, true, 0, false> : launch_quad<N, false, false, 0, false>;
     }
     if (aff) {
         *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
@@ -384,16 +388,16 @@ LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, bool dr = false, boo
     *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
     return coef ? launch_quad<N, false, true> : launch_quad<N, false, false>;
 }
-LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, bool dr = false, bool cta = false)
+LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, int pr = 0, bool cta = false)
 {
     switch (n) {
-    case 2: return pick_quad_n<2>(aff, coef, err, dr, cta);
-    case 3: return pick_quad_n<3>(aff, coef, err, dr, cta);
-    case 4: return pick_quad_n<4>(aff, coef, err, dr, cta);
-    case 5: return pick_quad_n<5>(aff, coef, err, dr, cta);
-    case 6: return pick_quad_n<6>(aff, coef, err, dr, cta);
-    case 7: return pick_quad_n<7>(aff, coef, err, dr, cta);
-    default: return pick_quad_n<8>(aff, coef, err, dr, cta);
+    case 2: return pick_quad_n<2>(aff, coef, err, pr, cta);
+    case 3: return pick_quad_n<3>(aff, coef, err, pr, cta);
+    case 4: return pick_quad_n<4>(aff, coef, err, pr, cta);
+    case 5: return pick_quad_n<5>(aff, coef, err, pr, cta);
+    case 6: return pick_quad_n<6>(aff, coef, err, pr, cta);
+    case 7: return pick_quad_n<7>(aff, coef, err, pr, cta);
+    default: return pick_quad_n<8>(aff, coef, err, pr, cta);
     }
 }
 // interpolation / derivative of the n-node Lagrange basis at the m = n+1 Gauss points (long double
@@ -510,6 +514,7 @@ struct dg_ctx {
     dg::MeshArgs M;
     alignas(16) unsigned char tab[sizeof(dg::Tab<dg::kMaxN>)];
     LaunchFn launch;
+    LaunchFn launch_jac; // DG_PROBLEM_NLREAC: the Jacobian action (k_quad mode 3)
     const char* kname;
     // axis-aligned n = 8 fast path (k_axis8)
     bool ax8;
@@ -539,9 +544,13 @@ struct dg_ctx {
 };
 
 static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0,
-                                 int p1, cudaStream_t st)
+                                 int p1, cudaStream_t st, const double* u0 = nullptr)
 {
     if (p1 <= p0) return cudaSuccess;
+    if (u0) { // the Jacobian action of the nonlinear variant (dg_apply_jacobian*)
+        const long long pcq = c->M.plane_cells;
+        return c->launch_jac(c->qtab, c->M, x, xb, xa, r, (long long)p0 * pcq, (long long)p1 * pcq, st, u0);
+    }
     if (c->ax8) {
         if (c->tmap_ptr != x) {
             cuuint64_t dims[2] = {16, (cuuint64_t)(c->local_dofs / 16)};
@@ -625,10 +634,11 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (mesh->coeff_kind != DG_COEFF_ONE && mesh->coeff_kind != DG_COEFF_SINCOS)
         return fail(DG_ERR_INVALID, "dg_setup: coeff_kind=%d", mesh->coeff_kind);
     if (!(mesh->penalty_scale > 0.0)) return fail(DG_ERR_INVALID, "dg_setup: penalty_scale must be > 0");
-    if (mesh->problem != DG_PROBLEM_PERIODIC && mesh->problem != DG_PROBLEM_DIFFREAC)
+    if (mesh->problem != DG_PROBLEM_PERIODIC && mesh->problem != DG_PROBLEM_DIFFREAC && mesh->problem != DG_PROBLEM_NLREAC)
         return fail(DG_ERR_INVALID, "dg_setup: problem=%d", mesh->problem);
-    if (mesh->problem == DG_PROBLEM_DIFFREAC && (mesh->geom_kind != DG_GEOM_AXIS || quad != k + 2))
-        return fail(DG_ERR_UNSUPPORTED, "dg_setup: the diffusion-reaction problem needs DG_GEOM_AXIS and quad = k+2");
+    const bool dr = mesh->problem == DG_PROBLEM_DIFFREAC || mesh->problem == DG_PROBLEM_NLREAC;
+    if (dr && (mesh->geom_kind != DG_GEOM_AXIS || mesh->coeff_kind != DG_COEFF_ONE || quad != k + 2))
+        return fail(DG_ERR_UNSUPPORTED, "dg_setup: the diffusion-reaction problems need DG_GEOM_AXIS, DG_COEFF_ONE and quad = k+2");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -667,7 +677,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         M.h[d] = 1.0 / mesh->N[d];
         M.gamma[d] = mesh->penalty_scale * k * (k + 1) * (double)mesh->N[d];
         // the paper's problem: gamma_F = alpha k (k+d-1) |F| / |T| = alpha k (k+2) / h_d
-        if (mesh->problem == DG_PROBLEM_DIFFREAC) M.gamma[d] = mesh->penalty_scale * k * (k + 2) * (double)mesh->N[d];
+        if (dr) M.gamma[d] = mesh->penalty_scale * k * (k + 2) * (double)mesh->N[d];
     }
     M.jac = nullptr;
     const int64_t n3 = (int64_t)n * n * n;
@@ -705,8 +715,9 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         }
         cudaError_t e = cudaSuccess;
         const bool cta = getenv("DG_QUAD_CTA") != nullptr; // experiments / tests: the CTA-synchronous k_quad
-        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e,
-                              mesh->problem == DG_PROBLEM_DIFFREAC, cta);
+        const int pr = mesh->problem == DG_PROBLEM_DIFFREAC ? 1 : (mesh->problem == DG_PROBLEM_NLREAC ? 2 : 0);
+        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr, cta);
+        if (e == cudaSuccess && pr == 2) c->launch_jac = pick_quad(n, false, false, &e, 3, true);
         if (e != cudaSuccess) {
             if (c->d_jac) cudaFree(c->d_jac);
             free(c);
@@ -714,6 +725,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         }
         const bool warp = n == 5 && !cta;
         c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? (warp ? "k_quadw_diffreac" : "k_quad_diffreac")
+                   : mesh->problem == DG_PROBLEM_NLREAC ? "k_quad_nlreac"
                                                         : (warp ? "k_quadw" : "k_quad");
     }
     // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
@@ -925,7 +937,9 @@ double dg_alg_flops(const dg_ctx* c)
         const double face = 2.0 * (8 * n * n * n + 9 * n * n * m + 12 * n * m * m) + (40.0 + Cc) * m * m;
         // the diffusion-reaction problem adds u at the M^3 points (2 n m^3), its back-projection (2 n m^3),
         // the full K (12 m^3) and the reaction / source term (3 m^3)
-        const double dr = (c->mesh.problem == DG_PROBLEM_DIFFREAC) ? 4 * n * m * m * m + 15 * m * m * m : 0.0;
+        // (the nonlinear variant: 6 more flops per point for c u^2 - f(x))
+        const double dr = (c->mesh.problem == DG_PROBLEM_DIFFREAC) ? 4 * n * m * m * m + 15 * m * m * m
+                          : (c->mesh.problem == DG_PROBLEM_NLREAC) ? 4 * n * m * m * m + 21 * m * m * m : 0.0;
         return (vol + dr + 3.0 * face) / (n * n * n) * (double)c->local_dofs;
     }
     if (c->mesh.geom_kind == DG_GEOM_AXIS && c->mesh.coeff_kind == DG_COEFF_ONE)
@@ -948,7 +962,40 @@ double dg_alg_bytes(const dg_ctx* c)
     return b;
 }
 
+static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1,
+                             const double* u0);
+
 int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1)
+{
+    return apply_planes_impl(c, x, xb, xa, r, p0, p1, nullptr);
+}
+
+int dg_apply_jacobian_planes(dg_ctx* c, const double* u0, const double* z, const double* zb, const double* za, double* r,
+                             int p0, int p1)
+{
+    if (!c) return fail(DG_ERR_INVALID, "dg_apply_jacobian: NULL ctx");
+    if (c->mesh.problem != DG_PROBLEM_NLREAC || !c->launch_jac)
+        return fail(DG_ERR_UNSUPPORTED, "dg_apply_jacobian: the context's problem (%d) is not DG_PROBLEM_NLREAC", c->mesh.problem);
+    if (!u0) return fail(DG_ERR_INVALID, "dg_apply_jacobian: NULL u0");
+    const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
+    const char *us = (const char*)u0, *rs = (const char*)r;
+    if (r && us < rs + bytes && rs < us + bytes) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 and r overlap");
+    if ((uintptr_t)u0 & 7) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 must be 8-byte aligned");
+    return apply_planes_impl(c, z, zb, za, r, p0, p1, u0);
+}
+
+int dg_apply_jacobian(dg_ctx* c, const double* u0, const double* z, double* r)
+{
+    if (!c) return fail(DG_ERR_INVALID, "dg_apply_jacobian: NULL ctx");
+    if (c->M.L != c->M.N0)
+        return fail(DG_ERR_INVALID, "dg_apply_jacobian: context owns %d of %d planes; use dg_apply_jacobian_planes", c->M.L,
+                    c->M.N0);
+    if (!z || !r) return fail(DG_ERR_INVALID, "dg_apply_jacobian: NULL vector");
+    return dg_apply_jacobian_planes(c, u0, z, z + (size_t)(c->M.L - 1) * c->plane_dofs, z, r, 0, c->M.L);
+}
+
+static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1,
+                             const double* u0)
 {
     if (!c || !x || !xb || !xa || !r) return fail(DG_ERR_INVALID, "dg_apply_planes: NULL argument");
     if (p0 < 0 || p1 > c->M.L || p0 > p1) return fail(DG_ERR_INVALID, "dg_apply_planes: planes [%d,%d) of %d", p0, p1, c->M.L);
@@ -961,7 +1008,7 @@ int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* 
     if (((uintptr_t)x & 15) && c->tile) return fail(DG_ERR_INVALID, "dg_apply: x must be 16-byte aligned");
     if ((((uintptr_t)x | (uintptr_t)xb | (uintptr_t)xa) & 15) && c->gen)
         return fail(DG_ERR_INVALID, "dg_apply: x and the halo planes must be 16-byte aligned");
-    cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream);
+    cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream, u0);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
     return DG_OK;
 }

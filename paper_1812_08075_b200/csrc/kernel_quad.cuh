@@ -82,7 +82,7 @@ struct Sw2 {
     }
 };
 
-template <int N, int M>
+template <int N, int M, bool U0 = false>
 struct QLay {
     static constexpr int CPB = (N <= 5) ? 2 : 1;
     static constexpr int NT = 256;
@@ -95,7 +95,8 @@ struct QLay {
     //           F2 [8][M2] (U-, U+, Gn-, Gn+, Gt1-, Gt1+, Gt2-, Gt2+) -> coefficients [4][M2] (Cv, Ct1, Ct2, Cn)
     static constexpr int FACE = 4 * N2 + 6 * NM + 8 * M2;
     static constexpr int GU = G2 + M3;      // u at the M^3 points (diffusion-reaction: reaction / source terms)
-    static constexpr int F = GU + M3;
+    static constexpr int U0Q = GU + M3;     // U0: the linearization point u0 at the M^3 points (Jacobian action)
+    static constexpr int F = U0Q + (U0 ? M3 : 0);
     static constexpr int GEO = F + 6 * FACE; // per cell: Gt[6], J rows 0-1 [6], o[2]; per face 16: dS, a-[3], a+[3], Jm rows 0-1 [6], om[2], pad
     static constexpr int CELL = GEO + 14 + 6 * 16;
     static constexpr int CELLP = (CELL + 1) / 2 * 2;
@@ -117,12 +118,19 @@ struct QLay {
 // volume (u at the quadrature points: the 4th quantity of the stacked stage 1, Eq. fusedtensor),
 // boundary faces with the Dirichlet data g = |x|^2 (one-sided flux, [u] -> u - g), penalty
 // alpha k (k+2) |F| / |T| (alpha = penalty_scale, set in M.gamma by dg_setup).
-template <int N, int M, bool AFFINE, bool COEFF, bool DR = false>
-__global__ void __launch_bounds__(256, qd::QLay<N, M>::MINB) // as many CTAs / SM as shared memory allows
+// PR: 0 the periodic operator; 1 the paper's (linear) diffusion-reaction residual; 2 its nonlinear variant
+// (reading R26: reaction c u^2, f = c|x|^4 - 10|x|^2 - 6); 3 the action of that variant's
+// Jacobian J(u0) x: u0, the linearization point, is evaluated at the M^3 points by
+// the same A A A sweeps (a second input of the fused stage 1), the reaction becomes 2 c u0 x, the f and g
+// terms drop out (they do not depend on the solution).
+template <int N, int M, bool AFFINE, bool COEFF, int PR = 0>
+__global__ void __launch_bounds__(256, qd::QLay<N, M, PR == 3>::MINB) // as many CTAs / SM as shared memory allows
 k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
-       long long c_begin, long long c_end, const __grid_constant__ QTab<N, M> T, const MeshArgs M_)
+       long long c_begin, long long c_end, const __grid_constant__ QTab<N, M> T, const MeshArgs M_,
+       const double* __restrict__ u0)
 {
-    using L = qd::QLay<N, M>;
+    constexpr bool DR = PR != 0;
+    using L = qd::QLay<N, M, PR == 3>;
     constexpr int CPB = L::CPB, NT = L::NT, N2 = L::N2, N3 = L::N3, M2 = L::M2, M3 = L::M3, NM = L::NM;
     const MeshArgs& Ms = M_;
     extern __shared__ __align__(16) double sm[];
@@ -145,6 +153,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     for (int i = tid; i < N; i += NT) { se0[i] = T.e0[i]; se1[i] = T.e1[i]; sd0[i] = T.d0[i]; sd1[i] = T.d1[i]; }
     for (int c = 0; c < ncell; ++c)
         for (int i = tid; i < N3; i += NT) cellp(c)[L::X + i] = __ldg(x + (cfirst + c) * N3 + i);
+    if (PR == 3) // the linearization point, into R (unused until stage 3)
+        for (int c = 0; c < ncell; ++c)
+            for (int i = tid; i < N3; i += NT) cellp(c)[L::R + i] = __ldg(u0 + (cfirst + c) * N3 + i);
 
     // cell coordinates, computed once per cell (32-bit: a slab has < 2^31 cells)
     __shared__ int s_co[CPB][5]; // lp, rem, i0, i1, i2
@@ -251,6 +262,19 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         fg[15] = (DR && (side ? ig[d] == Nd - 1 : ig[d] == 0)) ? 1.0 : 0.0;
     }
     __syncthreads();
+
+    // ---------------- P0b (Jacobian): u0 at the M^3 points, U0Q = A0 A1 A2 u0 ----------------
+    if (PR == 3) {
+        using S2 = qd::Sw3<N, N, N, 2, M, false, false>;
+        for (int t = tid; t < ncell * S2::NL; t += NT) { double* b = cellp(t / S2::NL); S2::line(b + L::R, b + L::Y2, T.A, t % S2::NL); }
+        __syncthreads();
+        using S1 = qd::Sw3<N, N, M, 1, M, false, false>;
+        for (int t = tid; t < ncell * S1::NL; t += NT) { double* b = cellp(t / S1::NL); S1::line(b + L::Y2, b + L::Z, T.A, t % S1::NL); }
+        __syncthreads();
+        using S0 = qd::Sw3<N, M, M, 0, M, false, false>;
+        for (int t = tid; t < ncell * S0::NL; t += NT) { double* b = cellp(t / S0::NL); S0::line(b + L::Z, b + L::U0Q, T.A, t % S0::NL); }
+        __syncthreads();
+    }
 
     // ---------------- P1: stage 1a (along j2); face traces along the normal (own from smem, neighbour from L2) ----
     {
@@ -361,7 +385,17 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             b[L::G0 + P] = W * fma(x0, xg, p0) / h0;
             b[L::G1 + P] = W * fma(x1, xg, p1) / h1;
             b[L::G2 + P] = W * fma(x2, xg, p2) / h2;
-            b[L::GU + P] = W * (10.0 * b[L::GU + P] + 6.0);
+            const double uq = b[L::GU + P];
+            double react;
+            if (PR == 1) {
+                react = 10.0 * uq + 6.0;                              // c u - f
+            } else if (PR == 2) {
+                const double s2 = x0 * x0 + x1 * x1 + x2 * x2;
+                react = 10.0 * uq * uq - (10.0 * s2 * s2 - 10.0 * s2 - 6.0); // c u^2 - f (R26)
+            } else {
+                react = 20.0 * b[L::U0Q + P] * uq;                    // 2 c u0 x
+            }
+            b[L::GU + P] = W * react;
             continue;
         }
         b[L::G0 + P] = cW * fma(g[0], a0, fma(g[3], a1, g[4] * a2));
@@ -404,7 +438,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             if (fg[15] != 0.0) {
                 // boundary face: outer normal sn e_d, [u] = u - g (theta and penalty terms), one-sided flux
                 const double sn = side ? 1.0 : -1.0;
-                const double jmp = Uo - (X0 * X0 + X1 * X1 + X2 * X2);
+                const double jmp = PR == 3 ? Uo : Uo - (X0 * X0 + X1 * X1 + X2 * X2); // Jacobian: g = 0
                 Cv = W * (-sn * Kgo + gam * jmp);
                 s = -W * jmp * sn;
             } else {

@@ -23,6 +23,9 @@ DG_GEOM_AXIS = 0
 DG_GEOM_AFFINE = 1
 DG_COEFF_ONE = 0
 DG_COEFF_SINCOS = 1
+DG_PROBLEM_PERIODIC = 0
+DG_PROBLEM_DIFFREAC = 1
+DG_PROBLEM_NLREAC = 2
 
 _ERRNAMES = {-1: "DG_ERR_INVALID", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_CUDA", -5: "DG_ERR_OOM"}
 
@@ -50,7 +53,8 @@ class dg_mesh(ctypes.Structure):
 
 EXPORTS = ["dg_setup", "dg_apply", "dg_apply_planes", "dg_apply_host", "dg_destroy", "dg_set_stream",
            "dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs", "dg_alg_flops", "dg_alg_bytes",
-           "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops"]
+           "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops",
+           "dg_apply_jacobian", "dg_apply_jacobian_planes"]
 
 _lib = None
 
@@ -69,6 +73,8 @@ def load(path: str = LIB_PATH):
     L.dg_apply.argtypes = [vp, vp, vp]
     L.dg_apply_planes.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
     L.dg_apply_host.argtypes = [vp, vp, vp]
+    L.dg_apply_jacobian.argtypes = [vp, vp, vp, vp]
+    L.dg_apply_jacobian_planes.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
     L.dg_destroy.argtypes = [vp]
     L.dg_set_stream.argtypes = [vp, vp]
     for f in ("dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs"):
@@ -129,6 +135,15 @@ def dg_apply(ctx: int, x, r):
 
 def dg_apply_planes(ctx: int, x, x_below, x_above, r, p_begin: int, p_end: int):
     _check(load().dg_apply_planes(ctx, _ptr(x), _ptr(x_below), _ptr(x_above), _ptr(r), p_begin, p_end))
+
+
+def dg_apply_jacobian(ctx: int, u0, z, r):
+    _check(load().dg_apply_jacobian(ctx, _ptr(u0), _ptr(z), _ptr(r)))
+
+
+def dg_apply_jacobian_planes(ctx: int, u0, z, z_below, z_above, r, p_begin: int, p_end: int):
+    _check(load().dg_apply_jacobian_planes(ctx, _ptr(u0), _ptr(z), _ptr(z_below), _ptr(z_above), _ptr(r), p_begin,
+                                           p_end))
 
 
 def dg_apply_host(ctx: int, x_host, r_host):
@@ -234,6 +249,26 @@ class Operator:
             r = torch.empty_like(x)
         self._chk(r)
         dg_apply(self.ctx, x, r)
+        return r
+
+    def apply_jacobian(self, u0, z, r=None):
+        """r = J(u0) z (DG_PROBLEM_NLREAC contexts; include/dg.h dg_apply_jacobian)."""
+        import torch
+        self._chk(u0)
+        self._chk(z)
+        if r is None:
+            r = torch.empty_like(z)
+        self._chk(r)
+        dg_apply_jacobian(self.ctx, u0, z, r)
+        return r
+
+    def apply_jacobian_planes(self, u0, z, z_below, z_above, r, p_begin: int, p_end: int):
+        self._chk(u0)
+        self._chk(z)
+        self._chk(r)
+        self._chk(z_below, self.plane_ndofs)
+        self._chk(z_above, self.plane_ndofs)
+        dg_apply_jacobian_planes(self.ctx, u0, z, z_below, z_above, r, p_begin, p_end)
         return r
 
     def apply_planes(self, x, x_below, x_above, r, p_begin: int, p_end: int):

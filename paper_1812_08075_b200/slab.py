@@ -110,21 +110,24 @@ class SlabApply:
         # exchange); otherwise interior + 2 boundary planes
         self.launches_per_apply = 1 if (p.world == 1 or p.nplanes <= 2) else 3
 
-    def __call__(self, x, r):
+    def __call__(self, x, r, fn=None):
+        """r = the rows of this slab; fn overrides the planes function for this call (same signature;
+        e.g. the Jacobian action with its linearization point bound)."""
         import torch
         p = self.p
+        fn = self.fn if fn is None else fn
         if p.world == 1:
             # whole mesh on one rank: halos are the wrap planes of x itself, one launch
             L = p.nplanes
-            self.fn(x, x[(L - 1) * self.plane_ndofs:], x[:self.plane_ndofs], r, 0, L)
+            fn(x, x[(L - 1) * self.plane_ndofs:], x[:self.plane_ndofs], r, 0, L)
             return r
         if not self.cuda:
             exchange_halos(x, self.halo_below, self.halo_above, self.plane_ndofs, p, self.group)
             a, b = p.interior
             if b > a:
-                self.fn(x, self.halo_below, self.halo_above, r, a, b)
+                fn(x, self.halo_below, self.halo_above, r, a, b)
             for a, b in p.boundary:
-                self.fn(x, self.halo_below, self.halo_above, r, a, b)
+                fn(x, self.halo_below, self.halo_above, r, a, b)
             return r
         cur = torch.cuda.current_stream(self.device)
         self.ev_x.record(cur)
@@ -134,13 +137,13 @@ class SlabApply:
             self.ev_halo.record(self.comm_stream)
         a, b = p.interior
         if b > a:
-            self.fn(x, self.halo_below, self.halo_above, r, a, b)
+            fn(x, self.halo_below, self.halo_above, r, a, b)
         cur.wait_event(self.ev_halo)
         if p.nplanes <= 2:
-            self.fn(x, self.halo_below, self.halo_above, r, 0, p.nplanes)
+            fn(x, self.halo_below, self.halo_above, r, 0, p.nplanes)
         else:
             for a, b in p.boundary:
-                self.fn(x, self.halo_below, self.halo_above, r, a, b)
+                fn(x, self.halo_below, self.halo_above, r, a, b)
         # keep the halo buffers alive until the compute stream is done with them
         self.halo_below.record_stream(cur)
         self.halo_above.record_stream(cur)
@@ -177,6 +180,14 @@ class SlabOperator:
         if r is None:
             r = torch.empty_like(x)
         return self._apply(x, r)
+
+    def apply_jacobian(self, u0, z, r=None):
+        """r = J(u0) z on this rank's slab (DG_PROBLEM_NLREAC): the halo exchange of z as for apply; u0 is
+        needed on the owned planes only."""
+        import torch
+        if r is None:
+            r = torch.empty_like(z)
+        return self._apply(z, r, fn=lambda zz, zb, za, rr, a, b: self.op.apply_jacobian_planes(u0, zz, zb, za, rr, a, b))
 
     def close(self):
         self.op.close()

@@ -9,7 +9,8 @@ RND = sys.argv[1] if len(sys.argv) > 1 else "r01"
 R = os.path.join(ROOT, "profiles", RND)
 T = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
 files = [f"bench_cfg{c}_n1.json" for c in range(5)] + ["bench_cfg2_quad7.json", "bench_diffreac_k3_64.json",
-                                                        "bench_diffreac_k5_48.json"]
+                                                        "bench_diffreac_k5_48.json", "bench_nlreac_k3_64.json",
+                                                        "bench_nljac_k3_64.json"]
 L = ["# Round 1 evidence (B200, 1 GPU)\n",
      "Produced by `tools/round_evidence.sh` on one gpurun box, copied by `tools/collect_evidence.py`, this file by",
      "`tools/evidence_readme.py`. Bench lines: `python bench.py --config C` (timed region = K applies, CUDA events on",
@@ -19,7 +20,8 @@ L = ["# Round 1 evidence (B200, 1 GPU)\n",
      "(`--set full`, caches flushed before the launch); for the affine configs it includes the per-cell setup tables",
      "(geometry records 288 B, c(x) factor tables 96(n+1) B, face c values 8(3n^2 rounded to even) B per cell) that",
      "`B_alg` (x, r and J only) does not count. Rows below the line: SURVEY §8(f2) general quadrature and §8(f1) the",
-     "paper's diffusion-reaction problem (correctness-first kernel; F_alg = its contractions as executed).\n",
+     "paper's diffusion-reaction problem, §8(f3) its nonlinear variant (residual and Jacobian action, reading R26)",
+     "(correctness-first kernel; F_alg = its contractions as executed).\n",
      "| line | workload | ms / apply | GDOF/s | kernel | bound | frac of roofline | frac HBM (alg bytes) | frac of measured DFMA peak | DRAM traffic / alg bytes |",
      "|---|---|---|---|---|---|---|---|---|---|"]
 for f in files:
