@@ -47,6 +47,8 @@ def lib():
                                             ctypes.c_double, dp, dp, i64p, ctypes.c_int64]
         L.oracle_apply_nlreac.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_double, ctypes.c_int, dp, dp, dp, i64p, ctypes.c_int64]
+        L.oracle_apply_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                          dp, dp, i64p, ctypes.c_int64]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -145,6 +147,24 @@ def apply_nlreac(w, x: np.ndarray, u0: np.ndarray | None = None, cells=None) -> 
                                    None if u0 is None else _dp(u0), _dp(x), _dp(r), cp, nc)
     if rc != 0:
         raise ValueError("oracle_apply_nlreac: invalid arguments")
+    return r
+
+
+def apply_stokes(w, x: np.ndarray, cells=None) -> np.ndarray:
+    """The paper's Stokes residual (Eq. stokes_weak; readings R27/R28) on the
+    axiparallel unit-cube mesh of workload `w` (w.problem == 3): per cell [u_0 | u_1 | u_2 | p] blocks of
+    3 n^3 + k^3 DOFs; alpha = w.penalty_scale."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    assert x.size == w.ndofs
+    r = np.full(w.ndofs, np.nan)
+    if cells is None:
+        cp, nc = None, 0
+    else:
+        cells = np.ascontiguousarray(cells, dtype=np.int64)
+        cp, nc = _i64p(cells), len(cells)
+    rc = lib().oracle_apply_stokes(w.N[0], w.N[1], w.N[2], w.k, float(w.penalty_scale), _dp(x), _dp(r), cp, nc)
+    if rc != 0:
+        raise ValueError("oracle_apply_stokes: invalid arguments")
     return r
 
 

@@ -634,3 +634,208 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* ====================================================================================== */
+/* Stokes (Eq. stokes_strong / stokes_weak).                 */
+/*   -mu Lap u + grad p = f, div u = 0 on (0,1)^3, u = g on Gamma_D, mu grad u n - p n = 0  */
+/*   on Gamma_N; mu = 1, f = 0 (g is the solution: reading R27),                          */
+/*   Gamma_D = the boundary without the face x_0 = 1 (the paper's "x_1 < 1" with 1-based   */
+/*   coordinates, R27), g = (4 x_1 (1 - x_1), 0, 0), exact pressure 8 (1 - x_0).           */
+/* Residual r(u_h, p_h; v_h, q_h) of Eq. stokes_weak, theta = -1, gamma_F as for the       */
+/* diffusion-reaction problem (alpha k (k+2) |F| / |T|, alpha = the argument):    */
+/*   volume      (grad u, grad v) - (p, div v) - (div u, q)                                 */
+/*   F in F_i+D  -({grad u} n, [v]) + theta([u], {grad v} n) + gamma([u], [v])              */
+/*               + ({p}, [v] . n) + ([u] . n, {q})                                          */
+/*   F in F_D    -theta(g, grad v n) - gamma(g, v) - (g . n, q)                              */
+/* Boundary faces: [w] = {w} = w|T, n the outer normal (R21). Velocity Q_k (n = k+1 GL      */
+/* nodes per direction), pressure Q_{k-1} (k GL nodes, R27), quadrature with m = k+1 Gauss  */
+/* points (R28). DOFs per cell: [u_0 (n^3) | u_1 (n^3) | u_2 (n^3) | p (k^3)], each block in */
+/* j0-fastest order, cells canonical (R27). Axiparallel mesh h_d = 1/N_d, non-periodic.     */
+/* Plain definition: every basis function evaluated directly (lagrange_1d products) at      */
+/* every quadrature point.                                                                   */
+/* ====================================================================================== */
+typedef struct {
+    int k, n, np, m, B;
+    double vx[OMAX], px[OMAX], qx[OMAX], qw[OMAX];
+} stab;
+
+/* value of the velocity basis function J and its reference gradient at reference point s */
+static void st_vbasis(const stab* S, int J, const double s[3], double* v, double g[3])
+{
+    const int n = S->n;
+    const int j[3] = {J % n, (J / n) % n, J / (n * n)};
+    double a[3], d[3];
+    for (int e = 0; e < 3; ++e) lagrange_1d(n, S->vx, j[e], s[e], &a[e], &d[e]);
+    *v = a[0] * a[1] * a[2];
+    g[0] = d[0] * a[1] * a[2];
+    g[1] = a[0] * d[1] * a[2];
+    g[2] = a[0] * a[1] * d[2];
+}
+static double st_pbasis(const stab* S, int J, const double s[3])
+{
+    const int np = S->np;
+    const int j[3] = {J % np, (J / np) % np, J / (np * np)};
+    double v = 1.0;
+    for (int e = 0; e < 3; ++e) {
+        double a, d;
+        lagrange_1d(np, S->px, j[e], s[e], &a, &d);
+        v *= a;
+    }
+    return v;
+}
+/* u (3 components), reference gradients gu[c][e], p of the block X at reference point s */
+static void st_eval(const stab* S, const double* X, const double s[3], double u[3], double gu[3][3], double* p)
+{
+    const int n3 = S->n * S->n * S->n, p3 = S->np * S->np * S->np;
+    for (int c = 0; c < 3; ++c) {
+        u[c] = 0.0;
+        gu[c][0] = gu[c][1] = gu[c][2] = 0.0;
+    }
+    for (int J = 0; J < n3; ++J) {
+        double v, g[3];
+        st_vbasis(S, J, s, &v, g);
+        for (int c = 0; c < 3; ++c) {
+            const double xc = X[c * n3 + J];
+            u[c] += xc * v;
+            for (int e = 0; e < 3; ++e) gu[c][e] += xc * g[e];
+        }
+    }
+    *p = 0.0;
+    for (int J = 0; J < p3; ++J) *p += X[3 * n3 + J] * st_pbasis(S, J, s);
+}
+
+static void cell_residual_stokes(const stab* S, const int N[3], const int ic[3], const double* const xs[7], double alpha,
+                                 double* r)
+{
+    const int n3 = S->n * S->n * S->n, p3 = S->np * S->np * S->np, m = S->m;
+    const double h[3] = {1.0 / N[0], 1.0 / N[1], 1.0 / N[2]};
+    const double vol = h[0] * h[1] * h[2];
+    const double theta = -1.0;
+    for (int I = 0; I < S->B; ++I) r[I] = 0.0;
+    /* volume */
+    for (int q2 = 0; q2 < m; ++q2)
+        for (int q1 = 0; q1 < m; ++q1)
+            for (int q0 = 0; q0 < m; ++q0) {
+                const double s[3] = {S->qx[q0], S->qx[q1], S->qx[q2]};
+                const double W = S->qw[q0] * S->qw[q1] * S->qw[q2] * vol;
+                double u[3], gu[3][3], p;
+                st_eval(S, xs[0], s, u, gu, &p);
+                double G[3][3], div = 0.0; /* physical gradients G[c][e] = d u_c / d x_e */
+                for (int c = 0; c < 3; ++c)
+                    for (int e = 0; e < 3; ++e) G[c][e] = gu[c][e] / h[e];
+                for (int c = 0; c < 3; ++c) div += G[c][c];
+                for (int J = 0; J < n3; ++J) {
+                    double v, g[3];
+                    st_vbasis(S, J, s, &v, g);
+                    for (int c = 0; c < 3; ++c) {
+                        double a = 0.0;
+                        for (int e = 0; e < 3; ++e) a += G[c][e] * g[e] / h[e];  /* (grad u_c, grad v) */
+                        a -= p * g[c] / h[c];                                       /* -(p, div v) */
+                        r[c * n3 + J] += W * a;
+                    }
+                }
+                for (int J = 0; J < p3; ++J) r[3 * n3 + J] += W * (-div * st_pbasis(S, J, s)); /* -(div u, q) */
+            }
+    /* faces */
+    const double kk = (double)S->k * (S->k + 2);
+    for (int d = 0; d < 3; ++d) {
+        int t1, t2;
+        tangential(d, &t1, &t2);
+        const double area = h[t1] * h[t2];
+        const double gamma = alpha * kk * area / vol;
+        for (int side = 0; side < 2; ++side) {
+            const int boundary = side ? (ic[d] == N[d] - 1) : (ic[d] == 0);
+            if (boundary && d == 0 && side == 1) continue; /* Gamma_N: x_0 = 1, no face terms */
+            for (int b = 0; b < m; ++b)
+                for (int a = 0; a < m; ++a) {
+                    double s[3];
+                    s[d] = (double)side; s[t1] = S->qx[a]; s[t2] = S->qx[b];
+                    double xF[3];
+                    for (int e = 0; e < 3; ++e) xF[e] = (ic[e] + s[e]) * h[e];
+                    const double W = S->qw[a] * S->qw[b] * area;
+                    double us[3], gus[3][3], ps;
+                    st_eval(S, xs[0], s, us, gus, &ps);
+                    if (boundary) {
+                        const double sn = side ? 1.0 : -1.0;
+                        const double g[3] = {4.0 * xF[1] * (1.0 - xF[1]), 0.0, 0.0};
+                        double jmp[3];
+                        for (int c = 0; c < 3; ++c) jmp[c] = us[c] - g[c];
+                        for (int J = 0; J < n3; ++J) {
+                            double v, gv[3];
+                            st_vbasis(S, J, s, &v, gv);
+                            const double dvn = sn * gv[d] / h[d]; /* grad v . n */
+                            for (int c = 0; c < 3; ++c) {
+                                const double dun = sn * gus[c][d] / h[d];
+                                double t = -dun * v + theta * jmp[c] * dvn + gamma * jmp[c] * v;
+                                if (c == d) t += ps * v * sn; /* ({p}, [v] . n) */
+                                r[c * n3 + J] += W * t;
+                            }
+                        }
+                        for (int J = 0; J < p3; ++J) r[3 * n3 + J] += W * sn * jmp[d] * st_pbasis(S, J, s);
+                    } else {
+                        const int self_is_minus = (side == 1);
+                        const double* xo = xs[self_is_minus ? 2 + 2 * d : 1 + 2 * d];
+                        double so[3];
+                        so[d] = self_is_minus ? 0.0 : 1.0; so[t1] = s[t1]; so[t2] = s[t2];
+                        double uo[3], guo[3][3], po;
+                        st_eval(S, xo, so, uo, guo, &po);
+                        const double sv = self_is_minus ? 1.0 : -1.0; /* [v] = sv v */
+                        double jump[3], avg[3];
+                        for (int c = 0; c < 3; ++c) {
+                            const double um = self_is_minus ? us[c] : uo[c], up = self_is_minus ? uo[c] : us[c];
+                            jump[c] = um - up;
+                            avg[c] = 0.5 * (gus[c][d] + guo[c][d]) / h[d]; /* {grad u_c} . n_F, n_F = +e_d */
+                        }
+                        const double pavg = 0.5 * (ps + po);
+                        for (int J = 0; J < n3; ++J) {
+                            double v, gv[3];
+                            st_vbasis(S, J, s, &v, gv);
+                            const double dvn = 0.5 * gv[d] / h[d]; /* {grad v} . n_F (v lives on this side) */
+                            for (int c = 0; c < 3; ++c) {
+                                double t = -avg[c] * sv * v + theta * jump[c] * dvn + gamma * jump[c] * sv * v;
+                                if (c == d) t += pavg * sv * v;
+                                r[c * n3 + J] += W * t;
+                            }
+                        }
+                        for (int J = 0; J < p3; ++J) r[3 * n3 + J] += W * jump[d] * 0.5 * st_pbasis(S, J, s);
+                    }
+                }
+        }
+    }
+}
+
+/*
+ * Stokes residual on the whole mesh (or the rows of `cells`): x, r global vectors of N0 N1 N2 (3 n^3 + k^3)
+ * doubles in the block layout above. k >= 1 (k = 1: piecewise-constant pressure). Returns 0 or -1.
+ */
+int oracle_apply_stokes(int N0, int N1, int N2, int k, double alpha, const double* x, double* r, const int64_t* cells,
+                        int64_t ncells)
+{
+    stab S;
+    if (N0 < 1 || N1 < 1 || N2 < 1 || k < 1 || k + 1 > OMAX) return -1;
+    S.k = k; S.n = k + 1; S.np = k; S.m = k + 1;
+    S.B = 3 * S.n * S.n * S.n + S.np * S.np * S.np;
+    double w[OMAX];
+    if (oracle_gauss_legendre(S.n, S.vx, w) || oracle_gauss_legendre(S.np, S.px, w) ||
+        oracle_gauss_legendre(S.m, S.qx, S.qw))
+        return -1;
+    const int N[3] = {N0, N1, N2};
+    const int64_t total = (int64_t)N0 * N1 * N2;
+    const int64_t cnt = cells ? ncells : total;
+#pragma omp parallel for schedule(dynamic, 2)
+    for (int64_t s = 0; s < cnt; ++s) {
+        const int64_t c = cells ? cells[s] : s;
+        const int ic[3] = {(int)(c / ((int64_t)N1 * N2)), (int)((c / N2) % N1), (int)(c % N2)};
+        const double* xs[7];
+        xs[0] = x + c * S.B;
+        for (int d = 0; d < 3; ++d)
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                int jc[3] = {ic[0], ic[1], ic[2]};
+                jc[d] = ic[d] + (sgn ? 1 : -1);
+                xs[1 + 2 * d + sgn] = (jc[d] < 0 || jc[d] >= N[d]) ? NULL
+                                                                   : x + (((int64_t)jc[0] * N1 + jc[1]) * N2 + jc[2]) * S.B;
+            }
+        cell_residual_stokes(&S, N, ic, xs, alpha, r + c * S.B);
+    }
+    return 0;
+}

@@ -91,7 +91,8 @@ class Workload:
     penalty_scale: float = 10.0  # gamma = penalty_scale * k (k+1) / h  (BASELINE.json configs)
     quad: int = -1              # Gauss points per direction; -1 -> k + 1
     gpus: tuple = (1,)
-    problem: int = 0            # 0: periodic SIPG of the configs; 1: the paper's diffusion-reaction problem; 2: its nonlinear variant
+    problem: int = 0            # 0: periodic SIPG of the configs; 1: the paper's diffusion-reaction problem; 2: its nonlinear
+                                #    variant (R26); 3: the paper's Stokes problem (R27, block 3 n^3 + k^3 per cell)
                                 #    (non-periodic cube, Dirichlet g = |x|^2, K = xx^T + I, c = 10,
                                 #    f = -6; penalty_scale = alpha = 3, gamma = alpha k(k+2) |F|/|T|)
     text: str = ""
@@ -109,8 +110,13 @@ class Workload:
         return self.N[0] * self.N[1] * self.N[2]
 
     @property
+    def block(self) -> int:
+        """DOFs per cell: n^3, or 3 n^3 + k^3 for Stokes (problem 3: [u_0 | u_1 | u_2 | p], R27)."""
+        return 3 * self.n ** 3 + self.k ** 3 if self.problem == 3 else self.n ** 3
+
+    @property
     def ndofs(self) -> int:
-        return self.ncells * self.n ** 3
+        return self.ncells * self.block
 
     @property
     def plane_cells(self) -> int:
@@ -146,6 +152,15 @@ def nlreac(k: int, N, seed: int = 13, alpha: float = 3.0) -> Workload:
         N = (N, N, N)
     return Workload(f"nlreac_k{k}_N{N[0]}x{N[1]}x{N[2]}_m{k + 2}", k, tuple(N), 0, 0,
                     seed=seed, penalty_scale=alpha, quad=k + 2, problem=2)
+
+
+def stokes(k: int, N, seed: int = 17, alpha: float = 3.0) -> Workload:
+    """The paper's Stokes problem (readings R27/R28) on an axiparallel
+    N0 x N1 x N2 mesh of (0,1)^3: velocity Q_k, pressure Q_{k-1}, k+1 Gauss points per direction."""
+    if isinstance(N, int):
+        N = (N, N, N)
+    return Workload(f"stokes_k{k}_N{N[0]}x{N[1]}x{N[2]}", k, tuple(N), 0, 0, seed=seed, penalty_scale=alpha,
+                    problem=3)
 
 
 def small(k: int, N, geom_kind: int = 0, coeff_kind: int = 0, seed: int = 7, quad: int = -1) -> Workload:

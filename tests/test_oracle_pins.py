@@ -462,3 +462,69 @@ def test_nlreac_jacobian_symmetric():
         e[j] = 1.0
         J[:, j] = oracle.apply_nlreac(w, e, u0=u0)
     assert np.abs(J - J.T).max() <= 1e-12 * np.abs(J).max()
+
+
+# ---------------------------------------------------------------- Stokes
+def _stokes_exact(w):
+    """Interpolant of the paper's solution: u = g = (4 x_1 (1 - x_1), 0, 0), p = 8 (1 - x_0)
+    (0-based coordinates, R27), in the block layout [u_0 | u_1 | u_2 | p]."""
+    n, k = w.n, w.k
+    N0, N1, N2 = w.N
+    c = np.arange(w.ncells)
+    i2, i1, i0 = c % N2, (c // N2) % N1, c // (N1 * N2)
+
+    def pts(m_):
+        xi = 0.5 * (np.polynomial.legendre.leggauss(m_)[0] + 1.0) if m_ > 1 else np.array([0.5])
+        j = np.arange(m_ ** 3)
+        j0, j1, j2 = j % m_, (j // m_) % m_, j // (m_ * m_)
+        return ((i0[:, None] + xi[j0][None, :]) / N0, (i1[:, None] + xi[j1][None, :]) / N1,
+                (i2[:, None] + xi[j2][None, :]) / N2)
+    X0, X1, X2 = pts(n)
+    P0, _, _ = pts(k)
+    u0 = 4.0 * X1 * (1.0 - X1)
+    z = np.zeros_like(u0)
+    p = 8.0 * (1.0 - P0)
+    return np.concatenate([u0, z, z, p], axis=1).reshape(-1)
+
+
+@pytest.mark.parametrize("k,N", [(2, (2, 3, 2)), (3, (2, 2, 2)), (4, (2, 1, 2))])
+def test_stokes_manufactured_solution(k, N):
+    """with mu = 1, f = 0, g = (4 x_1 (1 - x_1), 0, 0) the exact solution is u = g,
+    p = 8 (1 - x_0), in (Q_k)^3 x Q_{k-1} for k >= 2; the DG form is consistent and the k+1 point rule
+    integrates every term exactly, so the residual of the interpolant vanishes (every row: momentum and
+    continuity, Dirichlet and Neumann boundary cells)."""
+    w = synth.stokes(k, N)
+    x = _stokes_exact(w)
+    r = oracle.apply_stokes(w, x)
+    r0 = oracle.apply_stokes(w, np.zeros_like(x))
+    assert np.abs(r).max() <= 1e-11 * np.abs(r0).max()
+    # not vacuous: a wrong pressure level violates the Neumann condition p = 0 at x_0 = 1
+    y = x.copy().reshape(w.ncells, -1)
+    y[:, 3 * w.n ** 3:] += 0.1
+    assert np.abs(oracle.apply_stokes(w, y.reshape(-1))).max() > 1e-4 * np.abs(r0).max()
+
+
+@pytest.mark.parametrize("k,N", [(1, (2, 2, 3)), (2, (2, 2, 2)), (3, (2, 1, 2))])
+def test_stokes_bilinear_part_equals_kronecker_assembly(k, N):
+    """R(x) - R(0) == the independent Kronecker assembly of Eq. stokes_weak (oracle/brute.py: 1D SIPG, 1D
+    pressure-velocity coupling and mixed masses by exact polynomial integration, Dirichlet / Neumann ends of
+    the cube), dense on tiny meshes; also symmetric (b(p, v) and b(q, u) are the same form)."""
+    w = synth.stokes(k, N)
+    K = brute.stokes_dense(w)
+    assert np.abs(K - K.T).max() <= 1e-12 * np.abs(K).max()
+    rng = np.random.default_rng(21)
+    r0 = oracle.apply_stokes(w, np.zeros(w.ndofs))
+    for _ in range(3):
+        x = rng.standard_normal(w.ndofs)
+        got = oracle.apply_stokes(w, x) - r0
+        ref = K @ x
+        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+def test_stokes_penalty_linear():
+    """The alpha-dependence of R is gamma([u] - g, [v]): linear in alpha."""
+    k, N = 2, (2, 2, 2)
+    ws = [synth.stokes(k, N, alpha=a) for a in (0.0, 3.0, 6.0)]
+    x = np.random.default_rng(4).standard_normal(ws[0].ndofs)
+    r = [oracle.apply_stokes(w, x) for w in ws]
+    assert np.abs((r[2] - r[0]) - 2 * (r[1] - r[0])).max() <= 1e-12 * np.abs(r[2]).max()
