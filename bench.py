@@ -109,14 +109,16 @@ def oracle_sample_rate(w, budget_s: float, seed: int = 2024, jacobian: bool = Fa
     import oracle
     import synth
     rng = np.random.default_rng(seed)
-    n3 = w.n ** 3
+    n3 = w.block
 
     def run(ncell):
         cells = np.sort(rng.choice(w.ncells, ncell, replace=False)).astype(np.int64)
-        if w.problem in (1, 2):  # the paper's problem: the oracle on the whole (small) host vector, sampled rows
+        if w.problem in (1, 2, 3):  # the paper's problems: the oracle on the whole host vector, sampled rows
             x = synth.x_np(w)
             t0 = time.perf_counter()
-            if w.problem == 1:
+            if w.problem == 3:
+                oracle.apply_stokes(w, x, cells)
+            elif w.problem == 1:
                 oracle.apply_diffreac(w, x, cells)
             elif jacobian:
                 oracle.apply_nlreac(w, x, u0=np.sin(x), cells=cells)
@@ -163,7 +165,7 @@ def run_reference(args, w, rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(w, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
-                         "sample": f"{cells} random cells ({cells * w.n ** 3} DOFs) of {w.name} per step, "
+                         "sample": f"{cells} random cells ({cells * w.block} DOFs) of {w.name} per step, "
                                    f"~{secs:.1f} s each; ms_per_step extrapolated to the whole mesh"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -177,7 +179,8 @@ def _config(w, ngpu):
             "coefficient": "1" if w.coeff_kind == 0 else "1+0.5sin(2pi x0)cos(2pi x1)",
             "penalty": (f"{w.penalty_scale:g}*k(k+1)/h" if w.problem == 0 else f"alpha={w.penalty_scale:g}: alpha*k(k+2)|F|/|T|"),
             "problem": ("periodic SIPG (configs)", "diffusion-reaction, Dirichlet g=|x|^2 (P:L945-1003)",
-                        "nonlinear diffusion-reaction c u^2 (R26), Dirichlet g=|x|^2")[w.problem],
+                        "nonlinear diffusion-reaction c u^2 (R26), Dirichlet g=|x|^2",
+                        "Stokes Q_k/Q_{k-1}, mu=1, Dirichlet g=(4x_1(1-x_1),0,0) / Neumann x_0=1 (P:L1077-1118)")[w.problem],
             "parallelism": f"x0-slab{ngpu}",
             "l2": f"inputs larger than L2 ({8 * w.ndofs / 1e9:.2f} GB per vector vs 126 MB L2)"
             if 8 * w.ndofs > 2 * 126e6 else "L2 flushed between steps"}
@@ -195,9 +198,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--problem", default="config", choices=["config", "diffreac", "nlreac"],
+    ap.add_argument("--problem", default="config", choices=["config", "diffreac", "nlreac", "stokes"],
                     help="diffreac: the paper's diffusion-reaction problem (SURVEY §8(f1)) with --k / --N, k+2 points; "
-                         "nlreac: its nonlinear variant (SURVEY §8(f3), R26)")
+                         "nlreac: its nonlinear variant (SURVEY §8(f3), R26); stokes: the paper's Stokes problem "
+                         "(SURVEY §8(f4), R27)")
     ap.add_argument("--jacobian", action="store_true",
                     help="nlreac: time the Jacobian action J(u0) z (dg_apply_jacobian) instead of the residual")
     ap.add_argument("--k", type=int, default=3)
@@ -214,6 +218,8 @@ def main():
         w = synth.diffreac(args.k, args.N, quad=args.k + 2)
     if args.problem == "nlreac":
         w = synth.nlreac(args.k, args.N)
+    if args.problem == "stokes":
+        w = synth.stokes(args.k, args.N)
     if args.jacobian and w.problem != 2:
         raise SystemExit("--jacobian needs --problem nlreac")
     if args.quad > 0 and args.quad != w.k + 1:
@@ -400,7 +406,7 @@ def main():
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         v, cells, secs, th = oracle_sample_rate(w, args.cpu_seconds, jacobian=args.jacobian)
         cpu = {"value": v, "unit": UNIT, "cores": th, "kind": "oracle",
-               "sample": f"{cells} random cells ({cells * w.n ** 3} DOFs) of {w.name}, {secs:.1f} s"}
+               "sample": f"{cells} random cells ({cells * w.block} DOFs) of {w.name}, {secs:.1f} s"}
 
     # ---- sanity of the timed result (not a parity claim: tests/ do that): finite, nonzero
     ok = bool(torch.isfinite(r).all().item()) and r.abs().max().item() > 0

@@ -55,6 +55,12 @@ extern "C" {
                                  r = R(x) = A x - b (Eq. diffreac_weak incl. the f and g terms); axiparallel
                                  (DG_GEOM_AXIS) only, coeff_kind ignored, quad = k+2 (k_quad);
                                  gamma_F = penalty_scale k (k+2) |F| / |T| (the paper: penalty_scale = alpha = 3) */
+#define DG_PROBLEM_STOKES 3   /* the paper's Stokes problem (Eq. stokes_weak; DESIGN.md
+                                 R27/R28): (0,1)^3, mu = 1, f = 0, Dirichlet g = (4 x_1 (1 - x_1), 0, 0) on the
+                                 boundary without the face x_0 = 1 (Neumann there); velocity Q_k, pressure
+                                 Q_{k-1}; per cell 3 n^3 + k^3 DOFs [u_0 | u_1 | u_2 | p] (every dg_local_ndofs /
+                                 dg_plane_ndofs count uses this block); r = R(x) incl. the g terms; DG_GEOM_AXIS,
+                                 DG_COEFF_ONE, quad = k+1 (k_stokes); gamma_F as DG_PROBLEM_DIFFREAC */
 #define DG_PROBLEM_NLREAC 2   /* its nonlinear variant (reading R26): reaction 10 u^2 in
                                  place of 10 u, f = 10|x|^4 - 10|x|^2 - 6 (u = |x|^2 stays the exact solution),
                                  K, g, penalty, restrictions as DG_PROBLEM_DIFFREAC; dg_apply returns the
@@ -76,7 +82,7 @@ typedef struct dg_mesh {
     double penalty_scale;  /* gamma_F = penalty_scale * k (k+1) * N[d] on faces with normal d (> 0) */
     int32_t device;        /* CUDA device ordinal */
     void* stream;          /* cudaStream_t on which dg_apply* enqueue work (NULL: legacy default stream) */
-    int32_t problem;       /* DG_PROBLEM_PERIODIC (default, 0), DG_PROBLEM_DIFFREAC or DG_PROBLEM_NLREAC */
+    int32_t problem;       /* DG_PROBLEM_PERIODIC (default, 0), _DIFFREAC, _NLREAC or _STOKES */
 } dg_mesh;
 
 /* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,

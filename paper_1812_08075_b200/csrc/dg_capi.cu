@@ -6,6 +6,7 @@
 #include "kernel_gen.cuh"
 #include "kernel_quad.cuh"
 #include "kernel_quadw.cuh"
+#include "kernel_stokes.cuh"
 #include "kernel_tile.cuh"
 #include "tables.h"
 
@@ -400,6 +401,64 @@ LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, int pr = 0, boo
     default: return pick_quad_n<8>(aff, coef, err, pr, cta);
     }
 }
+// ---- the paper's Stokes problem: k_stokes, one cell per CTA
+template <int N>
+cudaError_t launch_stokes(const void* st_, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
+                          double* r, long long c0, long long c1, cudaStream_t st, const double*)
+{
+    if (c1 <= c0) return cudaSuccess;
+    using L = dg::sk::SLay<N>;
+    dg::k_stokes<N><<<(unsigned)(c1 - c0), L::NT, L::BYTES, st>>>(x, xb, xa, r, c0, c1,
+                                                                   *static_cast<const dg::STab<N>*>(st_), M);
+    return cudaGetLastError();
+}
+template <int N>
+LaunchFn pick_stokes_n(cudaError_t* err)
+{
+    *err = cudaFuncSetAttribute(dg::k_stokes<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, dg::sk::SLay<N>::BYTES);
+    return launch_stokes<N>;
+}
+LaunchFn pick_stokes(int n, cudaError_t* err)
+{
+    switch (n) {
+    case 2: return pick_stokes_n<2>(err);
+    case 3: return pick_stokes_n<3>(err);
+    case 4: return pick_stokes_n<4>(err);
+    case 5: return pick_stokes_n<5>(err);
+    case 6: return pick_stokes_n<6>(err);
+    case 7: return pick_stokes_n<7>(err);
+    default: return pick_stokes_n<8>(err);
+    }
+}
+// velocity tables (collocated: D at the n Gauss points) and the pressure basis (n-1 Gauss nodes) at the
+// velocity nodes (long double product formulas, as fill_qtab)
+template <int N>
+void fill_stab(const dg::HostTables& H, const dg::HostTables& Hp, void* out)
+{
+    constexpr int NP = N - 1;
+    dg::STab<N>* S = static_cast<dg::STab<N>*>(out);
+    for (int i = 0; i < N * N; ++i) S->D[i] = H.D[i];
+    for (int q = 0; q < N; ++q) {
+        const long double s = H.xi[q];
+        for (int j = 0; j < NP; ++j) {
+            long double v = 1.0L;
+            for (int a = 0; a < NP; ++a)
+                if (a != j) v *= (s - Hp.xi[a]) / ((long double)Hp.xi[j] - Hp.xi[a]);
+            S->AP[q * NP + j] = (double)v;
+        }
+        S->w[q] = H.w[q];
+        S->xi[q] = H.xi[q];
+        S->e0[q] = H.e0[q];
+        S->e1[q] = H.e1[q];
+        S->d0[q] = H.d0[q];
+        S->d1[q] = H.d1[q];
+    }
+    for (int j = 0; j < NP; ++j) {
+        S->ep0[j] = Hp.e0[j];
+        S->ep1[j] = Hp.e1[j];
+    }
+}
+
 // interpolation / derivative of the n-node Lagrange basis at the m = n+1 Gauss points (long double
 // product formulas, no division by (s - x_a): robust when a quadrature point is close to a node)
 template <int N>
@@ -525,6 +584,8 @@ struct dg_ctx {
     int m;     // Gauss points per direction
     bool quad; // m = n + 1: k_quad
     alignas(16) unsigned char qtab[sizeof(dg::QTab<dg::kMaxN, dg::kMaxN + 1>)];
+    bool stokes; // DG_PROBLEM_STOKES: k_stokes
+    alignas(16) unsigned char stab[sizeof(dg::STab<8>)];
     int gen_chunk;
     alignas(16) unsigned char eotab[sizeof(dg::EOTab<dg::kMaxN>)];
     int ax8_tile, ax8_T1, ax8_T2, ax8_chunk;
@@ -577,6 +638,10 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
 #undef AX8_LAUNCH
         }
         return cudaGetLastError();
+    }
+    if (c->stokes) {
+        const long long pcs = c->M.plane_cells;
+        return c->launch(c->stab, c->M, x, xb, xa, r, (long long)p0 * pcs, (long long)p1 * pcs, st, nullptr);
     }
     if (c->quad) {
         const long long pcq = c->M.plane_cells;
@@ -634,8 +699,12 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (mesh->coeff_kind != DG_COEFF_ONE && mesh->coeff_kind != DG_COEFF_SINCOS)
         return fail(DG_ERR_INVALID, "dg_setup: coeff_kind=%d", mesh->coeff_kind);
     if (!(mesh->penalty_scale > 0.0)) return fail(DG_ERR_INVALID, "dg_setup: penalty_scale must be > 0");
-    if (mesh->problem != DG_PROBLEM_PERIODIC && mesh->problem != DG_PROBLEM_DIFFREAC && mesh->problem != DG_PROBLEM_NLREAC)
+    if (mesh->problem != DG_PROBLEM_PERIODIC && mesh->problem != DG_PROBLEM_DIFFREAC && mesh->problem != DG_PROBLEM_NLREAC &&
+        mesh->problem != DG_PROBLEM_STOKES)
         return fail(DG_ERR_INVALID, "dg_setup: problem=%d", mesh->problem);
+    if (mesh->problem == DG_PROBLEM_STOKES &&
+        (mesh->geom_kind != DG_GEOM_AXIS || mesh->coeff_kind != DG_COEFF_ONE || quad != k + 1))
+        return fail(DG_ERR_UNSUPPORTED, "dg_setup: the Stokes problem needs DG_GEOM_AXIS, DG_COEFF_ONE and quad = k+1");
     const bool dr = mesh->problem == DG_PROBLEM_DIFFREAC || mesh->problem == DG_PROBLEM_NLREAC;
     if (dr && (mesh->geom_kind != DG_GEOM_AXIS || mesh->coeff_kind != DG_COEFF_ONE || quad != k + 2))
         return fail(DG_ERR_UNSUPPORTED, "dg_setup: the diffusion-reaction problems need DG_GEOM_AXIS, DG_COEFF_ONE and quad = k+2");
@@ -677,11 +746,13 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         M.h[d] = 1.0 / mesh->N[d];
         M.gamma[d] = mesh->penalty_scale * k * (k + 1) * (double)mesh->N[d];
         // the paper's problem: gamma_F = alpha k (k+d-1) |F| / |T| = alpha k (k+2) / h_d
-        if (dr) M.gamma[d] = mesh->penalty_scale * k * (k + 2) * (double)mesh->N[d];
+        if (dr || mesh->problem == DG_PROBLEM_STOKES) M.gamma[d] = mesh->penalty_scale * k * (k + 2) * (double)mesh->N[d];
     }
     M.jac = nullptr;
     const int64_t n3 = (int64_t)n * n * n;
-    c->plane_dofs = (int64_t)M.plane_cells * n3;
+    // DOFs per cell: n^3, Stokes 3 n^3 + k^3 ([u_0 | u_1 | u_2 | p])
+    const int64_t blk = mesh->problem == DG_PROBLEM_STOKES ? 3 * n3 + (int64_t)k * k * k : n3;
+    c->plane_dofs = (int64_t)M.plane_cells * blk;
     c->local_dofs = c->plane_dofs * M.L;
 
     if (mesh->geom_kind == DG_GEOM_AFFINE) {
@@ -727,6 +798,33 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? (warp ? "k_quadw_diffreac" : "k_quad_diffreac")
                    : mesh->problem == DG_PROBLEM_NLREAC ? "k_quad_nlreac"
                                                         : (warp ? "k_quadw" : "k_quad");
+    }
+    if (mesh->problem == DG_PROBLEM_STOKES) {
+        dg::HostTables Hp;
+        if (dg::build_tables(n - 1, &Hp)) {
+            if (c->d_jac) cudaFree(c->d_jac);
+            free(c);
+            return fail(DG_ERR_INVALID, "tables n=%d", n - 1);
+        }
+        switch (n) {
+        case 2: fill_stab<2>(H, Hp, c->stab); break;
+        case 3: fill_stab<3>(H, Hp, c->stab); break;
+        case 4: fill_stab<4>(H, Hp, c->stab); break;
+        case 5: fill_stab<5>(H, Hp, c->stab); break;
+        case 6: fill_stab<6>(H, Hp, c->stab); break;
+        case 7: fill_stab<7>(H, Hp, c->stab); break;
+        case 8: fill_stab<8>(H, Hp, c->stab); break;
+        }
+        cudaError_t e = cudaSuccess;
+        c->launch = pick_stokes(n, &e);
+        if (e != cudaSuccess) {
+            free(c);
+            return fail(DG_ERR_CUDA, "dg_setup: k_stokes attributes: %s", cudaGetErrorString(e));
+        }
+        c->stokes = true;
+        c->kname = "k_stokes";
+        *out = c;
+        return DG_OK;
     }
     // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
     if (!c->quad) {
@@ -927,6 +1025,17 @@ double dg_alg_flops(const dg_ctx* c)
     if (!c) return -1.0;
     const double n = c->n;
     double F;
+    if (c->stokes) {
+        // Stokes (k_stokes, collocated velocity, pressure n-1 nodes): per cell volume 9 gradient sweeps and
+        // their transposes (36 n^4), the pressure interpolation and its transpose
+        // 4 (p^3 n + p^2 n^2 + p n^3) (p = n-1), 20 n^3 pointwise; each face once: velocity traces and
+        // back-projections both sides (48 n^3), pressure traces / tangential interpolation and back
+        // (4 p^3 + 8 (p^2 n + p n^2)), 40 n^2 flux
+        const double p = n - 1;
+        const double vol = 36 * n * n * n * n + 4 * (p * p * p * n + p * p * n * n + p * n * n * n) + 20 * n * n * n;
+        const double face = 48 * n * n * n + 4 * p * p * p + 8 * (p * p * n + p * n * n) + 40 * n * n;
+        return (vol + 3.0 * face) / (3 * n * n * n + p * p * p) * (double)c->local_dofs;
+    }
     if (c->quad) {
         // general quadrature (k_quad, m points): the sum-factorisation contractions as executed (A != I):
         // volume 2 (4 n^3 m + 6 n^2 m^2 + 6 n m^3) + (21 + Cc) m^3 per cell; each face once:

@@ -26,6 +26,7 @@ DG_COEFF_SINCOS = 1
 DG_PROBLEM_PERIODIC = 0
 DG_PROBLEM_DIFFREAC = 1
 DG_PROBLEM_NLREAC = 2
+DG_PROBLEM_STOKES = 3
 
 _ERRNAMES = {-1: "DG_ERR_INVALID", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_CUDA", -5: "DG_ERR_OOM"}
 

@@ -19,7 +19,7 @@ cp = {"bench.json": "bench_cfg3_n1.json", "bench_ref.json": "bench_reference_cfg
 for c in (0, 1, 2, 4):
     cp[f"bench_cfg{c}.json"] = f"bench_cfg{c}_n1.json"
 for f in ("bench_cfg2_quad7.json", "bench_diffreac_k3_64.json", "bench_diffreac_k5_48.json", "bench_nlreac_k3_64.json",
-          "bench_nljac_k3_64.json"):
+          "bench_nljac_k3_64.json", "bench_stokes_k3_48.json", "bench_stokes_k5_32.json"):
     cp[f] = f
 for f in glob.glob(os.path.join(SRC, "ncu_*.md")) + glob.glob(os.path.join(SRC, "ncu_*.json")) + \
         glob.glob(os.path.join(SRC, "stalls_*.txt")) + glob.glob(os.path.join(SRC, "launches_*.csv")):

@@ -10,7 +10,7 @@ R = os.path.join(ROOT, "profiles", RND)
 T = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
 files = [f"bench_cfg{c}_n1.json" for c in range(5)] + ["bench_cfg2_quad7.json", "bench_diffreac_k3_64.json",
                                                         "bench_diffreac_k5_48.json", "bench_nlreac_k3_64.json",
-                                                        "bench_nljac_k3_64.json"]
+                                                        "bench_nljac_k3_64.json", "bench_stokes_k3_48.json", "bench_stokes_k5_32.json"]
 L = ["# Round 1 evidence (B200, 1 GPU)\n",
      "Produced by `tools/round_evidence.sh` on one gpurun box, copied by `tools/collect_evidence.py`, this file by",
      "`tools/evidence_readme.py`. Bench lines: `python bench.py --config C` (timed region = K applies, CUDA events on",
