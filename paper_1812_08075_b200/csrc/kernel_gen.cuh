@@ -169,6 +169,19 @@ __device__ __forceinline__ void cmul(double ar, double ai, double br, double bi,
     ci = fma(ar, bi, ai * br);
 }
 
+// a face point's (u, g) pair in two separate shared arrays, used like a double2
+struct TRRef {
+    double& x;
+    double& y;
+    __device__ __forceinline__ operator double2() const { return make_double2(x, y); }
+    __device__ __forceinline__ void operator=(double2 v) { x = v.x; y = v.y; }
+};
+struct TRView {
+    double* u;
+    double* g;
+    __device__ __forceinline__ TRRef operator[](int p) const { return TRRef{u[p], g[p]}; }
+};
+
 // shared-memory layout (in doubles) of k_gen<N, AFFINE, COEFF, T1, T2>
 template <int N, bool AFFINE, bool COEFF, int T1, int T2>
 struct Lay {
@@ -186,19 +199,22 @@ struct Lay {
     // affine face passes: per face line (N points per thread, 2 buffers, warp-local A -> B -> C) for n <= 6,
     // per face point (3 buffers, CTA barriers between the passes) for n >= 7
     static constexpr bool FACE_LINES = N <= 6;
-    // face-slot strides chosen against bank conflicts of the line tasks (16-B pairs: 3 FS = 5 mod 8, so
-    // both the t2-line (point-consecutive) and the t1-line (face-consecutive) task orders hit distinct
-    // banks; 8-B line buffers: odd FB)
-    static constexpr int pad_fs(int base) { return (3 * base) % 8 == 5 ? base : pad_fs(base + 1); }
-    static constexpr int FS = pad_fs(2 * N2);          // pairs per face (2 sides x N2 points + pad)
-    static constexpr int FB = (N2 % 2) ? N2 : N2 + 1;  // doubles per face in the line buffers
+    // face slots: [u-, u+, g-, g+] (N2 doubles each; u/V and gn/G kept apart so the 8-B reads of one of
+    // them touch every bank). Face strides chosen against bank conflicts of the warp-local line tasks
+    // (lane = face fo, line l): 3 FSD mod 16 = TSEL makes the t1-line passes (lane-varying offset
+    // 3 FSD fo + N l) conflict-free and the t2-line pass (3 FSD fo + l) at most 2-way; the same for the
+    // 8-B line buffers (FB)
+    static constexpr int TSEL = N == 2 ? 2 : (N == 3 ? 9 : (N == 4 ? 3 : (N == 5 ? 9 : 7)));
+    static constexpr int pad16(int base) { return (3 * base) % 16 == TSEL ? base : pad16(base + 1); }
+    static constexpr int FSD = pad16(4 * N2);          // doubles per face slot
+    static constexpr int FB = pad16(N2);               // doubles per face in the line buffers
     static constexpr int WCSZ = AFFINE ? (FACE_LINES ? 2 * NF * FB : 3 * NF * N2) : 0;
     static constexpr int RX = XS + 2 * NC * N3;                         // ring blocks, aliased by W / CG after P1
     static constexpr int RXEND = RX + (RXSZ > WCSZ ? RXSZ : WCSZ);
     static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
     static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // [2][NC][N3] grad0/1 -> Q0/1 -> R0/1
-    static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][side][u|V, gn|G][N2]
-    static constexpr int CX = TRB + NF * 2 * FS;                        // [2][NC][CXSZ] c(x) factor tables (volume)
+    static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][u|V, gn|G][side][N2] (+ pad)
+    static constexpr int CX = TRB + NF * FSD;                           // [2][NC][CXSZ] c(x) factor tables (volume)
     static constexpr int CF = CX + (COEFF ? 2 * NC * CXSZ : 0);         // [2][NCG][CFSZ] c(x) at upper-face points
     static constexpr int END = CF + (COEFF ? 2 * NCG * CFSZ : 0);
     static constexpr int BYTES = END * 8 + 64; // + 2 mbarriers
@@ -300,7 +316,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     double* const XS = sm + Y::XS;
     double* const RX = sm + Y::RX;
     double* const BX = sm + Y::RX;           // face buffers (AFFINE, after P1, aliasing the ring blocks):
-    constexpr int FS = Y::FS, FB = Y::FB;
+    constexpr int FSD = Y::FSD, FB = Y::FB;
     double* const BY = sm + Y::RX + NF * FB; // BX: w2 -> Cg, BY: D_t1 w1 -> D_t2^T Cg, [NF][FB]
     double* const PW = sm + Y::RX;              // point passes: W [NF][2][N2]
     double* const PCG = sm + Y::RX + 2 * NF * N2; //              Cg [NF][N2]
@@ -334,8 +350,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto xplane = [&](int lp) -> const double* { return lp < 0 ? xb : (lp >= M.L ? xa : x + (long long)lp * PC * N3); };
     auto grec = [&](int lp, int i1, int i2) -> const double* { return geo + (cidx(lp + 1, i1, i2)) * GREC; };
     // face slots: (u, gn) -> (V, G) pairs per face f, side (0: T-, 1: T+), point p
-    double2* const TR2 = reinterpret_cast<double2*>(TRB);
-    auto TRp = [&](int f, int side) -> double2* { return TR2 + f * FS + side * N2; };
+    // TRp(f, side)[p]: (.x = u / V, .y = gn / G) of face f, side, point p, stored in separate arrays
+    auto TRp = [&](int f, int side) { return gn::TRView{TRB + f * FSD + side * N2, TRB + f * FSD + (2 + side) * N2}; };
 
     // fixed thread coordinates: cell mc of the tile, line position (ma, mb)
     const bool act = tid < Y::NACT;
