@@ -212,8 +212,13 @@ struct Lay {
     static constexpr int RX = XS + 2 * NC * N3;                         // ring blocks, aliased by W / CG after P1
     static constexpr int RXEND = RX + (RXSZ > WCSZ ? RXSZ : WCSZ);
     static constexpr int GE = (RXEND + 1) / 2 * 2;                      // [2][NCG][GREC] geometry records
-    static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // [2][NC][N3] grad0/1 -> Q0/1 -> R0/1
-    static constexpr int TRB = G01 + 2 * NC * N3;                       // [NF][u|V, gn|G][side][N2] (+ pad)
+    // G0 / G1: [j2][cell][j0 + N j1] with the j2 stride padded (S0, S1) so that the d = 0 (G0) and d = 1 (G1)
+    // line accesses of a half-warp spread over the banks
+    static constexpr int P0 = N == 3 ? 10 : (N <= 6 ? 1 : 0);
+    static constexpr int P1 = N == 2 ? 2 : (N == 3 ? 11 : (N == 4 ? 4 : (N == 5 ? 13 : (N == 6 ? 6 : 0))));
+    static constexpr int S0 = NC * N2 + P0, S1 = NC * N2 + P1;
+    static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // G0 [N][S0], G1 [N][S1]: grad0/1 -> Q0/1 -> R0/1
+    static constexpr int TRB = (G01 + N * (S0 + S1) + 1) / 2 * 2;                       // [NF][u|V, gn|G][side][N2] (+ pad)
     static constexpr int CX = TRB + NF * FSD;                           // [2][NC][CXSZ] c(x) factor tables (volume)
     static constexpr int CF = CX + (COEFF ? 2 * NC * CXSZ : 0);         // [2][NCG][CFSZ] c(x) at upper-face points
     static constexpr int END = CF + (COEFF ? 2 * NCG * CFSZ : 0);
@@ -323,7 +328,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     constexpr bool FACE_LINES = Y::FACE_LINES;
     double* const GE = sm + Y::GE;
     double* const G0 = sm + Y::G01;
-    double* const G1 = sm + Y::G01 + NC * N3;
+    double* const G1 = sm + Y::G01 + N * Y::S0;
     double* const TRB = sm + Y::TRB;
     double* const CX = sm + Y::CX;
     double* const CF = sm + Y::CF;
@@ -362,10 +367,11 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     const int flo2 = mc2 > 0 ? 3 * (mc - 1) + 2 : 3 * NC + T2 + mc1;
     // G0 / G1 layout [j2][cell][j0 + N j1]: the d = 2 line points of consecutive threads are consecutive
     // (conflict-free stage 2 and final sum); index of point j on the thread's d-line of its cell
-    auto gix = [&](int d, int j) -> int {
-        return d == 0 ? mb * NC * N2 + mc * N2 + j + N * ma
-                      : (d == 1 ? mb * NC * N2 + mc * N2 + ma + N * j : j * NC * N2 + mc * N2 + mab);
+    auto gixs = [&](int S, int d, int j) -> int {
+        return d == 0 ? mb * S + mc * N2 + j + N * ma : (d == 1 ? mb * S + mc * N2 + ma + N * j : j * S + mc * N2 + mab);
     };
+    auto gix0 = [&](int d, int j) { return gixs(Y::S0, d, j); }; // G0 index
+    auto gix1 = [&](int d, int j) { return gixs(Y::S1, d, j); }; // G1 index
 
     if (tid < N) { sXi[tid] = E.xi[tid]; sW[tid] = E.w[tid]; }
     for (int i = tid; i < N * N; i += NT) sD[i] = E.D[i];
@@ -863,10 +869,10 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                     const double S = wab * E.Sc[d];
                     if (d == 0) {
 #pragma unroll
-                        for (int j = 0; j < N; ++j) G0[gix(0, j)] = S * y[j];
+                        for (int j = 0; j < N; ++j) G0[gix0(0, j)] = S * y[j];
                     } else if (d == 1) {
 #pragma unroll
-                        for (int j = 0; j < N; ++j) G1[gix(1, j)] = S * y[j];
+                        for (int j = 0; j < N; ++j) G1[gix1(1, j)] = S * y[j];
                     } else {
 #pragma unroll
                         for (int j = 0; j < N; ++j) y2[j] = S * y[j];
@@ -880,7 +886,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             if (act) {
                 double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
 #pragma unroll
-                for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y2[j] + G0[gix(2, j)] + G1[gix(2, j)];
+                for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y2[j] + G0[gix0(2, j)] + G1[gix1(2, j)];
             }
             continue;
         }
@@ -903,10 +909,10 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 TRp(3 * mc + d, 0)[mab] = make_double2(uhi, ghi);
                 if (d == 0) {
 #pragma unroll
-                    for (int j = 0; j < N; ++j) G0[gix(0, j)] = y[j];
+                    for (int j = 0; j < N; ++j) G0[gix0(0, j)] = y[j];
                 } else if (d == 1) {
 #pragma unroll
-                    for (int j = 0; j < N; ++j) G1[gix(1, j)] = y[j];
+                    for (int j = 0; j < N; ++j) G1[gix1(1, j)] = y[j];
                     TRp(flo1, 1)[mab] = make_double2(ulo, glo);
                 } else {
 #pragma unroll
@@ -945,7 +951,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             const double wab = sW[ma] * sW[mb];
 #pragma unroll
             for (int q = 0; q < N; ++q) {
-                const int P = gix(2, q);
+                const int P = gix0(2, q), P1 = gix1(2, q);
                 double cW = wab * E.w[q];
                 if (COEFF) {
                     const double* cx = cxcur + mc * CXSZ;
@@ -955,15 +961,15 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                     const double c1 = fma(z1r, e1[0], -z1i * e1[1]); // Re(z1 e1) = cos(2 pi x1)
                     cW *= fma(0.5 * s0, c1, 1.0);
                 }
-                const double a0 = G0[P], a1 = G1[P], a2 = g2[q];
+                const double a0 = G0[P], a1 = G1[P1], a2 = g2[q];
                 if (AFFINE) {
                     G0[P] = cW * fma(gt[0], a0, fma(gt[3], a1, gt[4] * a2));
-                    G1[P] = cW * fma(gt[3], a0, fma(gt[1], a1, gt[5] * a2));
+                    G1[P1] = cW * fma(gt[3], a0, fma(gt[1], a1, gt[5] * a2));
                     q2[q] = cW * fma(gt[4], a0, fma(gt[5], a1, gt[2] * a2));
                 } else {
                     const double adet = M.h[0] * M.h[1] * M.h[2];
                     G0[P] = cW * (adet / (M.h[0] * M.h[0])) * a0;
-                    G1[P] = cW * (adet / (M.h[1] * M.h[1])) * a1;
+                    G1[P1] = cW * (adet / (M.h[1] * M.h[1])) * a1;
                     q2[q] = cW * (adet / (M.h[2] * M.h[2])) * a2;
                 }
             }
@@ -1009,14 +1015,14 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             {
                 double v[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) v[j] = G0[gix(0, j)];
+                for (int j = 0; j < N; ++j) v[j] = G0[gix0(0, j)];
                 double xe[HE], xo[H > 0 ? H : 1];
                 gn::split<N>(v, xe, xo);
                 double y[N];
                 const double2 hi = TRp(3 * mc, 0)[mab];
                 gn::sweep<N, true, true>(E, xe, xo, y, pendV, pendG, hi.x, hi.y);
 #pragma unroll
-                for (int j = 0; j < N; ++j) G0[gix(0, j)] = y[j];
+                for (int j = 0; j < N; ++j) G0[gix0(0, j)] = y[j];
                 const double2 nx = TRp(3 * mc, 1)[mab]; // the T+ half of this face is the next plane's lower face
                 pendV = nx.x;
                 pendG = nx.y;
@@ -1024,14 +1030,14 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             {
                 double v[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) v[j] = G1[gix(1, j)];
+                for (int j = 0; j < N; ++j) v[j] = G1[gix1(1, j)];
                 double xe[HE], xo[H > 0 ? H : 1];
                 gn::split<N>(v, xe, xo);
                 double y[N];
                 const double2 lo = TRp(flo1, 1)[mab], hi = TRp(3 * mc + 1, 0)[mab];
                 gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
 #pragma unroll
-                for (int j = 0; j < N; ++j) G1[gix(1, j)] = y[j];
+                for (int j = 0; j < N; ++j) G1[gix1(1, j)] = y[j];
             }
         }
         __syncthreads();
@@ -1044,7 +1050,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
             double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
 #pragma unroll
-            for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y[j] + G0[gix(2, j)] + G1[gix(2, j)];
+            for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y[j] + G0[gix0(2, j)] + G1[gix1(2, j)];
         }
         GEN_STAMP(7);
         // (the barrier at the top of the next step orders these reads before the next writes)
