@@ -201,11 +201,11 @@ struct Lay {
     static constexpr bool FACE_LINES = N <= 6;
     // face slots: [u-, u+, g-, g+] (N2 doubles each; u/V and gn/G kept apart so the 8-B reads of one of
     // them touch every bank). Face strides chosen against bank conflicts of the warp-local line tasks
-    // (lane = face fo, line l): 3 FSD mod 16 = TSEL makes the t1-line passes (lane-varying offset
-    // 3 FSD fo + N l) conflict-free and the t2-line pass (3 FSD fo + l) at most 2-way; the same for the
-    // 8-B line buffers (FB)
+    // (lane = face fo, line l; faces stored by their ordinal, fslot): FSD mod 16 = TSEL makes the t1-line
+    // passes (lane-varying offset FSD fo + N l) conflict-free and the t2-line pass (FSD fo + l) at most
+    // 2-way; the same for the 8-B line buffers (FB)
     static constexpr int TSEL = N == 2 ? 2 : (N == 3 ? 9 : (N == 4 ? 3 : (N == 5 ? 9 : 7)));
-    static constexpr int pad16(int base) { return (3 * base) % 16 == TSEL ? base : pad16(base + 1); }
+    static constexpr int pad16(int base) { return base % 16 == TSEL ? base : pad16(base + 1); }
     static constexpr int FSD = pad16(4 * N2);          // doubles per face slot
     static constexpr int FB = pad16(N2);               // doubles per face in the line buffers
     static constexpr int WCSZ = AFFINE ? (FACE_LINES ? 2 * NF * FB : 3 * NF * N2) : 0;
@@ -356,7 +356,13 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto grec = [&](int lp, int i1, int i2) -> const double* { return geo + (cidx(lp + 1, i1, i2)) * GREC; };
     // face slots: (u, gn) -> (V, G) pairs per face f, side (0: T-, 1: T+), point p
     // TRp(f, side)[p]: (.x = u / V, .y = gn / G) of face f, side, point p, stored in separate arrays
-    auto TRp = [&](int f, int side) { return gn::TRView{TRB + f * FSD + side * N2, TRB + f * FSD + (2 + side) * N2}; };
+    // storage slot of face f (own faces 3 c + d, ring faces 3 NC + r): its ordinal d NC + c / 3 NC + r, so
+    // the faces of a warp's line tasks occupy consecutive slots
+    auto fslot = [&](int f) { return f < 3 * NC ? (f % 3) * NC + f / 3 : f; };
+    auto TRp = [&](int f, int side) {
+        const int o = fslot(f);
+        return gn::TRView{TRB + o * FSD + side * N2, TRB + o * FSD + (2 + side) * N2};
+    };
 
     // fixed thread coordinates: cell mc of the tile, line position (ma, mb)
     const bool act = tid < Y::NACT;
@@ -571,13 +577,13 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             const int p = a + N * b;
             const double um = TRp(f, 0)[p].x, up = TRp(f, 1)[p].x;
             w1[a] = fma(A.mt1, um, A.pt1 * up);
-            BX[f * FB + p] = fma(A.mt2, um, A.pt2 * up);
+            BX[fslot(f) * FB + p] = fma(A.mt2, um, A.pt2 * up);
         }
         double xe[HE], xo[H > 0 ? H : 1], y[N];
         gn::split<N>(w1, xe, xo);
         gn::sweep<N, false, false>(E, xe, xo, y);
 #pragma unroll
-        for (int a = 0; a < N; ++a) BY[f * FB + a + N * b] = y[a];
+        for (int a = 0; a < N; ++a) BY[fslot(f) * FB + a + N * b] = y[a];
     };
     // line B (t2-line a): {c grad u . n} = c_F/2 (a-_d gn- + a+_d gn+ + D_t1 w1 + D_t2 w2), SIPG flux
     // (Eq. diffreac_weak, theta = -1): Cv- -> TR(f,0).x, Cg -> BX, D_t2^T Cg -> BY
@@ -586,7 +592,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const FaceA A = face_a(DC, gb, f);
         double w2[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) w2[k] = BX[f * FB + a + N * k];
+        for (int k = 0; k < N; ++k) w2[k] = BX[fslot(f) * FB + a + N * k];
         double xe[HE], xo[H > 0 ? H : 1], s2[N];
         gn::split<N>(w2, xe, xo);
         gn::sweep<N, false, false>(E, xe, xo, s2);
@@ -596,7 +602,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         for (int b = 0; b < N; ++b) {
             const int p = a + N * b;
             const double2 m = TRp(f, 0)[p], pl = TRp(f, 1)[p];
-            const double s = fma(A.mdn, m.y, fma(A.pdn, pl.y, BY[f * FB + p] + s2[b]));
+            const double s = fma(A.mdn, m.y, fma(A.pdn, pl.y, BY[fslot(f) * FB + p] + s2[b]));
             const double cF = COEFF ? cfcur[face_rec(f) * CFSZ + d * N2 + p] : 1.0; // c at x_F on T- (R12)
             const double Wt = wa * sW[b] * A.dS;
             const double jump = m.x - pl.x;
@@ -608,8 +614,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         gn::sweep<N, true, false>(E, xe, xo, t2);
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-            BX[f * FB + a + N * b] = cg[b];
-            BY[f * FB + a + N * b] = t2[b];
+            BX[fslot(f) * FB + a + N * b] = cg[b];
+            BY[fslot(f) * FB + a + N * b] = t2[b];
         }
     };
     // line C (t1-line b): V+- = +-Cv- + a+-_t1 D_t1^T Cg + a+-_t2 D_t2^T Cg, G+- = a+-_d Cg
@@ -617,14 +623,14 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const FaceA A = face_a(DC, gb, f);
         double cg[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) cg[k] = BX[f * FB + k + N * b];
+        for (int k = 0; k < N; ++k) cg[k] = BX[fslot(f) * FB + k + N * b];
         double xe[HE], xo[H > 0 ? H : 1], t1[N];
         gn::split<N>(cg, xe, xo);
         gn::sweep<N, true, false>(E, xe, xo, t1);
 #pragma unroll
         for (int a = 0; a < N; ++a) {
             const int p = a + N * b;
-            const double Cvm = TRp(f, 0)[p].x, t2 = BY[f * FB + p];
+            const double Cvm = TRp(f, 0)[p].x, t2 = BY[fslot(f) * FB + p];
             TRp(f, 0)[p] = make_double2(fma(A.mt1, t1[a], fma(A.mt2, t2, Cvm)), A.mdn * cg[a]);
             TRp(f, 1)[p] = make_double2(fma(A.pt1, t1[a], fma(A.pt2, t2, -Cvm)), A.pdn * cg[a]);
         }
