@@ -662,13 +662,20 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // passes A -> B -> C of a face need only __syncwarp (no CTA barriers between them); the face direction
     // is a run-time value (faces of several directions share a warp)
     auto face_warp = [&](const double* gb) {
-        constexpr int FPW = 32 / N;          // faces per warp and round
+        // n = 6: whole faces per half-warp (2 x 2 faces, lanes 12-15 idle) — with FSD = 7 mod 16 every pass
+        // is bank-conflict free; otherwise 32 / n faces on consecutive lanes
+        constexpr bool HALF = N == 6;
+        constexpr int FPH = 16 / N;
+        constexpr int FPW = HALF ? 2 * FPH : 32 / N; // faces per warp and round
         constexpr int NWARP = NT / 32;
         const int warp = tid >> 5, lane = tid & 31;
-        const int fo = lane / N, l = lane - fo * N;
+        const int hl = HALF ? (lane & 15) : lane;
+        const int fo = HALF ? (lane >> 4) * FPH + hl / N : lane / N;
+        const int l = hl - (hl / N) * N;
+        const bool lane_on = HALF ? hl < FPH * N : lane < FPW * N;
         for (int base = 0; base < NF; base += FPW * NWARP) {
             const int o = base + warp * FPW + fo;
-            const bool on = lane < FPW * N && o < NF;
+            const bool on = lane_on && o < NF;
             int f = 0, d = 0;
             if (on) {
                 if (o < NC) { f = 3 * o; d = 0; }
