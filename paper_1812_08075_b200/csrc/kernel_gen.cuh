@@ -364,6 +364,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         return gn::TRView{TRB + o * FSD + side * N2, TRB + o * FSD + (2 + side) * N2};
     };
 
+    // the thread that issues the bulk copies: the last one (no stage-2 point, no face line for n >= 4), off
+    // the critical path of the face phase
+    constexpr int PROD = Y::NACT < NT ? NT - 1 : 0;
     // fixed thread coordinates: cell mc of the tile, line position (ma, mb)
     const bool act = tid < Y::NACT;
     const int mc = act ? tid / N2 : 0, mab = act ? tid % N2 : 0, ma = mab % N, mb = mab / N;
@@ -755,7 +758,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // ---------------- prologue: the lower d=0 face of plane p_begin (T- = plane p_begin - 1) ----------------
     double pendV = 0.0, pendG = 0.0; // T+ half of the d=0 face below the thread's line (a, b) of cell mc
     {
-        if (tid == 0) {
+        if (tid == PROD) {
             gn::mbar_expect_tx(barA, 2 * T1 * ROWB + GEOB);
             issue_x(p_begin - 1, XS + NC * N3);
             issue_x(p_begin, XS);
@@ -816,7 +819,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             pendG = vg.y;
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid == PROD) {
             gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
             issue_x(p_begin + 1, XS + NC * N3);
             if (AFFINE || COEFF) issue_geo(p_begin, 0);
@@ -860,7 +863,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             foreign(XN);
             __syncthreads();
             if (s + 1 < nsteps) { // own plane buffer and ring buffer are free
-                if (tid == 0) {
+                if (tid == PROD) {
                     gn::mbar_expect_tx(barA, T1 * ROWB);
                     issue_x(lp + 2, XS + (s & 1) * NC * N3);
                     issue_ring_bulk(lp + 1);
@@ -941,7 +944,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         GEN_STAMP(2);
 
         // stream the next step's own blocks (plane lp + 2) and geometry (plane lp + 1) behind the compute
-        if (tid == 0 && s + 1 < nsteps) {
+        if (tid == PROD && s + 1 < nsteps) {
             gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
             issue_x(lp + 2, XS + (s & 1) * NC * N3);
             if (AFFINE || COEFF) issue_geo(lp + 1, (s + 1) & 1);
@@ -1009,7 +1012,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             GEN_STAMP(5);
 #else
             // ---------------- P3: face passes A -> B -> C, warp-local ----------------
+            GEN_STAMP(4);
             face_warp(gb);
+            GEN_STAMP(5);
             __syncthreads();
             GEN_STAMP(3);
 #endif
@@ -1019,7 +1024,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
         // the ring buffer (aliased by the face buffers) is free: stream the next plane's ring blocks
         if (s + 1 < nsteps) {
-            if (tid == 0) issue_ring_bulk(lp + 1);
+            if (tid == PROD) issue_ring_bulk(lp + 1);
             issue_ring_cp(lp + 1);
         }
 
