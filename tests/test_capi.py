@@ -66,3 +66,28 @@ def test_errors_without_device_or_bad_args(lib):
         assert ei.value.code == dg.DG_ERR_CUDA
     assert lib.dg_apply(None, None, None) == dg.DG_ERR_INVALID
     assert lib.dg_destroy(None) == dg.DG_OK
+
+
+def test_problem_validation(lib):
+    """The problem field: unknown kinds are invalid; the diffusion-reaction, nonlinear and Stokes problems are
+    restricted to the combinations their kernels implement (DG_ERR_UNSUPPORTED otherwise), checked before any
+    CUDA call; the Jacobian entry rejects NULL arguments."""
+    from paper_1812_08075_b200 import dg
+    m = dg.dg_mesh()
+    m.N[0] = m.N[1] = m.N[2] = 4
+    m.nplanes = 4
+    m.penalty_scale = 3.0
+    h = ctypes.c_void_p()
+    m.problem = 7
+    assert lib.dg_setup(ctypes.byref(m), 2, 4, ctypes.byref(h)) == dg.DG_ERR_INVALID
+    for prob in (dg.DG_PROBLEM_DIFFREAC, dg.DG_PROBLEM_NLREAC):
+        m.problem = prob
+        assert lib.dg_setup(ctypes.byref(m), 2, 3, ctypes.byref(h)) == dg.DG_ERR_UNSUPPORTED  # needs quad = k+2
+        m.coeff_kind = dg.DG_COEFF_SINCOS
+        assert lib.dg_setup(ctypes.byref(m), 2, 4, ctypes.byref(h)) == dg.DG_ERR_UNSUPPORTED
+        m.coeff_kind = dg.DG_COEFF_ONE
+    m.problem = dg.DG_PROBLEM_STOKES
+    assert lib.dg_setup(ctypes.byref(m), 2, 4, ctypes.byref(h)) == dg.DG_ERR_UNSUPPORTED  # needs quad = k+1
+    assert "Stokes" in dg.dg_last_error()
+    assert lib.dg_apply_jacobian(None, None, None, None) == dg.DG_ERR_INVALID
+    assert lib.dg_apply_jacobian_planes(None, None, None, None, None, None, 0, 0) == dg.DG_ERR_INVALID
