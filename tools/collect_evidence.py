@@ -31,7 +31,9 @@ for a, b in cp.items():
         n += 1
 
 WORK = {"axis8_cfg3": "cfg3_poisson_q7_96", "gen_cfg1": "cfg1_poisson_q3_32", "gen_cfg2": "cfg2_diffusion_q5_64_affine",
-        "gen_cfg4": "cfg4_diffusion_q4_256_affine"}
+        "gen_cfg4": "cfg4_diffusion_q4_256_affine",
+        # (workload, the kernel name dg_kernel_name reports)
+        "quad_dr3": ("diffreac_k3_N64x64x64_m5", "k_quad_diffreac"), "stokes_k3": ("stokes_k3_N48x48x48", "k_stokes")}
 tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 traffic = json.load(open(tp)) if os.path.exists(tp) else {}
 unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -46,10 +48,13 @@ for key, wl in WORK.items():
     path = os.path.join(SRC, f"ncu_{key}.json")
     if not os.path.exists(path):
         continue
+    kname = None
+    if isinstance(wl, tuple):
+        wl, kname = wl
     for d in json.load(open(path)).get("full", []):
         m = re.match(r"void (k_\w+)", d["kernel"])
         if m:
-            traffic.setdefault(wl, {})[m.group(1)] = val(d["DRAM read"]) + val(d["DRAM write"])
+            traffic.setdefault(wl, {})[kname or m.group(1)] = val(d["DRAM read"]) + val(d["DRAM write"])
 json.dump(traffic, open(tp, "w"), indent=1)
 print("copied", n, "files ->", DST)
 print(json.dumps(traffic, indent=1))

@@ -34,8 +34,15 @@ B4="python bench.py --config 4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg4 $B4 > $O/ncu4.log 2>&1
 B1="python bench.py --config 1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg1 $B1 > $O/ncu1.log 2>&1
+# SURVEY §8(f) kernels: the diffusion-reaction residual (k_quad), the Jacobian action, Stokes (k_stokes)
+B5="python bench.py --problem diffreac --k 3 --N 64 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_quad -s 3 -c 1 -o $O/prof_quad_dr3 $B5 > $O/ncu5.log 2>&1
+B6="python bench.py --problem nlreac --jacobian --k 3 --N 64 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_quad -s 3 -c 1 -o $O/prof_quad_nljac3 $B6 > $O/ncu6.log 2>&1
+B7="python bench.py --problem stokes --k 3 --N 48 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+ncu --set full --clock-control none --import-source on -k regex:k_stokes -s 3 -c 1 -o $O/prof_stokes_k3 $B7 > $O/ncu7.log 2>&1
 # summaries on the box (the .ncu-rep files are ~20 MB each; gpurun returns <= 64 MiB)
-for R in axis8_cfg3 gen_cfg2 gen_cfg4 gen_cfg1; do
+for R in axis8_cfg3 gen_cfg2 gen_cfg4 gen_cfg1 quad_dr3 quad_nljac3 stokes_k3; do
   python tools/ncu_stalls.py $O/prof_$R.ncu-rep > $O/stalls_$R.txt 2>&1
   python tools/ncu_stalls.py $O/prof_$R.ncu-rep --lines >> $O/stalls_$R.txt 2>&1
 done
@@ -43,6 +50,9 @@ python tools/ncu_summary.py --launches $O/launches_cfg3.csv --rep $O/prof_axis8_
 python tools/ncu_summary.py --launches $O/launches_cfg2.csv --rep $O/prof_gen_cfg2.ncu-rep --out $O/ncu_gen_cfg2 --title "k_gen on cfg2 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --launches $O/launches_cfg4.csv --rep $O/prof_gen_cfg4.ncu-rep --out $O/ncu_gen_cfg4 --title "k_gen on cfg4 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --rep $O/prof_gen_cfg1.ncu-rep --out $O/ncu_gen_cfg1 --title "k_gen on cfg1 (N=1)" > /dev/null 2>&1
+python tools/ncu_summary.py --rep $O/prof_quad_dr3.ncu-rep --out $O/ncu_quad_dr3 --title "k_quad_diffreac, k=3 on 64^3 (SURVEY 8(f1))" > /dev/null 2>&1
+python tools/ncu_summary.py --rep $O/prof_quad_nljac3.ncu-rep --out $O/ncu_quad_nljac3 --title "k_quad_nlreac Jacobian action, k=3 on 64^3 (SURVEY 8(f3))" > /dev/null 2>&1
+python tools/ncu_summary.py --rep $O/prof_stokes_k3.ncu-rep --out $O/ncu_stokes_k3 --title "k_stokes, k=3 on 48^3 (SURVEY 8(f4))" > /dev/null 2>&1
 rm -f $O/*.ncu-rep  # summaries only: gpurun returns <= 64 MiB
 tail -2 $O/pytest_gpu.log
 cat $O/bench.json
