@@ -21,7 +21,8 @@ L = ["# Round 1 evidence (B200, 1 GPU)\n",
      "(geometry records 288 B, c(x) factor tables 96(n+1) B, face c values 8(3n^2 rounded to even) B per cell) that",
      "`B_alg` (x, r and J only) does not count. Rows below the line: SURVEY §8(f2) general quadrature and §8(f1) the",
      "paper's diffusion-reaction problem, §8(f3) its nonlinear variant (residual and Jacobian action, reading R26),",
-     "§8(f4) the paper's Stokes problem (correctness-first kernels; F_alg = their contractions as executed).\n",
+     "§8(f4) the paper's Stokes problem (correctness-first kernels; F_alg = their contractions as executed; ncu",
+     "captures: `ncu_quad_dr3`, `ncu_quad_nljac3`, `ncu_stokes_k3`, stalls in `stalls_*.txt`).\n",
      "| line | workload | ms / apply | GDOF/s | kernel | bound | frac of roofline | frac HBM (alg bytes) | frac of measured DFMA peak | DRAM traffic / alg bytes |",
      "|---|---|---|---|---|---|---|---|---|---|"]
 for f in files:
