@@ -155,9 +155,10 @@ class NewtonResult:
 
 
 def newton(op, ndofs: int, device="cuda", x0=None, rtol: float = 1e-12, maxiter: int = 20,
-           cg_rtol: float = 1e-13, cg_maxiter: int = 4000) -> NewtonResult:
+           cg_rtol: float = 1e-13, cg_maxiter: int = 4000, graph: bool = False) -> NewtonResult:
     """Solve R(x) = 0 for a DG_PROBLEM_NLREAC operator: x <- x - J(x)^{-1} R(x), the linear systems by CG on
-    the matrix-free Jacobian action op.apply_jacobian(x, .) (one libdg launch each)."""
+    the matrix-free Jacobian action op.apply_jacobian(x, .) (one libdg launch each; graph=True: the inner CG
+    as cg_graph, the linearization point x being a fixed buffer updated in place)."""
     import torch
     x = torch.zeros(ndofs, dtype=torch.float64, device=device) if x0 is None else x0.clone()
     r = op.apply(x).clone()
@@ -171,8 +172,17 @@ def newton(op, ndofs: int, device="cuda", x0=None, rtol: float = 1e-12, maxiter:
         op.apply_jacobian(x, v, jz)
         return jz
 
+    orig = op._stream
+
+    def on_capture(stream):
+        op.set_stream(stream if stream is not None else orig)
+
     while it < maxiter and hist[-1] > rtol * r_init:
-        res = cg(apply_J, -r, rtol=cg_rtol, maxiter=cg_maxiter)
+        if graph:
+            res = cg_graph(lambda v, out: op.apply_jacobian(x, v, out), -r, rtol=cg_rtol, maxiter=cg_maxiter,
+                           on_capture=on_capture)
+        else:
+            res = cg(apply_J, -r, rtol=cg_rtol, maxiter=cg_maxiter)
         cgits.append(res.iterations)
         x.add_(res.x)
         op.apply(x, r)

@@ -113,14 +113,14 @@ def test_nlreac_slab_loopback_bitwise(world):
     full.close()
 
 
-@pytest.mark.parametrize("k", [2, 3])
-def test_newton_solves_the_nonlinear_problem(k):
+@pytest.mark.parametrize("k,graph", [(2, False), (3, False), (3, True)])
+def test_newton_solves_the_nonlinear_problem(k, graph):
     """Newton-CG driving dg_apply / dg_apply_jacobian reaches the discrete solution, which for the manufactured
     data is the interpolant of |x|^2; the residual norms fall quadratically in the last steps."""
     from paper_1812_08075_b200 import solve
     w = synth.nlreac(k, (3, 4, 3))
     op = _op(w)
-    res = solve.newton(op, w.ndofs, rtol=1e-12)
+    res = solve.newton(op, w.ndofs, rtol=1e-12, graph=graph)
     assert res.converged, res.residual_norms
     exact = _interp(w, lambda a, b, c: a * a + b * b + c * c)
     err = np.abs(res.x.cpu().numpy() - exact).max()
