@@ -331,8 +331,7 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
 }
 
 // ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
-// n = 5: one warp per cell (k_quadw, measured faster) unless WARP = false; n <= 4 (too few lines per warp
-// phase) and n >= 6 (per-cell buffers beyond a warp's share of shared memory): k_quad
+// (WARP = true and n = 5: the warp-per-cell k_quadw, selected by DG_QUAD_WARP)
 template <int N, bool AFF, bool COEF, int PR = 0, bool WARP = true>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                         double* r, long long c0, long long c1, cudaStream_t st, const double* u0)
@@ -785,7 +784,9 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         case 8: fill_qtab<8>(H, Hm, c->qtab); break;
         }
         cudaError_t e = cudaSuccess;
-        const bool cta = getenv("DG_QUAD_CTA") != nullptr; // experiments / tests: the CTA-synchronous k_quad
+        // k_quad (per-cell thread groups) is the default; DG_QUAD_WARP selects the warp-per-cell k_quadw for
+        // n = 5 (tests compare the two; measured slower since k_quad's cells progress independently)
+        const bool cta = getenv("DG_QUAD_WARP") == nullptr;
         const int pr = mesh->problem == DG_PROBLEM_DIFFREAC ? 1 : (mesh->problem == DG_PROBLEM_NLREAC ? 2 : 0);
         c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr, cta);
         if (e == cudaSuccess && pr == 2) c->launch_jac = pick_quad(n, false, false, &e, 3, true);

@@ -84,8 +84,12 @@ struct Sw2 {
 
 template <int N, int M, bool U0 = false>
 struct QLay {
-    static constexpr int CPB = (N <= 5) ? 2 : 1;
     static constexpr int NT = 256;
+    // thread groups: each group of GT threads owns one cell and synchronises with a named barrier of its own,
+    // so the cells of a CTA progress independently (n <= 4: 4 groups of 64; n = 5: 2 of 128; else 1 of 256)
+    // (with the extra u0 buffer of the Jacobian action 4 cells of n = 4 exceed half the shared memory: 2 of 128)
+    static constexpr int GT = N <= 4 ? (U0 && N == 4 ? 128 : 64) : (N == 5 ? 128 : 256);
+    static constexpr int CPB = NT / GT;
     static constexpr int N2 = N * N, N3 = N * N * N, M2 = M * M, M3 = M * M * M, NM = N * M;
     // per cell (doubles)
     static constexpr int X = 0, R = X + N3, Y2 = R + N3, Y2d = Y2 + N2 * M, Z = Y2d + N2 * M, Zd1 = Z + N * M2,
@@ -131,7 +135,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
 {
     constexpr bool DR = PR != 0;
     using L = qd::QLay<N, M, PR == 3>;
-    constexpr int CPB = L::CPB, NT = L::NT, N2 = L::N2, N3 = L::N3, M2 = L::M2, M3 = L::M3, NM = L::NM;
+    constexpr int CPB = L::CPB, NT = L::NT, GT = L::GT, N2 = L::N2, N3 = L::N3, M2 = L::M2, M3 = L::M3, NM = L::NM;
     const MeshArgs& Ms = M_;
     extern __shared__ __align__(16) double sm[];
     double* const sA = sm + L::TAB;
@@ -143,38 +147,45 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     double* const sd0 = se1 + N;
     double* const sd1 = sd0 + N;
     const int tid = threadIdx.x;
-    const long long cfirst = c_begin + (long long)blockIdx.x * CPB;
-    const int ncell = (int)min((long long)CPB, c_end - cfirst);
-    auto cellp = [&](int c) { return sm + c * L::CELLP; };
+    const int grp = tid / GT, gtid = tid - grp * GT; // this thread's group (= its cell in the CTA)
+    const long long cfirst = c_begin + (long long)blockIdx.x * CPB + grp;
+    const int ncell = cfirst < c_end ? 1 : 0;        // cells of the group
+    auto cellp = [&](int c) { return sm + (grp + c) * L::CELLP; };
+    // group barrier (named barrier 1 + grp over the group's GT threads; the CTA barrier when one group)
+    auto gsync = [&]() {
+        if constexpr (GT == NT) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GT) : "memory");
+    };
     auto facep = [&](int c, int f) { return cellp(c) + L::F + f * L::FACE; };
 
     for (int i = tid; i < M * N; i += NT) { sA[i] = T.A[i]; sDq[i] = T.Dq[i]; }
     for (int i = tid; i < M; i += NT) { sw[i] = T.wq[i]; sxq[i] = T.xq[i]; }
     for (int i = tid; i < N; i += NT) { se0[i] = T.e0[i]; se1[i] = T.e1[i]; sd0[i] = T.d0[i]; sd1[i] = T.d1[i]; }
     for (int c = 0; c < ncell; ++c)
-        for (int i = tid; i < N3; i += NT) cellp(c)[L::X + i] = __ldg(x + (cfirst + c) * N3 + i);
+        for (int i = gtid; i < N3; i += GT) cellp(c)[L::X + i] = __ldg(x + (cfirst + c) * N3 + i);
     if (PR == 3) // the linearization point, into R (unused until stage 3)
         for (int c = 0; c < ncell; ++c)
-            for (int i = tid; i < N3; i += NT) cellp(c)[L::R + i] = __ldg(u0 + (cfirst + c) * N3 + i);
+            for (int i = gtid; i < N3; i += GT) cellp(c)[L::R + i] = __ldg(u0 + (cfirst + c) * N3 + i);
 
     // cell coordinates, computed once per cell (32-bit: a slab has < 2^31 cells)
     __shared__ int s_co[CPB][5]; // lp, rem, i0, i1, i2
-    if (tid < ncell) {
-        const int lc = (int)(cfirst + tid);
+    if (gtid == 0 && ncell) {
+        const int lc = (int)cfirst;
         const int lp = lc / Ms.plane_cells, rem = lc - lp * Ms.plane_cells;
-        s_co[tid][0] = lp;
-        s_co[tid][1] = rem;
-        s_co[tid][2] = (Ms.plane_begin + lp) % Ms.N0;
-        s_co[tid][3] = rem / Ms.N2;
-        s_co[tid][4] = rem - (rem / Ms.N2) * Ms.N2;
+        s_co[grp][0] = lp;
+        s_co[grp][1] = rem;
+        s_co[grp][2] = (Ms.plane_begin + lp) % Ms.N0;
+        s_co[grp][3] = rem / Ms.N2;
+        s_co[grp][4] = rem - (rem / Ms.N2) * Ms.N2;
     }
-    __syncthreads();
+    __syncthreads(); // (tables are shared by the groups; from here on each group syncs on its own)
+    if (!ncell) return;
     auto coords = [&](int c, int& lp, int& rem, int ig[3]) {
-        lp = s_co[c][0];
-        rem = s_co[c][1];
-        ig[0] = s_co[c][2];
-        ig[1] = s_co[c][3];
-        ig[2] = s_co[c][4];
+        lp = s_co[grp + c][0];
+        rem = s_co[grp + c][1];
+        ig[0] = s_co[grp + c][2];
+        ig[1] = s_co[grp + c][3];
+        ig[2] = s_co[grp + c][4];
     };
     auto jac_of = [&](int lp, int rem, double* J) {
         const double* jp = Ms.jac + ((long long)(lp + 1) * Ms.plane_cells + rem) * 9;
@@ -193,7 +204,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     };
 
     // ---------------- P0: geometry (one thread per cell for the volume, per (cell, face) for the faces) --------
-    for (int t = tid; t < ncell * 7; t += NT) {
+    for (int t = gtid; t < ncell * 7; t += GT) {
         const int c = t / 7, f = t % 7;
         int lp, rem, ig[3];
         coords(c, lp, rem, ig);
@@ -261,31 +272,31 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         const int Nd = d == 0 ? Ms.N0 : (d == 1 ? Ms.N1 : Ms.N2);
         fg[15] = (DR && (side ? ig[d] == Nd - 1 : ig[d] == 0)) ? 1.0 : 0.0;
     }
-    __syncthreads();
+    gsync();
 
     // ---------------- P0b (Jacobian): u0 at the M^3 points, U0Q = A0 A1 A2 u0 ----------------
     if (PR == 3) {
         using S2 = qd::Sw3<N, N, N, 2, M, false, false>;
-        for (int t = tid; t < ncell * S2::NL; t += NT) { double* b = cellp(t / S2::NL); S2::line(b + L::R, b + L::Y2, T.A, t % S2::NL); }
-        __syncthreads();
+        for (int t = gtid; t < ncell * S2::NL; t += GT) { double* b = cellp(t / S2::NL); S2::line(b + L::R, b + L::Y2, T.A, t % S2::NL); }
+        gsync();
         using S1 = qd::Sw3<N, N, M, 1, M, false, false>;
-        for (int t = tid; t < ncell * S1::NL; t += NT) { double* b = cellp(t / S1::NL); S1::line(b + L::Y2, b + L::Z, T.A, t % S1::NL); }
-        __syncthreads();
+        for (int t = gtid; t < ncell * S1::NL; t += GT) { double* b = cellp(t / S1::NL); S1::line(b + L::Y2, b + L::Z, T.A, t % S1::NL); }
+        gsync();
         using S0 = qd::Sw3<N, M, M, 0, M, false, false>;
-        for (int t = tid; t < ncell * S0::NL; t += NT) { double* b = cellp(t / S0::NL); S0::line(b + L::Z, b + L::U0Q, T.A, t % S0::NL); }
-        __syncthreads();
+        for (int t = gtid; t < ncell * S0::NL; t += GT) { double* b = cellp(t / S0::NL); S0::line(b + L::Z, b + L::U0Q, T.A, t % S0::NL); }
+        gsync();
     }
 
     // ---------------- P1: stage 1a (along j2); face traces along the normal (own from smem, neighbour from L2) ----
     {
         using S = qd::Sw3<N, N, N, 2, M, false, false>;
-        for (int t = tid; t < ncell * 2 * S::NL; t += NT) {
+        for (int t = gtid; t < ncell * 2 * S::NL; t += GT) {
             const int c = t / (2 * S::NL), k = (t / S::NL) % 2, l = t % S::NL;
             double* b = cellp(c);
             if (k) S::line(b + L::X, b + L::Y2d, T.Dq, l);
             else S::line(b + L::X, b + L::Y2, T.A, l);
         }
-        for (int t = tid; t < ncell * 6 * N2; t += NT) {
+        for (int t = gtid; t < ncell * 6 * N2; t += GT) {
             const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
             const int d = f >> 1, side = f & 1;
             int lp, rem, ig[3];
@@ -314,11 +325,11 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             FT[3 * N2 + p] = gn;
         }
     }
-    __syncthreads();
+    gsync();
     // ---------------- P2: stage 1b (along j1); face contraction along t1 ----------------
     {
         using SA = qd::Sw3<N, N, M, 1, M, false, false>;
-        for (int t = tid; t < ncell * 3 * SA::NL; t += NT) {
+        for (int t = gtid; t < ncell * 3 * SA::NL; t += GT) {
             const int c = t / (3 * SA::NL), k = (t / SA::NL) % 3, l = t % SA::NL;
             double* b = cellp(c);
             if (k == 0) SA::line(b + L::Y2, b + L::Z, T.A, l);
@@ -326,7 +337,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else SA::line(b + L::Y2d, b + L::Zd2, T.A, l);
         }
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
-        for (int t = tid; t < ncell * 6 * 6 * F::NL; t += NT) {
+        for (int t = gtid; t < ncell * 6 * 6 * F::NL; t += GT) {
             const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
             double* FT = facep(c, f);
             double* F1 = FT + 4 * N2;
@@ -336,12 +347,12 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else F::line(src, F1 + k * NM, T.A, l);
         }
     }
-    __syncthreads();
+    gsync();
     // ---------------- P3: stage 1c (along j0); face contraction along t2 ----------------
     {
         using SB = qd::Sw3<N, M, M, 0, M, false, false>;
         constexpr int NQ = DR ? 4 : 3;
-        for (int t = tid; t < ncell * NQ * SB::NL; t += NT) {
+        for (int t = gtid; t < ncell * NQ * SB::NL; t += GT) {
             const int c = t / (NQ * SB::NL), k = (t / SB::NL) % NQ, l = t % SB::NL;
             double* b = cellp(c);
             if (k == 0) SB::line(b + L::Z, b + L::G0, T.Dq, l);
@@ -350,7 +361,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else SB::line(b + L::Z, b + L::GU, T.A, l); // u = A0 A1 A2 X
         }
         using F = qd::Sw2<M, N, 1, M, false, false>; // M x N -> M x M
-        for (int t = tid; t < ncell * 6 * 8 * F::NL; t += NT) {
+        for (int t = gtid; t < ncell * 6 * 8 * F::NL; t += GT) {
             const int c = t / (48 * F::NL), f = (t / (8 * F::NL)) % 6, k = (t / F::NL) % 8, l = t % F::NL;
             double* F1 = facep(c, f) + 4 * N2;
             double* F2 = F1 + 6 * NM;
@@ -361,9 +372,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else F::line(src, F2 + k * M2, T.A, l);
         }
     }
-    __syncthreads();
+    gsync();
     // ---------------- P4: stage 2 (pointwise at the M^3 points); face fluxes at the M^2 points ----------------
-    for (int t = tid; t < ncell * M3; t += NT) {
+    for (int t = gtid; t < ncell * M3; t += GT) {
         const int c = t / M3, P = t % M3, q0 = P % M, q1 = (P / M) % M, q2 = P / M2;
         double* b = cellp(c);
         const double* g = b + L::GEO;
@@ -402,7 +413,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         b[L::G1 + P] = cW * fma(g[3], a0, fma(g[1], a1, g[5] * a2));
         b[L::G2 + P] = cW * fma(g[4], a0, fma(g[5], a1, g[2] * a2));
     }
-    for (int t = tid; t < ncell * 6 * M2; t += NT) {
+    for (int t = gtid; t < ncell * 6 * M2; t += GT) {
         const int c = t / (6 * M2), f = (t / M2) % 6, p = t % M2, a = p % M, bq = p / M;
         const int d = f >> 1, side = f & 1;
         const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
@@ -477,11 +488,11 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         F2[2 * M2 + p] = ao[t2] * Cg;
         F2[3 * M2 + p] = ao[d] * Cg;        // normal-gradient coefficient
     }
-    __syncthreads();
+    gsync();
     // ---------------- P5: stage 3a (D0^T / A0^T along j0); face back-projection along t2 ----------------
     {
         using SB = qd::Sw3<M, M, M, 0, N, true, false>; // M^3 -> N x M x M
-        for (int t = tid; t < ncell * 3 * SB::NL; t += NT) {
+        for (int t = gtid; t < ncell * 3 * SB::NL; t += GT) {
             const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
             if (k == 0) {
@@ -494,7 +505,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // Pv = A^T_t2 Cv + D^T_t2 Ct2, Pt = A^T_t2 Ct1, Pn = A^T_t2 Cn   ([t1 = M][t2 = N])
         using F = qd::Sw2<M, M, 1, N, true, false>;
         using FA = qd::Sw2<M, M, 1, N, true, true>;
-        for (int t = tid; t < ncell * 6 * 3 * F::NL; t += NT) {
+        for (int t = gtid; t < ncell * 6 * 3 * F::NL; t += GT) {
             const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
             double* F1 = facep(c, f) + 4 * N2;
             const double* C = F1 + 6 * NM;
@@ -503,12 +514,12 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else F::line(C + 3 * M2, F1 + 2 * NM, T.A, l);
         }
     }
-    __syncthreads();
+    gsync();
     // ---------------- P6: stage 3b (along j1); face back-projection along t1 ----------------
     {
         using SA = qd::Sw3<N, M, M, 1, N, true, false>;  // N x M x M -> N x N x M
         using SAa = qd::Sw3<N, M, M, 1, N, true, true>;
-        for (int t = tid; t < ncell * 2 * SA::NL; t += NT) {
+        for (int t = gtid; t < ncell * 2 * SA::NL; t += GT) {
             const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
             double* b = cellp(c);
             if (k == 0) { SA::line(b + L::Z, b + L::Y2, T.A, l); SAa::line(b + L::Zd1, b + L::Y2, T.Dq, l); } // Ya
@@ -517,7 +528,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // V2 = A^T_t1 Pv + D^T_t1 Pt, G2 = A^T_t1 Pn   ([t1 = N][t2 = N], into FT)
         using F = qd::Sw2<M, N, 0, N, true, false>;
         using FA = qd::Sw2<M, N, 0, N, true, true>;
-        for (int t = tid; t < ncell * 6 * 2 * F::NL; t += NT) {
+        for (int t = gtid; t < ncell * 6 * 2 * F::NL; t += GT) {
             const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
             double* FT = facep(c, f);
             const double* P = FT + 4 * N2;
@@ -525,21 +536,21 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else F::line(P + 2 * NM, FT + N2, T.A, l);
         }
     }
-    __syncthreads();
+    gsync();
     // ---------------- P7: stage 3c (along j2) into R ----------------
     {
         using S = qd::Sw3<N, N, M, 2, N, true, false>;
         using Sa = qd::Sw3<N, N, M, 2, N, true, true>;
-        for (int t = tid; t < ncell * S::NL; t += NT) {
+        for (int t = gtid; t < ncell * S::NL; t += GT) {
             const int c = t / S::NL, l = t % S::NL;
             double* b = cellp(c);
             S::line(b + L::Y2, b + L::R, T.A, l);
             Sa::line(b + L::Y2d, b + L::R, T.Dq, l);
         }
     }
-    __syncthreads();
+    gsync();
     // ---------------- P8: add the face back-projections along the normals, write r once ----------------
-    for (int t = tid; t < ncell * N3; t += NT) {
+    for (int t = gtid; t < ncell * N3; t += GT) {
         const int c = t / N3, P = t % N3;
         const int j[3] = {P % N, (P / N) % N, P / N2};
         double v = cellp(c)[L::R + P];

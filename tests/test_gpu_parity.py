@@ -320,13 +320,13 @@ def test_quad_overintegration(k, geom, coeff):
     N = (3, 2, 5) if k >= 5 else (3, 3, 5)
     w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=500 + k, quad=k + 2)
     op = _op(w)
-    assert op.kernel_name == ("k_quadw" if k == 4 else "k_quad")
+    assert op.kernel_name == "k_quad"
     op.close()
     assert _full_check(w) <= TOL
 
 
 @pytest.mark.parametrize("k", [2, 4])
-def test_quad_equals_collocation_for_polynomial_integrands(k):  # k = 4: k_quadw, k = 2: k_quad
+def test_quad_equals_collocation_for_polynomial_integrands(k):
     """With c = 1 both rules integrate exactly: the k+2-point operator (k_quad) equals the collocated
     one (k_gen) to rounding on an affine mesh."""
     w1 = synth.small(k, (4, 4, 4), geom_kind=1, coeff_kind=0, seed=77)
@@ -400,7 +400,7 @@ def test_diffreac_parity(k):
     N = (3, 4, 5) if k <= 4 else (2, 3, 3)
     w = synth.diffreac(k, N, quad=k + 2)
     op = _dr_op(w)
-    assert op.kernel_name == ("k_quadw_diffreac" if k == 4 else "k_quad_diffreac")
+    assert op.kernel_name == "k_quad_diffreac"
     x = synth.x_torch(w, device="cuda")
     r = op.apply(x)
     torch.cuda.synchronize()
@@ -513,7 +513,7 @@ def test_cg_graph_matches_cg():
 
 @pytest.mark.parametrize("k,geom,coeff,dr", [(4, 1, 1, False), (4, 0, 1, False), (4, 0, 0, True)])
 def test_quad_warp_matches_cta_kernel(k, geom, coeff, dr, monkeypatch):
-    """k_quadw (one warp per cell) against k_quad (the CTA-synchronous formulation) on the same inputs."""
+    """k_quadw (one warp per cell, DG_QUAD_WARP) against k_quad (per-cell thread groups, the default) on the same inputs."""
     if dr:
         w = synth.diffreac(k, (3, 4, 3), quad=k + 2)
         mk = lambda: _dr_op(w)
@@ -521,10 +521,10 @@ def test_quad_warp_matches_cta_kernel(k, geom, coeff, dr, monkeypatch):
         w = synth.small(k, (3, 4, 3), geom_kind=geom, coeff_kind=coeff, seed=600 + k, quad=k + 2)
         mk = lambda: _op(w)
     x = synth.x_torch(w, device="cuda")
+    monkeypatch.setenv("DG_QUAD_WARP", "1")
     a = mk()
-    monkeypatch.setenv("DG_QUAD_CTA", "1")
+    monkeypatch.delenv("DG_QUAD_WARP")
     b = mk()
-    monkeypatch.delenv("DG_QUAD_CTA")
     assert a.kernel_name.startswith("k_quadw") and not b.kernel_name.startswith("k_quadw")
     ra, rb = a.apply(x), b.apply(x)
     assert (ra - rb).abs().max().item() <= 1e-13 * rb.abs().max().item()
