@@ -100,7 +100,8 @@ struct QLay {
     static constexpr int FACE = 4 * N2 + 6 * NM + 8 * M2;
     static constexpr int GU = G2 + M3;      // u at the M^3 points (diffusion-reaction: reaction / source terms)
     static constexpr int U0Q = GU + M3;     // U0: the linearization point u0 at the M^3 points (Jacobian action)
-    static constexpr int F = U0Q + (U0 ? M3 : 0);
+    static constexpr int T2U = U0Q + (U0 ? M3 : 0); // U0: u0 after the j2 and j1 sweeps [N][M][M]
+    static constexpr int F = T2U + (U0 ? N * M2 : 0);
     static constexpr int GEO = F + 6 * FACE; // per cell: Gt[6], J rows 0-1 [6], o[2]; per face 16: dS, a-[3], a+[3], Jm rows 0-1 [6], om[2], pad
     static constexpr int CELL = GEO + 14 + 6 * 16;
     static constexpr int CELLP = (CELL + 1) / 2 * 2;
@@ -274,18 +275,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     }
     gsync();
 
-    // ---------------- P0b (Jacobian): u0 at the M^3 points, U0Q = A0 A1 A2 u0 ----------------
-    if (PR == 3) {
-        using S2 = qd::Sw3<N, N, N, 2, M, false, false>;
-        for (int t = gtid; t < ncell * S2::NL; t += GT) { double* b = cellp(t / S2::NL); S2::line(b + L::R, b + L::Y2, T.A, t % S2::NL); }
-        gsync();
-        using S1 = qd::Sw3<N, N, M, 1, M, false, false>;
-        for (int t = gtid; t < ncell * S1::NL; t += GT) { double* b = cellp(t / S1::NL); S1::line(b + L::Y2, b + L::Z, T.A, t % S1::NL); }
-        gsync();
-        using S0 = qd::Sw3<N, M, M, 0, M, false, false>;
-        for (int t = gtid; t < ncell * S0::NL; t += GT) { double* b = cellp(t / S0::NL); S0::line(b + L::Z, b + L::U0Q, T.A, t % S0::NL); }
-        gsync();
-    }
+    // (Jacobian: u0 at the M^3 points, U0Q = A0 A1 A2 u0, by three sweeps riding along with stage 1a-1c in
+    // P1-P3: R -> T1 (face 0's F2 area, free until P3) -> T2U -> U0Q)
+    auto u0_T1 = [&](int c) { return facep(c, 0) + 4 * N2 + 6 * NM; };
 
     // ---------------- P1: stage 1a (along j2); face traces along the normal (own from smem, neighbour from L2) ----
     {
@@ -296,6 +288,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             if (k) S::line(b + L::X, b + L::Y2d, T.Dq, l);
             else S::line(b + L::X, b + L::Y2, T.A, l);
         }
+        if (PR == 3)
+            for (int t = gtid; t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.A, t % S::NL);
         for (int t = gtid; t < ncell * 6 * N2; t += GT) {
             const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
             const int d = f >> 1, side = f & 1;
@@ -336,6 +330,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else if (k == 1) SA::line(b + L::Y2, b + L::Zd1, T.Dq, l);
             else SA::line(b + L::Y2d, b + L::Zd2, T.A, l);
         }
+        if (PR == 3)
+            for (int t = gtid; t < ncell * SA::NL; t += GT) SA::line(u0_T1(t / SA::NL), cellp(t / SA::NL) + L::T2U, T.A, t % SA::NL);
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
         for (int t = gtid; t < ncell * 6 * 6 * F::NL; t += GT) {
             const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
@@ -360,6 +356,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else if (k == 2) SB::line(b + L::Zd2, b + L::G2, T.A, l);
             else SB::line(b + L::Z, b + L::GU, T.A, l); // u = A0 A1 A2 X
         }
+        if (PR == 3)
+            for (int t = gtid; t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.A, t % SB::NL);
         using F = qd::Sw2<M, N, 1, M, false, false>; // M x N -> M x M
         for (int t = gtid; t < ncell * 6 * 8 * F::NL; t += GT) {
             const int c = t / (48 * F::NL), f = (t / (8 * F::NL)) % 6, k = (t / F::NL) % 8, l = t % F::NL;
