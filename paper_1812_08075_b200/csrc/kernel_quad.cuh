@@ -87,22 +87,24 @@ struct QLay {
     static constexpr int NT = 256;
     // thread groups: each group of GT threads owns one cell and synchronises with a named barrier of its own,
     // so the cells of a CTA progress independently (n <= 4: 4 groups of 64; n = 5: 2 of 128; else 1 of 256)
-    // (with the extra u0 buffer of the Jacobian action 4 cells of n = 4 exceed half the shared memory: 2 of 128)
-    static constexpr int GT = N <= 4 ? (U0 && N == 4 ? 128 : 64) : (N == 5 ? 128 : 256);
+    static constexpr int GT = N <= 4 ? 64 : (N == 5 ? 128 : 256);
     static constexpr int CPB = NT / GT;
     static constexpr int N2 = N * N, N3 = N * N * N, M2 = M * M, M3 = M * M * M, NM = N * M;
-    // per cell (doubles)
-    static constexpr int X = 0, R = X + N3, Y2 = R + N3, Y2d = Y2 + N2 * M, Z = Y2d + N2 * M, Zd1 = Z + N * M2,
-                         Zd2 = Zd1 + N * M2, G0 = Zd2 + N * M2, G1 = G0 + M3, G2 = G1 + M3;
-    // per face: FT [4][N2] (own u, own g, nb u, nb g) -> later FB2 [2][N2] (V2, G2)
-    //           F1 [6][NM] (own Ua1, Ud1, Ga1; nb Ua1, Ud1, Ga1) -> later FB1 [3][NM] (Pv, Pt, Pn)
-    //           F2 [8][M2] (U-, U+, Gn-, Gn+, Gt1-, Gt1+, Gt2-, Gt2+) -> coefficients [4][M2] (Cv, Ct1, Ct2, Cn)
-    static constexpr int FACE = 4 * N2 + 6 * NM + 8 * M2;
+    // per cell (doubles). Region A = X, R, Y2, Y2d and the face traces FT is dead from P3 to P5 and holds the
+    // face flux coefficients C of P4 -> P5 there (when they fit; n <= 3: a region of their own)
+    //   FT [face][4][N2] (own u, own g, nb u, nb g) -> later FB2 [2][N2] (V2, G2)
+    //   F1 [face][6][NM] (own Ua1, Ud1, Ga1; nb Ua1, Ud1, Ga1) -> later FB1 [3][NM] (Pv, Pt, Pn)
+    //   C  [face][4][M2] (Cv, Ct1, Ct2, Cn): the face values at the M^2 points are formed in P4 directly from F1
+    static constexpr int X = 0, R = X + N3, Y2 = R + N3, Y2d = Y2 + N2 * M, FT = Y2d + N2 * M;
+    static constexpr int AEND = FT + 6 * 4 * N2;
+    static constexpr bool CALIAS = 6 * 4 * M2 <= AEND;
+    static constexpr int Z = AEND, Zd1 = Z + N * M2, Zd2 = Zd1 + N * M2, G0 = Zd2 + N * M2, G1 = G0 + M3, G2 = G1 + M3;
     static constexpr int GU = G2 + M3;      // u at the M^3 points (diffusion-reaction: reaction / source terms)
     static constexpr int U0Q = GU + M3;     // U0: the linearization point u0 at the M^3 points (Jacobian action)
     static constexpr int T2U = U0Q + (U0 ? M3 : 0); // U0: u0 after the j2 and j1 sweeps [N][M][M]
-    static constexpr int F = T2U + (U0 ? N * M2 : 0);
-    static constexpr int GEO = F + 6 * FACE; // per cell: Gt[6], J rows 0-1 [6], o[2]; per face 16: dS, a-[3], a+[3], Jm rows 0-1 [6], om[2], pad
+    static constexpr int F1 = T2U + (U0 ? N * M2 : 0);
+    static constexpr int C = CALIAS ? X : F1 + 6 * 6 * NM;
+    static constexpr int GEO = F1 + 6 * 6 * NM + (CALIAS ? 0 : 6 * 4 * M2); // per cell: Gt[6], J rows 0-1 [6], o[2]; per face 16
     static constexpr int CELL = GEO + 14 + 6 * 16;
     static constexpr int CELLP = (CELL + 1) / 2 * 2;
     static constexpr int TAB = CPB * CELLP;   // shared tables: A, Dq (M N each), wq, xq (M), e0, e1, d0, d1 (N)
@@ -111,7 +113,8 @@ struct QLay {
     // resident CTAs per SM the shared memory allows (the register cap follows from it)
     // (at most 2 for n >= 6: their sweeps need ~128 registers; 85 spill heavily)
     static constexpr int MINB_SMEM = (BYTES + 2048) * 4 <= 228 * 1024 ? 4 : ((BYTES + 2048) * 3 <= 228 * 1024 ? 3 : ((BYTES + 2048) * 2 <= 228 * 1024 ? 2 : 1));
-    static constexpr int MINB = (N >= 6 && MINB_SMEM > 2) ? 2 : MINB_SMEM;
+    // (at most 3 otherwise: 4 would cap the registers at 64 and spill heavily)
+    static constexpr int MINB = (N >= 6 && MINB_SMEM > 2) ? 2 : (MINB_SMEM > 3 ? 3 : MINB_SMEM);
 };
 
 } // namespace qd
@@ -157,7 +160,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         if constexpr (GT == NT) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GT) : "memory");
     };
-    auto facep = [&](int c, int f) { return cellp(c) + L::F + f * L::FACE; };
+    auto ftp = [&](int c, int f) { return cellp(c) + L::FT + f * 4 * N2; };  // face traces / FB2
+    auto f1p = [&](int c, int f) { return cellp(c) + L::F1 + f * 6 * NM; };  // t1 contractions / FB1
+    auto cfp = [&](int c, int f) { return cellp(c) + L::C + f * 4 * M2; };   // flux coefficients
 
     for (int i = tid; i < M * N; i += NT) { sA[i] = T.A[i]; sDq[i] = T.Dq[i]; }
     for (int i = tid; i < M; i += NT) { sw[i] = T.wq[i]; sxq[i] = T.xq[i]; }
@@ -276,8 +281,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     gsync();
 
     // (Jacobian: u0 at the M^3 points, U0Q = A0 A1 A2 u0, by three sweeps riding along with stage 1a-1c in
-    // P1-P3: R -> T1 (face 0's F2 area, free until P3) -> T2U -> U0Q)
-    auto u0_T1 = [&](int c) { return facep(c, 0) + 4 * N2 + 6 * NM; };
+    // P1-P3: R -> T1 (the G0 area, free until P3) -> T2U -> U0Q)
+    auto u0_T1 = [&](int c) { return cellp(c) + L::G0; }; // (G0 is first written in P3)
 
     // ---------------- P1: stage 1a (along j2); face traces along the normal (own from smem, neighbour from L2) ----
     {
@@ -312,7 +317,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
                 un = fma(side ? se0[j] : se1[j], vn, un);
                 gn = fma(side ? sd0[j] : sd1[j], vn, gn);
             }
-            double* FT = facep(c, f);
+            double* FT = ftp(c, f);
             FT[p] = uo;
             FT[N2 + p] = go;
             FT[2 * N2 + p] = un;
@@ -335,8 +340,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
         for (int t = gtid; t < ncell * 6 * 6 * F::NL; t += GT) {
             const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
-            double* FT = facep(c, f);
-            double* F1 = FT + 4 * N2;
+            double* FT = ftp(c, f);
+            double* F1 = f1p(c, f);
             // k: 0 own Ua1 = A u, 1 own Ud1 = D u, 2 own Ga1 = A g, 3..5 the same for the neighbour
             const double* src = FT + ((k < 3) ? (k == 2 ? N2 : 0) : (k == 5 ? 3 * N2 : 2 * N2));
             if (k % 3 == 1) F::line(src, F1 + k * NM, T.Dq, l);
@@ -358,17 +363,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         }
         if (PR == 3)
             for (int t = gtid; t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.A, t % SB::NL);
-        using F = qd::Sw2<M, N, 1, M, false, false>; // M x N -> M x M
-        for (int t = gtid; t < ncell * 6 * 8 * F::NL; t += GT) {
-            const int c = t / (48 * F::NL), f = (t / (8 * F::NL)) % 6, k = (t / F::NL) % 8, l = t % F::NL;
-            double* F1 = facep(c, f) + 4 * N2;
-            double* F2 = F1 + 6 * NM;
-            // outputs (side s = 0 own, 1 neighbour): U_s = A Ua1_s, Gn_s = A Ga1_s, Gt1_s = A Ud1_s, Gt2_s = D Ua1_s
-            const int s = k & 1, q = k >> 1; // q: 0 U, 1 Gn, 2 Gt1, 3 Gt2
-            const double* src = F1 + (3 * s + (q == 0 || q == 3 ? 0 : (q == 1 ? 2 : 1))) * NM;
-            if (q == 3) F::line(src, F2 + k * M2, T.Dq, l);
-            else F::line(src, F2 + k * M2, T.A, l);
-        }
+        // (the face values at the M^2 points are formed pointwise in P4 from F1: no stored [8][M^2] array)
     }
     gsync();
     // ---------------- P4: stage 2 (pointwise at the M^3 points); face fluxes at the M^2 points ----------------
@@ -415,11 +410,28 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         const int c = t / (6 * M2), f = (t / M2) % 6, p = t % M2, a = p % M, bq = p / M;
         const int d = f >> 1, side = f & 1;
         const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
-        double* F2 = facep(c, f) + 4 * N2 + 6 * NM;
+        double* F2 = cfp(c, f); // coefficients out
         const double* fg = cellp(c) + L::GEO + 14 + 16 * f;
-        // own (s=0) and neighbour (s=1) -> T- / T+
-        const double Uo = F2[0 * M2 + p], Un = F2[1 * M2 + p], Gno = F2[2 * M2 + p], Gnn = F2[3 * M2 + p];
-        const double T1o = F2[4 * M2 + p], T1n = F2[5 * M2 + p], T2o = F2[6 * M2 + p], T2n = F2[7 * M2 + p];
+        // own (s=0) and neighbour (s=1) -> T- / T+: the t2 contractions of F1 at the point (a, bq):
+        // U_s = A Ua1_s, Gn_s = A Ga1_s, Gt1_s = A Ud1_s, Gt2_s = D Ua1_s
+        double Uo = 0, Un = 0, Gno = 0, Gnn = 0, T1o = 0, T1n = 0, T2o = 0, T2n = 0;
+        {
+            const double* F1 = f1p(c, f) + a;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double Aj = sA[bq * N + j], Dj = sDq[bq * N + j];
+                const double ua0 = F1[0 * NM + M * j], ud0 = F1[1 * NM + M * j], ga0 = F1[2 * NM + M * j];
+                const double ua1 = F1[3 * NM + M * j], ud1 = F1[4 * NM + M * j], ga1 = F1[5 * NM + M * j];
+                Uo = fma(Aj, ua0, Uo);
+                Un = fma(Aj, ua1, Un);
+                Gno = fma(Aj, ga0, Gno);
+                Gnn = fma(Aj, ga1, Gnn);
+                T1o = fma(Aj, ud0, T1o);
+                T1n = fma(Aj, ud1, T1n);
+                T2o = fma(Dj, ua0, T2o);
+                T2n = fma(Dj, ua1, T2n);
+            }
+        }
         const double um = side ? Uo : Un, up = side ? Un : Uo;
         const double gnm = side ? Gno : Gnn, gnp = side ? Gnn : Gno;
         const double t1m = side ? T1o : T1n, t1p = side ? T1n : T1o;
@@ -505,8 +517,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         using FA = qd::Sw2<M, M, 1, N, true, true>;
         for (int t = gtid; t < ncell * 6 * 3 * F::NL; t += GT) {
             const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
-            double* F1 = facep(c, f) + 4 * N2;
-            const double* C = F1 + 6 * NM;
+            double* F1 = f1p(c, f);
+            const double* C = cfp(c, f);
             if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, T.A, l); FA::line(C + 2 * M2, F1 + 0 * NM, T.Dq, l); }
             else if (k == 1) F::line(C + 1 * M2, F1 + 1 * NM, T.A, l);
             else F::line(C + 3 * M2, F1 + 2 * NM, T.A, l);
@@ -528,8 +540,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         using FA = qd::Sw2<M, N, 0, N, true, true>;
         for (int t = gtid; t < ncell * 6 * 2 * F::NL; t += GT) {
             const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
-            double* FT = facep(c, f);
-            const double* P = FT + 4 * N2;
+            double* FT = ftp(c, f);
+            const double* P = f1p(c, f);
             if (k == 0) { F::line(P + 0 * NM, FT, T.A, l); FA::line(P + 1 * NM, FT, T.Dq, l); }
             else F::line(P + 2 * NM, FT + N2, T.A, l);
         }
@@ -558,7 +570,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int p = j[t1] + N * j[t2];
 #pragma unroll
             for (int side = 0; side < 2; ++side) {
-                const double* FT = facep(c, 2 * d + side);
+                const double* FT = ftp(c, 2 * d + side);
                 const double e = side ? se1[j[d]] : se0[j[d]], dd = side ? sd1[j[d]] : sd0[j[d]];
                 v = fma(e, FT[p], fma(dd, FT[N2 + p], v));
             }
