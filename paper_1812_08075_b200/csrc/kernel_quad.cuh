@@ -86,8 +86,8 @@ template <int N, int M, bool U0 = false>
 struct QLay {
     static constexpr int NT = 256;
     // thread groups: each group of GT threads owns one cell and synchronises with a named barrier of its own,
-    // so the cells of a CTA progress independently (n <= 4: 4 groups of 64; n = 5: 2 of 128; else 1 of 256)
-    static constexpr int GT = N <= 4 ? 64 : (N == 5 ? 128 : 256);
+    // so the cells of a CTA progress independently (n <= 4: 4 groups of 64; n = 5, 6: 2 of 128; else 1 of 256)
+    static constexpr int GT = N <= 4 ? 64 : (N <= 6 ? 128 : 256);
     static constexpr int CPB = NT / GT;
     static constexpr int N2 = N * N, N3 = N * N * N, M2 = M * M, M3 = M * M * M, NM = N * M;
     // per cell (doubles). Region A = X, R, Y2, Y2d and the face traces FT is dead from P3 to P5 and holds the
