@@ -38,8 +38,9 @@ struct SLay {
     static constexpr int NP = N - 1;
     static constexpr int N2 = N * N, N3 = N * N * N, NP2 = NP * NP, NP3 = NP * NP * NP;
     static constexpr int B = 3 * N3 + NP3; // DOFs per cell: [u_0 | u_1 | u_2 | p]
-    // n <= 3: one round of the 9 n^2 gradient lines (measured: k = 2 1.52 -> 1.26 ms); n = 4: 128; else 256
-    static constexpr int NT = N <= 3 ? (9 * N * N + 31) / 32 * 32 : (N == 4 ? 128 : 256);
+    // n <= 3: one round of the 9 n^2 gradient lines (measured: k = 2 1.52 -> 1.26 ms); n = 4, 5: 128 (k = 4:
+    // 1.24 -> 1.11 ms on 40^3); else 256
+    static constexpr int NT = N <= 3 ? (9 * N * N + 31) / 32 * 32 : (N <= 5 ? 128 : 256);
     // per-cell shared buffers (doubles)
     static constexpr int U = 0;            // velocity (3 N3), later the velocity residual RU
     static constexpr int PR = U + 3 * N3;  // pressure (NP3), later the pressure residual RP
