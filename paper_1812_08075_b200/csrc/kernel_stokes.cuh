@@ -107,6 +107,22 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     __syncthreads();
 
     // ---------------- P1: gradients (9 D sweeps), pressure A_p along j2, face traces ----------------
+    // the neighbours' values for this thread's face-trace tasks are loaded first (from L2) and consumed after
+    // the gradient sweeps, so their latency hides behind the sweeps instead of stalling the P1 barrier
+    // (n <= 5; for larger n the register cost outweighs it)
+    constexpr bool PREF = N <= 5;
+    constexpr int NFT = PREF ? (18 * N2 + NT - 1) / NT : 1; // face-trace tasks per thread (at most)
+    double vnb[NFT][N];
+#pragma unroll
+    for (int k = 0; k < NFT; ++k) {
+        const int t = tid + k * NT;
+        if (PREF && t < 18 * N2) {
+            const int f = t / (3 * N2), c = (t / N2) % 3, p = t % N2, a = p % N, bq = p / N;
+            const double* nb = nbp(f);
+#pragma unroll
+            for (int j = 0; j < N; ++j) vnb[k][j] = nb ? __ldg(nb + c * N3 + pidx<N>(f >> 1, j, a, bq)) : 0.0;
+        }
+    }
     for (int t = tid; t < 9 * N2; t += NT) {
         const int ce = t / N2, l = t % N2, c = ce / 3, e = ce % 3;
         const double* in = U + c * N3;
@@ -116,10 +132,14 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.D, l);
     }
     for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, NP, 2, N, false, false>::line(PR, TA, T.AP, t);
-    for (int t = tid; t < 18 * N2; t += NT) {
+    constexpr int NFL = PREF ? NFT : (18 * N2 + NT - 1) / NT;
+#pragma unroll
+    for (int k = 0; k < NFL; ++k) {
+        const int t = tid + k * NT;
+        if (t >= 18 * N2) break;
         const int f = t / (3 * N2), c = (t / N2) % 3, p = t % N2, a = p % N, bq = p / N;
         const int d = f >> 1, side = f & 1;
-        const double* nb = nbp(f);
+        const double* nb = PREF ? nullptr : nbp(f);
         const double* es = side ? T.e1 : T.e0;
         const double* ds = side ? T.d1 : T.d0;
         const double* en = side ? T.e0 : T.e1;
@@ -127,15 +147,12 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         double uo = 0, go = 0, un = 0, gn = 0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            const int P = pidx<N>(d, j, a, bq);
-            const double vo = U[c * N3 + P];
+            const double vo = U[c * N3 + pidx<N>(d, j, a, bq)];
             uo = fma(es[j], vo, uo);
             go = fma(ds[j], vo, go);
-            if (nb) {
-                const double vn = __ldg(nb + c * N3 + P);
-                un = fma(en[j], vn, un);
-                gn = fma(dn[j], vn, gn);
-            }
+            const double vn = PREF ? vnb[k][j] : (nb ? __ldg(nb + c * N3 + pidx<N>(d, j, a, bq)) : 0.0);
+            un = fma(en[j], vn, un); // (zero on the boundary of the cube)
+            gn = fma(dn[j], vn, gn);
         }
         double* TR = face(f) + L::TR + c * 4 * N2;
         TR[p] = uo;
