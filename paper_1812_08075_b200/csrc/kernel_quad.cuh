@@ -286,6 +286,33 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
 
     // ---------------- P1: stage 1a (along j2); face traces along the normal (own from smem, neighbour from L2) ----
     {
+        // the neighbour values of this thread's trace tasks are loaded before the stage-1a sweeps and consumed
+        // after them (L2 latency behind the sweeps; n <= 5, where the registers allow it)
+        constexpr bool PREF = N <= 5;
+        constexpr int NFT = PREF ? (6 * N2 + GT - 1) / GT : 1;
+        double vnb[NFT][N];
+        auto nb_of = [&](int c, int f) -> const double* {
+            const int d = f >> 1, side = f & 1;
+            int lp, rem, ig[3];
+            coords(c, lp, rem, ig);
+            int nlp, nrem, nig[3];
+            neighbour(lp, rem, ig, d, side, nlp, nrem, nig);
+            if (d == 0) return nlp < 0 ? xb + (long long)rem * N3 : (nlp >= Ms.L ? xa + (long long)rem * N3 : x + ((long long)nlp * Ms.plane_cells + rem) * N3);
+            return x + ((long long)lp * Ms.plane_cells + nrem) * N3;
+        };
+        if constexpr (PREF) {
+#pragma unroll
+            for (int k = 0; k < NFT; ++k) {
+                const int t = gtid + k * GT;
+                if (t < ncell * 6 * N2) {
+                    const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
+                    const bool bnd = DR && cellp(c)[L::GEO + 14 + 16 * f + 15] != 0.0;
+                    const double* nbx = nb_of(c, f);
+#pragma unroll
+                    for (int j = 0; j < N; ++j) vnb[k][j] = bnd ? 0.0 : __ldg(nbx + pidx<N>(f >> 1, j, a, bq));
+                }
+            }
+        }
         using S = qd::Sw3<N, N, N, 2, M, false, false>;
         for (int t = gtid; t < ncell * 2 * S::NL; t += GT) {
             const int c = t / (2 * S::NL), k = (t / S::NL) % 2, l = t % S::NL;
@@ -295,23 +322,21 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         }
         if (PR == 3)
             for (int t = gtid; t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.A, t % S::NL);
-        for (int t = gtid; t < ncell * 6 * N2; t += GT) {
+        constexpr int NFL = PREF ? NFT : (6 * N2 + GT - 1) / GT;
+#pragma unroll
+        for (int k = 0; k < NFL; ++k) {
+            const int t = gtid + k * GT;
+            if (t >= ncell * 6 * N2) break;
             const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
             const int d = f >> 1, side = f & 1;
-            int lp, rem, ig[3];
-            coords(c, lp, rem, ig);
-            int nlp, nrem, nig[3];
-            neighbour(lp, rem, ig, d, side, nlp, nrem, nig);
-            const double* nbx;
-            if (d == 0) nbx = nlp < 0 ? xb + (long long)rem * N3 : (nlp >= Ms.L ? xa + (long long)rem * N3 : x + ((long long)nlp * Ms.plane_cells + rem) * N3);
-            else nbx = x + ((long long)lp * Ms.plane_cells + nrem) * N3;
+            const double* nbx = PREF ? nullptr : nb_of(c, f);
             const double* xo = cellp(c) + L::X;
             const bool bnd = DR && cellp(c)[L::GEO + 14 + 16 * f + 15] != 0.0;
             double uo = 0, go = 0, un = 0, gn = 0;
 #pragma unroll
             for (int j = 0; j < N; ++j) {
                 const double vo = xo[pidx<N>(d, j, a, bq)];
-                const double vn = bnd ? 0.0 : __ldg(nbx + pidx<N>(d, j, a, bq));
+                const double vn = PREF ? vnb[k][j] : (bnd ? 0.0 : __ldg(nbx + pidx<N>(d, j, a, bq)));
                 uo = fma(side ? se1[j] : se0[j], vo, uo);
                 go = fma(side ? sd1[j] : sd0[j], vo, go);
                 un = fma(side ? se0[j] : se1[j], vn, un);
