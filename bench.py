@@ -202,6 +202,9 @@ def main():
                     help="diffreac: the paper's diffusion-reaction problem (SURVEY §8(f1)) with --k / --N, k+2 points; "
                          "nlreac: its nonlinear variant (SURVEY §8(f3), R26); stokes: the paper's Stokes problem "
                          "(SURVEY §8(f4), R27)")
+    ap.add_argument("--solve", action="store_true",
+                    help="diffreac, N=1: also time the CUDA-graph CG iteration driving dg_apply (SURVEY §8(f3)); "
+                         "reported under 'solve' next to the operator line")
     ap.add_argument("--jacobian", action="store_true",
                     help="nlreac: time the Jacobian action J(u0) z (dg_apply_jacobian) instead of the residual")
     ap.add_argument("--k", type=int, default=3)
@@ -419,6 +422,15 @@ def main():
         "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
         "warm_ms_per_step": warm_ms,
     }
+    if args.solve and world == 1 and w.problem == 1:
+        from paper_1812_08075_b200 import solve as _solve
+        res = _solve.solve_residual(op, sop.ndofs, device=dev, graph=True, timed_iterations=K)
+        line["solve"] = {"what": "CG iteration on A x = -R(0): libdg apply + 2 dots + 3 updates, one CUDA graph "
+                                 "replay (solve.cg_graph), CUDA events over K replays",
+                         "ms_per_iteration": res.seconds_per_iteration * 1e3,
+                         "apply_share": (statistics.mean(step_ms) if flush is None else warm_ms or kern_ms) /
+                         (res.seconds_per_iteration * 1e3),
+                         "dof_iterations_per_s": w.ndofs / res.seconds_per_iteration}
     if args.jacobian:
         line["config"]["operator"] = "Jacobian action J(u0) z (dg_apply_jacobian), u0 = sin(x)"
         line["roofline"]["kernel"] = op.kernel_name + " (mode 3: Jacobian)"

@@ -51,7 +51,7 @@ def cg(apply_A, b, x0=None, rtol: float = 1e-12, maxiter: int = 2000) -> CGResul
 
 
 def cg_graph(apply_into, b, rtol: float = 1e-12, maxiter: int = 2000, check_every: int = 16,
-             on_capture=None) -> CGResult:
+             on_capture=None, timed_iterations: int | None = None) -> CGResult:
     """CG with one iteration (operator application, two dot products, three vector updates) captured in a CUDA
     graph and replayed `check_every` times between host-side convergence checks: no host synchronisation
     inside the iteration, one graph launch per iteration instead of ~10 kernel launches.
@@ -105,6 +105,22 @@ def cg_graph(apply_into, b, rtol: float = 1e-12, maxiter: int = 2000, check_ever
         step()
     if on_capture:
         on_capture(None)
+    if timed_iterations:
+        # measurement mode (bench.py --solve): exactly timed_iterations replays timed with CUDA events on the
+        # launching stream after 3 warm-up replays; no convergence loop
+        st = torch.cuda.current_stream(b.device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(timed_iterations):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        it += 3 + timed_iterations
+        hist.append(rr.sqrt().item())
+        return CGResult(x, it, hist, hist[-1] <= rtol * bn, e0.elapsed_time(e1) * 1e-3 / timed_iterations)
     import time
     t0, it0 = time.perf_counter(), it
     while it < maxiter and hist[-1] > rtol * bn:
@@ -117,7 +133,7 @@ def cg_graph(apply_into, b, rtol: float = 1e-12, maxiter: int = 2000, check_ever
 
 
 def solve_residual(op, ndofs: int, device="cuda", rtol: float = 1e-12, maxiter: int = 2000,
-                   graph: bool = False, check_every: int = 16) -> CGResult:
+                   graph: bool = False, check_every: int = 16, timed_iterations: int | None = None) -> CGResult:
     """Solve R(x) = 0 for an affine residual operator (op.apply(x) = A x - b): CG on A x = -R(0).
     graph=True: the CUDA-graph CG (cg_graph); op must be a libdg Operator (its stream is pointed at the
     capture stream during capture)."""
@@ -136,7 +152,7 @@ def solve_residual(op, ndofs: int, device="cuda", rtol: float = 1e-12, maxiter: 
             op.set_stream(stream if stream is not None else orig)
 
         return cg_graph(apply_into, -r0, rtol=rtol, maxiter=maxiter, check_every=check_every,
-                        on_capture=on_capture)
+                        on_capture=on_capture, timed_iterations=timed_iterations)
 
     def apply_A(v):
         op.apply(v, tmp)

@@ -14,7 +14,7 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref
 for C in 0 1 2 4; do timeout 900 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_cfg$C.json 2> $O/bench_cfg$C.err; done
 # SURVEY §8(f2) general quadrature (cfg2 with 7 points) and §8(f1) the paper's diffusion-reaction problem
 timeout 900 python bench.py --config 2 --quad 7 --steps 5 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_cfg2_quad7.json 2> $O/bench_cfg2_quad7.err
-timeout 900 python bench.py --problem diffreac --k 3 --N 64 --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > $O/bench_diffreac_k3_64.json 2> $O/bench_diffreac.err
+timeout 900 python bench.py --problem diffreac --k 3 --N 64 --solve --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > $O/bench_diffreac_k3_64.json 2> $O/bench_diffreac.err
 timeout 900 python bench.py --problem diffreac --k 5 --N 48 --steps 10 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_diffreac_k5_48.json 2>> $O/bench_diffreac.err
 # the nonlinear variant (R26): residual and Jacobian action
 timeout 900 python bench.py --problem nlreac --k 3 --N 64 --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > $O/bench_nlreac_k3_64.json 2> $O/bench_nlreac.err
