@@ -50,5 +50,13 @@ L.append("of the timed region, `--profile-from-start off`: one kernel launch per
 L.append("(`--set full` summaries), `stalls_*.txt` (warp-stall samples, opcode mix, per-source-line stalls),")
 L.append("`pytest_gpu.txt`, `smoke.txt`, `clocks_bench.csv` (nvidia-smi during the default bench). `history/` holds the")
 L.append("first measured version (v1 cell kernel, 16.9 ms on cfg3).")
+pdr = os.path.join(R, "bench_diffreac_k3_64.json")
+if os.path.exists(pdr):
+    sv = json.load(open(pdr)).get("solve")
+    if sv:
+        L.append("")
+        L.append("`bench_diffreac_k3_64.json` also carries `solve`: one CUDA-graph CG iteration driving `dg_apply`")
+        L.append(f"(`bench.py --problem diffreac --solve`, SURVEY §8(f3)): {sv['ms_per_iteration']:.2f} ms per iteration "
+                 f"at 64^3, k = 3, the apply {100 * sv['apply_share']:.0f} % of it.")
 open(os.path.join(R, "README.md"), "w").write("\n".join(L) + "\n")
 print("\n".join(L))
