@@ -123,13 +123,31 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
             for (int j = 0; j < N; ++j) vnb[k][j] = nb ? __ldg(nb + c * N3 + pidx<N>(f >> 1, j, a, bq)) : 0.0;
         }
     }
-    for (int t = tid; t < 9 * N2; t += NT) {
-        const int ce = t / N2, l = t % N2, c = ce / 3, e = ce % 3;
-        const double* in = U + c * N3;
-        double* out = G + ce * N3;
-        if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.D, l);
-        else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.D, l);
-        else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.D, l);
+    if constexpr (N == 4 && NT % 32 == 0) {
+        // n = 4: a gradient sweep (c, e) has 16 lines = half a warp; pair half-warps of the same direction e
+        // in one warp so that no warp runs two differently-specialised sweeps one after the other
+        // (slots of 32 lanes: (0,3) (1,4) (2,5) 6 7 8 with ce = 3 c + e)
+        constexpr int NSLOT = 6;
+        for (int slot = tid >> 5; slot < NSLOT; slot += NT / 32) {
+            const int h = (tid >> 4) & 1, l = tid & 15;
+            const int ce = slot < 3 ? slot + 3 * h : (h ? -1 : slot + 3);
+            if (ce < 0) continue;
+            const int c = ce / 3, e = ce % 3;
+            const double* in = U + c * N3;
+            double* out = G + ce * N3;
+            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.D, l);
+            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.D, l);
+            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.D, l);
+        }
+    } else {
+        for (int t = tid; t < 9 * N2; t += NT) {
+            const int ce = t / N2, l = t % N2, c = ce / 3, e = ce % 3;
+            const double* in = U + c * N3;
+            double* out = G + ce * N3;
+            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.D, l);
+            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.D, l);
+            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.D, l);
+        }
     }
     for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, NP, 2, N, false, false>::line(PR, TA, T.AP, t);
     constexpr int NFL = PREF ? NFT : (18 * N2 + NT - 1) / NT;
