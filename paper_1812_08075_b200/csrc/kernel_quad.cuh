@@ -57,6 +57,28 @@ struct Sw3 {
             out[ob + ost * q] = ACC ? out[ob + ost * q] + a : a;
         }
     }
+    // one input line, two tables -> two outputs (the line is loaded once and a warp runs one sweep body)
+    __device__ static void line2(const double* in, double* out1, const double* T1, double* out2, const double* T2, int l)
+    {
+        int ib, ist, ob, ost;
+        if (DIM == 0) { ib = E0 * l; ist = 1; ob = O0 * l; ost = 1; }
+        else if (DIM == 1) { const int i0 = l % E0, i2 = l / E0; ib = i0 + E0 * E1 * i2; ist = E0; ob = i0 + O0 * O1 * i2; ost = O0; }
+        else { ib = l; ist = E0 * E1; ob = l; ost = O0 * O1; }
+        double v[LIN];
+#pragma unroll
+        for (int j = 0; j < LIN; ++j) v[j] = in[ib + ist * j];
+#pragma unroll
+        for (int q = 0; q < LO; ++q) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int j = 0; j < LIN; ++j) {
+                a = fma(TRN ? T1[j * LO + q] : T1[q * LIN + j], v[j], a);
+                b = fma(TRN ? T2[j * LO + q] : T2[q * LIN + j], v[j], b);
+            }
+            out1[ob + ost * q] = ACC ? out1[ob + ost * q] + a : a;
+            out2[ob + ost * q] = ACC ? out2[ob + ost * q] + b : b;
+        }
+    }
 };
 
 // the same for a 2D array with extents (E0, E1)
@@ -314,11 +336,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             }
         }
         using S = qd::Sw3<N, N, N, 2, M, false, false>;
-        for (int t = gtid; t < ncell * 2 * S::NL; t += GT) {
-            const int c = t / (2 * S::NL), k = (t / S::NL) % 2, l = t % S::NL;
+        for (int t = gtid; t < ncell * S::NL; t += GT) {
+            const int c = t / S::NL, l = t % S::NL;
             double* b = cellp(c);
-            if (k) S::line(b + L::X, b + L::Y2d, T.Dq, l);
-            else S::line(b + L::X, b + L::Y2, T.A, l);
+            S::line2(b + L::X, b + L::Y2, T.A, b + L::Y2d, T.Dq, l); // A2 X and D2 X from one load of the line
         }
         if (PR == 3)
             for (int t = gtid; t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.A, t % S::NL);
@@ -377,14 +398,17 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     // ---------------- P3: stage 1c (along j0); face contraction along t2 ----------------
     {
         using SB = qd::Sw3<N, M, M, 0, M, false, false>;
-        constexpr int NQ = DR ? 4 : 3;
-        for (int t = gtid; t < ncell * NQ * SB::NL; t += GT) {
-            const int c = t / (NQ * SB::NL), k = (t / SB::NL) % NQ, l = t % SB::NL;
+        // (k = 0: Z -> G0 with D0 and, for the diffusion-reaction problems, Z -> GU = u with A0 from the same
+        // line; k = 1, 2: the A0 sweeps of Zd1, Zd2 — one sweep body per task kind)
+        for (int t = gtid; t < ncell * 3 * SB::NL; t += GT) {
+            const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
-            if (k == 0) SB::line(b + L::Z, b + L::G0, T.Dq, l);
-            else if (k == 1) SB::line(b + L::Zd1, b + L::G1, T.A, l);
-            else if (k == 2) SB::line(b + L::Zd2, b + L::G2, T.A, l);
-            else SB::line(b + L::Z, b + L::GU, T.A, l); // u = A0 A1 A2 X
+            if (k == 0) {
+                if (DR) SB::line2(b + L::Z, b + L::G0, T.Dq, b + L::GU, T.A, l);
+                else SB::line(b + L::Z, b + L::G0, T.Dq, l);
+            } else {
+                SB::line(b + (k == 1 ? L::Zd1 : L::Zd2), b + (k == 1 ? L::G1 : L::G2), T.A, l);
+            }
         }
         if (PR == 3)
             for (int t = gtid; t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.A, t % SB::NL);
