@@ -374,11 +374,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     // ---------------- P2: stage 1b (along j1); face contraction along t1 ----------------
     {
         using SA = qd::Sw3<N, N, M, 1, M, false, false>;
-        for (int t = gtid; t < ncell * 3 * SA::NL; t += GT) {
-            const int c = t / (3 * SA::NL), k = (t / SA::NL) % 3, l = t % SA::NL;
+        for (int t = gtid; t < ncell * 2 * SA::NL; t += GT) {
+            const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
             double* b = cellp(c);
-            if (k == 0) SA::line(b + L::Y2, b + L::Z, T.A, l);
-            else if (k == 1) SA::line(b + L::Y2, b + L::Zd1, T.Dq, l);
+            if (k == 0) SA::line2(b + L::Y2, b + L::Z, T.A, b + L::Zd1, T.Dq, l); // A1 (A2 X), D1 (A2 X)
             else SA::line(b + L::Y2d, b + L::Zd2, T.A, l);
         }
         if (PR == 3)
