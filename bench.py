@@ -101,76 +101,138 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
-def oracle_sample_rate(w, budget_s: float, seed: int = 2024, jacobian: bool = False):
-    """Time the oracle (as it stands) on a deterministic random sample of cells of workload w,
-    sized to roughly budget_s seconds of host CPU work. Returns (DOF/s, cells, seconds, threads)."""
-    import numpy as np
+def _host_info():
+    """lscpu model, host cores and the oracle's OpenMP thread count (SURVEY §8(d) oracle timing)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
 
-    import oracle
-    import synth
-    rng = np.random.default_rng(seed)
-    n3 = w.block
 
-    def run(ncell):
-        cells = np.sort(rng.choice(w.ncells, ncell, replace=False)).astype(np.int64)
-        if w.problem in (1, 2, 3):  # the paper's problems: the oracle on the whole host vector, sampled rows
-            x = synth.x_np(w)
-            t0 = time.perf_counter()
-            if w.problem == 3:
-                oracle.apply_stokes(w, x, cells)
-            elif w.problem == 1:
-                oracle.apply_diffreac(w, x, cells)
-            elif jacobian:
-                oracle.apply_nlreac(w, x, u0=np.sin(x), cells=cells)
-            else:
-                oracle.apply_nlreac(w, x, cells=cells)
-            return time.perf_counter() - t0
-        nb = oracle.neighbours(w, cells)
-        x7 = synth.x_cells_np(w, nb.reshape(-1)).reshape(len(cells), 7, n3)
-        j7 = synth.jac_cells_np(w, nb.reshape(-1)).reshape(len(cells), 7, 9) if w.geom_kind else None
+class OracleSample:
+    """The oracle (as it stands) on a fixed, deterministic random sample of cells of workload w, sized once
+    (calibrate) to about `budget_s` seconds of host CPU work; run() times one evaluation of that sample."""
+
+    def __init__(self, w, seed: int = 2024, jacobian: bool = False):
+        import numpy as np
+
+        import synth
+        self.w, self.jacobian = w, jacobian
+        self.rng = np.random.default_rng(seed)
+        self.x = synth.x_np(w) if w.problem in (1, 2, 3) else None
+        self.cells = None
+
+    def _prepare(self, ncell):
+        import numpy as np
+
+        import oracle
+        import synth
+        w = self.w
+        self.cells = np.sort(self.rng.choice(w.ncells, ncell, replace=False)).astype(np.int64)
+        if w.problem not in (1, 2, 3):
+            nb = oracle.neighbours(w, self.cells)
+            self.x7 = synth.x_cells_np(w, nb.reshape(-1)).reshape(len(self.cells), 7, w.block)
+            self.j7 = synth.jac_cells_np(w, nb.reshape(-1)).reshape(len(self.cells), 7, 9) if w.geom_kind else None
+
+    def run(self):
+        import numpy as np
+
+        import oracle
+        w, cells = self.w, self.cells
         t0 = time.perf_counter()
-        oracle.apply_cells_local(w, cells, x7, j7)
+        if w.problem == 3:
+            oracle.apply_stokes(w, self.x, cells)
+        elif w.problem == 1:
+            oracle.apply_diffreac(w, self.x, cells)
+        elif w.problem == 2:
+            oracle.apply_nlreac(w, self.x, u0=np.sin(self.x) if self.jacobian else None, cells=cells)
+        else:
+            oracle.apply_cells_local(w, cells, self.x7, self.j7)
         return time.perf_counter() - t0
 
-    th = oracle.num_threads()
-    ncell = max(th, 8)
-    t = run(ncell)
-    while t < 0.2 * budget_s and ncell < w.ncells:      # grow the probe until it costs ~20% of the budget
-        ncell = min(w.ncells, ncell * 4)
-        t = run(ncell)
-    target = int(min(w.ncells, max(ncell, ncell * budget_s / max(t, 1e-9))))
-    if target > ncell * 1.2:
-        ncell = target
-        t = run(ncell)
-    return ncell * n3 / t, ncell, t, th
+    def calibrate(self, budget_s: float):
+        import oracle
+        th = oracle.num_threads()
+        ncell = min(self.w.ncells, max(th, 8))
+        self._prepare(ncell)
+        t = self.run()
+        while t < 0.1 * budget_s and ncell < self.w.ncells:  # grow the probe until it costs ~10% of the budget
+            ncell = min(self.w.ncells, ncell * 4)
+            self._prepare(ncell)
+            t = self.run()
+        target = int(min(self.w.ncells, max(ncell, ncell * budget_s / max(t, 1e-9))))
+        if target != ncell:
+            self._prepare(target)
+        return self
+
+    @property
+    def dofs(self):
+        return len(self.cells) * self.w.block
+
+
+def oracle_sample_rate(w, budget_s: float, seed: int = 2024, jacobian: bool = False, threads: int | None = None):
+    """Time the oracle on a random cell sample of about budget_s seconds. Returns (DOF/s, cells, seconds, threads)."""
+    import oracle
+    th0 = oracle.num_threads()
+    if threads:
+        oracle.set_threads(threads)
+    try:
+        s = OracleSample(w, seed, jacobian).calibrate(budget_s)
+        t = s.run()
+        return s.dofs / t, len(s.cells), t, oracle.num_threads()
+    finally:
+        oracle.set_threads(th0)
 
 
 def run_reference(args, w, rank):
-    """--impl reference: the oracle on the host cores, rank 0 only."""
+    """--impl reference: the oracle on the host cores, rank 0 only; one calibrated sample per step so that the
+    whole --steps K --warmup W run stays within a few minutes."""
     if rank != 0:
         return 0
-    budget = max(0.5, min(5.0, 150.0 / (args.steps + args.warmup)))
+    import oracle
+    budget = max(0.3, min(4.0, 100.0 / (args.steps + args.warmup)))
+    s = OracleSample(w, jacobian=args.jacobian).calibrate(budget)
     for _ in range(args.warmup):
-        oracle_sample_rate(w, budget, jacobian=args.jacobian)
-    rates, cells, secs = [], 0, 0.0
-    th = 1
-    for _ in range(args.steps):
-        v, c, t, th = oracle_sample_rate(w, budget, jacobian=args.jacobian)
-        rates.append(v)
-        cells, secs = c, t
-    value = statistics.median(rates)
+        s.run()
+    times = [s.run() for _ in range(args.steps)]
+    t_step = statistics.median(times)
+    value = s.dofs / t_step
+    th = oracle.num_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": w.ndofs / value * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config(w, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": th, "kind": "oracle",
-                         "sample": f"{cells} random cells ({cells * w.block} DOFs) of {w.name} per step, "
-                                   f"~{secs:.1f} s each; ms_per_step extrapolated to the whole mesh"},
+                         "sample": f"{len(s.cells)} random cells ({s.dofs} DOFs) of {w.name} per step, "
+                                   f"median {t_step:.2f} s per step; ms_per_step extrapolated to the whole mesh",
+                         **_host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _profile_record(workload, kernel):
+    """ncu numbers of this kernel on this workload from the newest profiles/<round>/ncu_counters.json
+    (written by tools/ncu_summary.py from an `ncu --set full` capture of the same command)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_counters.json")), reverse=True):
+        try:
+            rec = json.load(open(path)).get(workload, {}).get(kernel)
+        except Exception:
+            rec = None
+        if rec:
+            rec = dict(rec)
+            rec["src"] = os.path.relpath(path, ROOT)
+            return rec
+    return None
 
 
 def _config(w, ngpu):
@@ -231,6 +293,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and args.impl != "reference":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N ranks with torchrun "
+                         f"(python -m torch.distributed.run --nproc-per-node {args.gpus} ... bench.py --gpus {args.gpus})")
     if args.impl == "reference":
         return run_reference(args, w, rank)
 
@@ -273,8 +338,8 @@ def main():
         step(x, r)
     barrier()
 
-    # ---- timed region: K steps, events on the launching stream; per-step event pairs give the
-    #      kernel's average duration (N = 1: one launch per step, so step == kernel)
+    # ---- timed region: exactly K steps, events on the launching stream, barrier + synchronize on both sides;
+    #      per-step event pairs give the kernel's average duration (N = 1: one launch per step, so step == kernel)
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t_start = torch.cuda.Event(enable_timing=True)
@@ -298,34 +363,58 @@ def main():
         t_end.record(stream)
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
-    barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    warm_ms = None
-    if flush is not None:
-        # L2-resident vectors: also the warm number (no flush between applies; SURVEY §8(d) timing protocol)
-        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
-        w0.record(stream)
-        for _ in range(K):
-            step(x, r)
-        w1.record(stream)
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        # ---- sustained: >= 200 ms of back-to-back applies (SURVEY §8(d) timing protocol: >= 100 ms per line),
+        #      replayed from one CUDA graph when an apply is short (cfg0 / cfg1: launch latency), under the same
+        #      clock sampler; the roofline below uses this per-apply time (warm L2 for L2-resident vectors)
+        est = max(statistics.median(step_ms), 1e-3)
+        R = int(min(20000, max(K, 200.0 / est)))
+        graph = None
+        if est < 1.0 and world == 1:
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(stream)
+            with torch.cuda.stream(gs):
+                op.set_stream(gs)
+                step(x, r)  # warm the capture stream
+                graph = torch.cuda.CUDAGraph()
+                reps = min(R, 500)
+                with torch.cuda.graph(graph, stream=gs):
+                    for _ in range(reps):
+                        step(x, r)
+            stream.wait_stream(gs)
+            op.set_stream(stream)
+            nrep = max(1, R // reps)
+            R = reps * nrep
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        s0.record(stream)
+        if graph is not None:
+            for _ in range(nrep):
+                graph.replay()
+        else:
+            for _ in range(R):
+                step(x, r)
+        s1.record(stream)
         torch.cuda.synchronize()
-        warm_ms = w0.elapsed_time(w1) / K
+        sustained_ms = s0.elapsed_time(s1) / R
+    barrier()
+    warm_ms = sustained_ms if flush is not None else None
     total_ms = t_start.elapsed_time(t_end) if flush is None else sum(step_ms)
-    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t_local = torch.tensor([total_ms, sustained_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    total_ms = t_local.item()
+    total_ms = t_local[0].item()
     ms_per_step = total_ms / K
     value = w.ndofs / (ms_per_step * 1e-3)
 
-    # ---- roofline of the dominant kernel (per launch, this rank)
+    # ---- roofline of the dominant kernel (per launch, this rank; per-apply time of the sustained region)
     pk = _peaks()
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     fp64_nominal = sms * 64 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s: SMs x 64 DFMA/clk x 2 flop x clock
     fp64_meas, _ = dg.dg_bench_fp64(local_rank, 4000)
-    kern_ms = statistics.mean(step_ms)
+    kern_ms = sustained_ms if world == 1 else statistics.mean(step_ms)
     F = op.alg_flops
     if args.jacobian:
         # J(u0) z: + u0 at the m^3 points (2 (n^3 m + n^2 m^2 + n m^3) per cell), reaction 2 c u0 z without f
@@ -337,25 +426,36 @@ def main():
     t_byte = B / (pk["hbm_gbs"] * 1e9)
     ach_tf = F / (kern_ms * 1e-3) / 1e12
     ach_gbs = B / (kern_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(w.name, {}).get(op.kernel_name)
-        except Exception:
-            traffic = None
+    prof = _profile_record(w.name, op.kernel_name)
+    traffic = prof.get("dram_bytes") if prof else None
     if t_flop >= t_byte:
         roof = {"bound": "alu", "achieved": ach_tf, "peak": fp64_nominal, "unit": "TFLOP/s",
                 "frac": ach_tf / fp64_nominal, "traffic": traffic,
-                "peak_src": f"derived: {sms} SMs x 64 DFMA/clk x 2 x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md §5)"}
+                "peak_src": f"derived: {sms} SMs x 64 DFMA/clk x 2 x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md §4); "
+                            f"'achieved' = F_alg (SURVEY §8(d) algorithmic flops) / kernel time"}
     else:
         roof = {"bound": "hbm", "achieved": ach_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach_gbs / pk["hbm_gbs"], "traffic": traffic, "peak_src": f"{pk['src']} copy bandwidth"}
-    roof.update({"kernel": op.kernel_name, "kernel_ms": kern_ms, "alg_flops_per_launch": F,
-                 "alg_bytes_per_launch": B, "frac_fp64": ach_tf / fp64_nominal,
+    roof.update({"kernel": op.kernel_name, "kernel_ms": kern_ms,
+                 "kernel_ms_src": "sustained region (>= 200 ms back-to-back, graph-replayed if short)" if world == 1
+                 else "mean of the K timed steps",
+                 "alg_flops_per_launch": F, "alg_bytes_per_launch": B, "frac_fp64": ach_tf / fp64_nominal,
                  "frac_fp64_measured_dfma": ach_tf / fp64_meas, "fp64_dfma_measured_tflops": fp64_meas,
                  "frac_hbm": ach_gbs / pk["hbm_gbs"], "t_roof_ms": max(t_flop, t_byte) * 1e3,
-                 "frac_roof": max(t_flop, t_byte) * 1e3 / kern_ms})
+                 "frac_roof": max(t_flop, t_byte) * 1e3 / kern_ms,
+                 "traffic_src": (f"ncu --set full of this kernel on this config ({prof.get('src')}): "
+                                 "dram__bytes_read.sum + dram__bytes_write.sum per launch") if prof else None})
+    if w.problem == 0 and w.geom_kind == 0 and w.coeff_kind == 0 and op.kernel_name in ("k_axis8", "k_gen"):
+        # the axis-aligned kernels run the Kronecker-sum line operator (S_d = D^T W D along each line): SURVEY §8(d)
+        # asks for the fraction against that smaller count too (volume 6 n^4 instead of 12 n^4 + 3 n^3 per cell)
+        nn = w.n
+        F_kron = (6.0 * nn + 48.0 + 30.0 / nn) * sop.ndofs
+        roof["frac_kron"] = F_kron / (kern_ms * 1e-3) / 1e12 / fp64_nominal
+        roof["alg_flops_kron_per_launch"] = F_kron
+    if prof and prof.get("fp64_flops_issued"):
+        # what the FP64 pipe actually executed (ncu: 2 dfma + dadd + dmul thread instructions), at this run's time
+        roof["fp64_flops_issued_per_launch"] = prof["fp64_flops_issued"]
+        roof["frac_exec"] = prof["fp64_flops_issued"] / (kern_ms * 1e-3) / 1e12 / fp64_nominal
 
     # ---- e2e: same metric through the public API with host buffers (pinned), copies timed
     e2e = None
@@ -404,12 +504,17 @@ def main():
                 if world == 1 else "per rank: pinned H2D of the slab, halo exchange + kernels, D2H of r")}
         del xh, rh, uh
 
-    # ---- CPU baseline (rank 0, N = 1 only)
+    # ---- CPU baseline (rank 0, N = 1 only): the oracle as it stands on all host cores; for the small configs
+    #      (cfg0 / cfg1) also on one thread (SURVEY §8(d) oracle timing)
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         v, cells, secs, th = oracle_sample_rate(w, args.cpu_seconds, jacobian=args.jacobian)
         cpu = {"value": v, "unit": UNIT, "cores": th, "kind": "oracle",
-               "sample": f"{cells} random cells ({cells * w.block} DOFs) of {w.name}, {secs:.1f} s"}
+               "sample": f"{cells} random cells ({cells * w.block} DOFs) of {w.name}, {secs:.1f} s", **_host_info()}
+        if w.ndofs <= 4_000_000:
+            v1, c1, s1, _ = oracle_sample_rate(w, min(4.0, args.cpu_seconds / 3), jacobian=args.jacobian, threads=1)
+            cpu["one_thread"] = {"value": v1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{c1} random cells ({c1 * w.block} DOFs), {s1:.1f} s"}
 
     # ---- sanity of the timed result (not a parity claim: tests/ do that): finite, nonzero
     ok = bool(torch.isfinite(r).all().item()) and r.abs().max().item() > 0
@@ -420,6 +525,8 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * sop.launches_per_apply,
         "clocks": clk.summary(), "result_finite": ok,
         "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
+        "sustained": {"ms_per_apply": sustained_ms, "applies": R, "graph": graph is not None,
+                      "value": w.ndofs / (sustained_ms * 1e-3), "l2": "warm" if flush is not None else "cold (vectors > L2)"},
         "warm_ms_per_step": warm_ms,
     }
     if args.solve and world == 1 and w.problem == 1:

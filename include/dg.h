@@ -93,12 +93,19 @@ typedef struct dg_mesh {
  * (288 B/cell: |det J| J^-1 J^-T, rows of J, upper-face normals / surface elements);
  * DG_COEFF_SINCOS: c(x) factor tables (96 (n+1) B/cell) and c at the upper-face points
  * (8 (3n^2 rounded up to even) B/cell); DG_GEOM_AXIS + DG_COEFF_ONE: nothing. *out owned by
- * the caller, release with dg_destroy. Synchronous. */
+ * the caller, release with dg_destroy. Synchronous. Kernel selection is deterministic: k_axis8 for
+ * axis-aligned Q7 with c = 1 and N1 % 2 == N2 % 4 == 0; k_gen when its (i1, i2) tile divides the mesh;
+ * k_cell_general otherwise; k_quad / k_stokes for the other problems. A failing kernel attribute
+ * call or allocation returns DG_ERR_CUDA / DG_ERR_OOM (no silent switch to another kernel) and
+ * releases everything allocated so far. */
 int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out);
 
 /* r = A x for a context owning the WHOLE mesh (nplanes == N[0]).
- * x, r: caller-owned DEVICE pointers to dg_local_ndofs() doubles each, 8-byte aligned, not
- * overlapping (else DG_ERR_INVALID). r is overwritten (every entry written exactly once).
+ * x, r: caller-owned DEVICE pointers to dg_local_ndofs() doubles each, not overlapping (else
+ * DG_ERR_INVALID). Alignment (else DG_ERR_INVALID, checked before any launch): x, r and the halo
+ * planes of dg_apply_planes 16-byte aligned for every kernel (16-B vector / bulk-copy accesses);
+ * x additionally 128-byte aligned when dg_kernel_name() is "k_axis8" (the TMA tensor map base).
+ * cudaMalloc / PyTorch allocations satisfy both. r is overwritten (every entry written exactly once).
  * Asynchronous on the context stream; the caller synchronises. */
 int dg_apply(dg_ctx* ctx, const double* x, double* r);
 
@@ -121,7 +128,7 @@ int dg_apply_planes(dg_ctx* ctx, const double* x, const double* x_below, const d
  * u0 and z are evaluated at the quadrature points by the same sum-factorisation sweeps in one
  * kernel (k_quad mode 3). Arguments as dg_apply / dg_apply_planes (z takes x's place, z_below /
  * z_above its halo planes); u0: DEVICE, dg_local_ndofs() doubles of the owned planes only (the
- * Jacobian's u0-dependence is cell-local), 8-byte aligned, must not overlap r.
+ * Jacobian's u0-dependence is cell-local), 16-byte aligned, must not overlap r.
  * DG_ERR_UNSUPPORTED unless the context's problem is DG_PROBLEM_NLREAC. Asynchronous. */
 int dg_apply_jacobian(dg_ctx* ctx, const double* u0, const double* z, double* r);
 int dg_apply_jacobian_planes(dg_ctx* ctx, const double* u0, const double* z, const double* z_below,

@@ -50,6 +50,7 @@ def lib():
         L.oracle_apply_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                           dp, dp, i64p, ctypes.c_int64]
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -64,6 +65,11 @@ def _i64p(a):
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_threads(n: int) -> None:
+    """OpenMP thread count of the oracle loops (timing only)."""
+    lib().oracle_set_threads(int(n))
 
 
 def gauss_legendre(m: int):

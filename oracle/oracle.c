@@ -635,6 +635,16 @@ int oracle_num_threads(void)
 #endif
 }
 
+/* Thread count of the OpenMP loops (timing only: bench.py's 1-thread oracle time). */
+void oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* ====================================================================================== */
 /* Stokes (Eq. stokes_strong / stokes_weak).                 */
 /*   -mu Lap u + grad p = f, div u = 0 on (0,1)^3, u = g on Gamma_D, mu grad u n - p n = 0  */

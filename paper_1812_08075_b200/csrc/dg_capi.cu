@@ -7,7 +7,6 @@
 #include "kernel_quad.cuh"
 #include "kernel_quadw.cuh"
 #include "kernel_stokes.cuh"
-#include "kernel_tile.cuh"
 #include "tables.h"
 
 #include <cudaTypedefs.h>
@@ -85,75 +84,6 @@ LaunchFn pick(int n, bool aff, bool coef)
     case 7: return pick_cell<7>(aff, coef);
     case 8: return pick_cell<8>(aff, coef);
     default: return nullptr;
-    }
-}
-
-// ---- marching-tile general kernel (k_tile): tile per degree
-template <int N> struct TileShape;
-// NT = T1 T2 N^2 rounded up to a warp multiple (one thread per cell line position)
-template <> struct TileShape<2> { static constexpr int T1 = 4, T2 = 8, NT = 128; };
-template <> struct TileShape<3> { static constexpr int T1 = 2, T2 = 4, NT = 96; };
-template <> struct TileShape<4> { static constexpr int T1 = 2, T2 = 4, NT = 128; };
-template <> struct TileShape<5> { static constexpr int T1 = 2, T2 = 2, NT = 128; };
-template <> struct TileShape<6> { static constexpr int T1 = 2, T2 = 2, NT = 160; };
-template <> struct TileShape<7> { static constexpr int T1 = 2, T2 = 2, NT = 224; };
-template <> struct TileShape<8> { static constexpr int T1 = 2, T2 = 2, NT = 256; };
-
-struct TileInfo {
-    LaunchFn fn;
-    int T1, T2, smem;
-    cudaError_t (*attr)();
-};
-
-template <int N, bool AFF, bool COEF>
-cudaError_t launch_tile(const void* tab, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                        double* r, long long p0, long long p1, cudaStream_t st, const double* geo)
-{
-    constexpr int T1 = TileShape<N>::T1, T2 = TileShape<N>::T2, NT = TileShape<N>::NT;
-    using Y = dg::tl::Lay<N, T1, T2>;
-    if (p1 <= p0) return cudaSuccess;
-    const unsigned grid = (unsigned)((M.N1 / T1) * (M.N2 / T2));
-    dg::k_tile<N, AFF, COEF, T1, T2, NT><<<grid, NT, Y::BYTES, st>>>(
-        x, xb, xa, r, (int)p0, (int)p1, *static_cast<const dg::Tab<N>*>(tab), M, geo);
-    return cudaGetLastError();
-}
-
-template <int N, bool AFF, bool COEF>
-cudaError_t attr_tile()
-{
-    constexpr int T1 = TileShape<N>::T1, T2 = TileShape<N>::T2, NT = TileShape<N>::NT;
-    return cudaFuncSetAttribute(dg::k_tile<N, AFF, COEF, T1, T2, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                dg::tl::Lay<N, T1, T2>::BYTES);
-}
-
-template <int N>
-TileInfo tile_info(bool aff, bool coef)
-{
-    constexpr int T1 = TileShape<N>::T1, T2 = TileShape<N>::T2;
-    TileInfo t;
-    t.T1 = T1;
-    t.T2 = T2;
-    t.smem = dg::tl::Lay<N, T1, T2>::BYTES;
-    if (aff) {
-        t.fn = coef ? launch_tile<N, true, true> : launch_tile<N, true, false>;
-        t.attr = coef ? attr_tile<N, true, true> : attr_tile<N, true, false>;
-    } else {
-        t.fn = coef ? launch_tile<N, false, true> : launch_tile<N, false, false>;
-        t.attr = coef ? attr_tile<N, false, true> : attr_tile<N, false, false>;
-    }
-    return t;
-}
-
-TileInfo pick_tile(int n, bool aff, bool coef)
-{
-    switch (n) {
-    case 2: return tile_info<2>(aff, coef);
-    case 3: return tile_info<3>(aff, coef);
-    case 4: return tile_info<4>(aff, coef);
-    case 5: return tile_info<5>(aff, coef);
-    case 6: return tile_info<6>(aff, coef);
-    case 7: return tile_info<7>(aff, coef);
-    default: return tile_info<8>(aff, coef);
     }
 }
 
@@ -576,8 +506,6 @@ struct dg_ctx {
     const char* kname;
     // axis-aligned n = 8 fast path (k_axis8)
     bool ax8;
-    bool tile;
-    TileInfo tinfo;
     bool gen;
     GenInfo ginfo;
     int m;     // Gauss points per direction
@@ -593,13 +521,14 @@ struct dg_ctx {
     const double* tmap_ptr;
     long long* dbg; // DG_TRACE: device buffer of per-phase clock64 stamps (k_axis8)
     double* d_jac;
-    double* d_geo;  // k_tile / k_gen geometry records (affine)
+    double* d_geo;  // k_gen geometry records (affine)
     double* d_ctab;  // k_gen c(x) factor tables (coefficient c(x))
     double* d_cface; // k_gen c(x) at the upper-face points of every cell
     // host-pipeline state (dg_apply_host)
     double* hx_d;
     double* hr_d;
     cudaStream_t s_h2d, s_d2h, s_cmp;
+    cudaEvent_t ev_in[8], ev_cmp[8]; // created with the streams, destroyed by dg_destroy (no per-call events)
     int64_t plane_dofs, local_dofs;
 };
 
@@ -647,7 +576,6 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         return c->launch(c->qtab, c->M, x, xb, xa, r, (long long)p0 * pcq, (long long)p1 * pcq, st, nullptr);
     }
     if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo, c->d_ctab, c->d_cface);
-    if (c->tile) return c->tinfo.fn(c->tab, c->M, x, xb, xa, r, p0, p1, st, c->d_geo);
     const long long pc = c->M.plane_cells;
     return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
 }
@@ -673,6 +601,19 @@ int host_line_ops(const dg::HostTables& Ht, double P, const double* x, const dou
     return DG_OK;
 }
 } // namespace
+
+// release a partially built context and report the failure (dg_setup never leaks on an error path)
+static int setup_fail(dg_ctx* c, int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    dg_destroy(c);
+    g_err = buf;
+    return code;
+}
 
 extern "C" {
 
@@ -770,9 +711,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         // overintegration: m = n + 1 Gauss points, interpolation A != I -> k_quad
         dg::HostTables Hm;
         if (dg::build_tables(quad, &Hm)) {
-            if (c->d_jac) cudaFree(c->d_jac);
-            free(c);
-            return fail(DG_ERR_INVALID, "tables m=%d", quad);
+            return setup_fail(c, DG_ERR_INVALID, "tables m=%d", quad);
         }
         switch (n) {
         case 2: fill_qtab<2>(H, Hm, c->qtab); break;
@@ -791,9 +730,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr, cta);
         if (e == cudaSuccess && pr == 2) c->launch_jac = pick_quad(n, false, false, &e, 3, true);
         if (e != cudaSuccess) {
-            if (c->d_jac) cudaFree(c->d_jac);
-            free(c);
-            return fail(DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
+            return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
         }
         const bool warp = n == 5 && !cta;
         c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? (warp ? "k_quadw_diffreac" : "k_quad_diffreac")
@@ -803,9 +740,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (mesh->problem == DG_PROBLEM_STOKES) {
         dg::HostTables Hp;
         if (dg::build_tables(n - 1, &Hp)) {
-            if (c->d_jac) cudaFree(c->d_jac);
-            free(c);
-            return fail(DG_ERR_INVALID, "tables n=%d", n - 1);
+            return setup_fail(c, DG_ERR_INVALID, "tables n=%d", n - 1);
         }
         switch (n) {
         case 2: fill_stab<2>(H, Hp, c->stab); break;
@@ -819,26 +754,26 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         cudaError_t e = cudaSuccess;
         c->launch = pick_stokes(n, &e);
         if (e != cudaSuccess) {
-            free(c);
-            return fail(DG_ERR_CUDA, "dg_setup: k_stokes attributes: %s", cudaGetErrorString(e));
+            return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_stokes attributes: %s", cudaGetErrorString(e));
         }
         c->stokes = true;
         c->kname = "k_stokes";
         *out = c;
         return DG_OK;
     }
-    // marching-tile kernel when the mesh tiles evenly and every tile row is a 16-B aligned bulk copy
     if (!c->quad) {
-        c->tinfo = pick_tile(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
-        const int64_t rowb = (int64_t)c->tinfo.T2 * n3 * 8;
-        const bool rows_aligned = (rowb % 16 == 0) && ((n3 * 8) % 16 == 0 || (mesh->N[2] % 2 == 0 && c->tinfo.T2 % 2 == 0));
-        c->tile = mesh->N[1] % c->tinfo.T1 == 0 && mesh->N[2] % c->tinfo.T2 == 0 && rows_aligned &&
-                  getenv("DG_FORCE_GENERAL") == nullptr && c->tinfo.attr() == cudaSuccess;
-        // k_gen (preferred): tiles divide the mesh; odd n^3 needs even T2 and N2 for 16-B aligned bulk rows
+        // k_gen when its tiles divide the mesh (odd n^3 needs even T2 and N2 for 16-B aligned bulk rows); otherwise
+        // the cell-centric k_cell_general (any N >= 2). A failing attribute call or allocation is an error, not a
+        // silent switch to another kernel.
         c->ginfo = pick_gen(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
         c->gen = mesh->N[1] % c->ginfo.T1 == 0 && mesh->N[2] % c->ginfo.T2 == 0 &&
-                 ((n3 % 2 == 0) || (mesh->N[2] % 2 == 0 && c->ginfo.T2 % 2 == 0)) && getenv("DG_FORCE_GENERAL") == nullptr &&
-                 getenv("DG_NO_GEN") == nullptr && c->ginfo.attr() == cudaSuccess;
+                 ((n3 % 2 == 0) || (mesh->N[2] % 2 == 0 && c->ginfo.T2 % 2 == 0)) && getenv("DG_FORCE_GENERAL") == nullptr;
+        if (c->gen) {
+            cudaError_t e = c->ginfo.attr();
+            if (e != cudaSuccess)
+                return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_gen shared-memory attribute (%d B): %s", c->ginfo.smem,
+                                  cudaGetErrorString(e));
+        }
         {
             // planes per work item: enough (chunk, tile) items for ~8 per SM, at most 32 planes
             // (each chunk re-evaluates the face below its first plane)
@@ -859,16 +794,14 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             case 8: fill_eotab<8>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
             }
         }
-        if ((c->tile || c->gen) && mesh->geom_kind == DG_GEOM_AFFINE) {
-            // per-cell geometry records for the tile kernel (k_geom, once)
+        if (c->gen && mesh->geom_kind == DG_GEOM_AFFINE) {
+            // per-cell geometry records for k_gen (k_geom, once)
             const long long nc = (long long)M.plane_cells * (M.L + 2);
             cudaError_t e = cudaMalloc(&c->d_geo, sizeof(double) * dg::GREC * (size_t)nc);
-            if (e != cudaSuccess) {
-                c->tile = c->gen = false;
-            } else {
-                dg::k_geom<<<(unsigned)((nc + 255) / 256), 256>>>(c->d_jac, c->d_geo, nc, M.plane_cells, M.N1, M.N2, M.L + 2);
-                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_geo); c->d_geo = nullptr; c->tile = c->gen = false; }
-            }
+            if (e != cudaSuccess) { c->d_geo = nullptr; return setup_fail(c, DG_ERR_OOM, "dg_setup: geometry records: %s", cudaGetErrorString(e)); }
+            dg::k_geom<<<(unsigned)((nc + 255) / 256), 256>>>(c->d_jac, c->d_geo, nc, M.plane_cells, M.N1, M.N2, M.L + 2);
+            e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_geom: %s", cudaGetErrorString(e));
         }
         if (c->gen && mesh->coeff_kind == DG_COEFF_SINCOS) {
             // per-cell c(x) factor tables for k_gen (k_ctab, once)
@@ -876,38 +809,36 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             const long long nen = 2LL * 3 * (n + 1);
             const long long cfsz = (3LL * n * n + 1) / 2 * 2;
             cudaError_t e = cudaMalloc(&c->d_ctab, sizeof(double) * 2 * nen * (size_t)nc);
-            if (e == cudaSuccess) e = cudaMalloc(&c->d_cface, sizeof(double) * cfsz * (size_t)nc);
-            if (e != cudaSuccess) {
-                c->gen = false;
-            } else {
-                dg::XiTab X;
-                for (int i = 0; i < 9; ++i) X.xi[i] = i < n ? H.xi[i] : 1.0;
-                X.xi[n] = 1.0;
-                const long long tot = nc * nen;
-                const unsigned g = (unsigned)((tot + 255) / 256);
-                switch (n) {
-                case 2: dg::k_ctab<2><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                case 3: dg::k_ctab<3><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                case 4: dg::k_ctab<4><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                case 5: dg::k_ctab<5><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                case 6: dg::k_ctab<6><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                case 7: dg::k_ctab<7><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                case 8: dg::k_ctab<8><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
-                }
-                const unsigned g2 = (unsigned)((nc * cfsz + 255) / 256);
-                switch (n) {
-                case 2: dg::k_cface<2><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                case 3: dg::k_cface<3><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                case 4: dg::k_cface<4><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                case 5: dg::k_cface<5><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                case 6: dg::k_cface<6><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                case 7: dg::k_cface<7><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                case 8: dg::k_cface<8><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
-                }
-                if (cudaDeviceSynchronize() != cudaSuccess) { cudaFree(c->d_ctab); cudaFree(c->d_cface); c->d_ctab = c->d_cface = nullptr; c->gen = false; }
+            if (e != cudaSuccess) { c->d_ctab = nullptr; return setup_fail(c, DG_ERR_OOM, "dg_setup: c(x) tables: %s", cudaGetErrorString(e)); }
+            e = cudaMalloc(&c->d_cface, sizeof(double) * cfsz * (size_t)nc);
+            if (e != cudaSuccess) { c->d_cface = nullptr; return setup_fail(c, DG_ERR_OOM, "dg_setup: face c(x) tables: %s", cudaGetErrorString(e)); }
+            dg::XiTab X;
+            for (int i = 0; i < 9; ++i) X.xi[i] = i < n ? H.xi[i] : 1.0;
+            X.xi[n] = 1.0;
+            const long long tot = nc * nen;
+            const unsigned g = (unsigned)((tot + 255) / 256);
+            switch (n) {
+            case 2: dg::k_ctab<2><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+            case 3: dg::k_ctab<3><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+            case 4: dg::k_ctab<4><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+            case 5: dg::k_ctab<5><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+            case 6: dg::k_ctab<6><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+            case 7: dg::k_ctab<7><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
+            case 8: dg::k_ctab<8><<<g, 256>>>(c->d_jac, c->d_ctab, nc, M, X); break;
             }
+            const unsigned g2 = (unsigned)((nc * cfsz + 255) / 256);
+            switch (n) {
+            case 2: dg::k_cface<2><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            case 3: dg::k_cface<3><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            case 4: dg::k_cface<4><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            case 5: dg::k_cface<5><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            case 6: dg::k_cface<6><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            case 7: dg::k_cface<7><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            case 8: dg::k_cface<8><<<g2, 256>>>(c->d_jac, c->d_cface, nc, M, X); break;
+            }
+            e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_ctab / k_cface: %s", cudaGetErrorString(e));
         }
-        if (c->tile) c->kname = "k_tile";
         if (c->gen) c->kname = "k_gen";
 #ifdef DG_GEN_TRACE
         if (c->gen && getenv("DG_TRACE") && !c->dbg) {
@@ -949,8 +880,10 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             AX8_VARIANTS(AX8_ATTR)
 #undef AX8_ATTR
         }
-        if (e != cudaSuccess || !get_encode()) c->ax8 = false;
-        else c->kname = "k_axis8";
+        if (e != cudaSuccess)
+            return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_axis8 shared-memory attribute: %s", cudaGetErrorString(e));
+        if (!get_encode()) return setup_fail(c, DG_ERR_CUDA, "dg_setup: cuTensorMapEncodeTiled unavailable (driver)");
+        c->kname = "k_axis8";
         if (c->ax8 && getenv("DG_TRACE")) {
             if (cudaMalloc(&c->dbg, sizeof(long long) * 1024 * 16 * 8) != cudaSuccess) c->dbg = nullptr;
             else cudaMemset(c->dbg, 0, sizeof(long long) * 1024 * 16 * 8);
@@ -982,6 +915,10 @@ int dg_destroy(dg_ctx* c)
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
+    for (int i = 0; i < 8; ++i) {
+        if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+        if (c->ev_cmp[i]) cudaEventDestroy(c->ev_cmp[i]);
+    }
     free(c);
     return DG_OK;
 }
@@ -1090,7 +1027,7 @@ int dg_apply_jacobian_planes(dg_ctx* c, const double* u0, const double* z, const
     const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
     const char *us = (const char*)u0, *rs = (const char*)r;
     if (r && us < rs + bytes && rs < us + bytes) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 and r overlap");
-    if ((uintptr_t)u0 & 7) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 must be 8-byte aligned");
+    if ((uintptr_t)u0 & 15) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 must be 16-byte aligned");
     return apply_planes_impl(c, z, zb, za, r, p0, p1, u0);
 }
 
@@ -1112,12 +1049,11 @@ static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const
     const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
     const char *xs = (const char*)x, *rs = (const char*)r;
     if (xs < rs + bytes && rs < xs + bytes) return fail(DG_ERR_INVALID, "dg_apply: x and r overlap");
-    if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 7)
-        return fail(DG_ERR_INVALID, "dg_apply: pointers must be 8-byte aligned");
-    if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned");
-    if (((uintptr_t)x & 15) && c->tile) return fail(DG_ERR_INVALID, "dg_apply: x must be 16-byte aligned");
-    if ((((uintptr_t)x | (uintptr_t)xb | (uintptr_t)xa) & 15) && c->gen)
-        return fail(DG_ERR_INVALID, "dg_apply: x and the halo planes must be 16-byte aligned");
+    // alignment contract (include/dg.h): x, r and both halo planes 16-byte aligned for every kernel (vector /
+    // bulk-copy loads and stores); x 128-byte aligned for k_axis8 (TMA tensor map base)
+    if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 15)
+        return fail(DG_ERR_INVALID, "dg_apply: x, r, x_below and x_above must be 16-byte aligned");
+    if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned (k_axis8)");
     cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream, u0);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
     return DG_OK;
@@ -1139,12 +1075,16 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
     if (c->M.L != c->M.N0) return fail(DG_ERR_INVALID, "dg_apply_host: whole-mesh context required");
     CU(cudaSetDevice(c->device));
     const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
-    if (!c->hx_d) {
-        CU(cudaMalloc(&c->hx_d, bytes));
-        CU(cudaMalloc(&c->hr_d, bytes));
-        CU(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
-        CU(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
-        CU(cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking));
+    // staging state, created on first use and owned by the context (each piece only once, so a failed first
+    // call leaks nothing and a retry completes it; dg_destroy frees what exists)
+    if (!c->hx_d) CU(cudaMalloc(&c->hx_d, bytes));
+    if (!c->hr_d) CU(cudaMalloc(&c->hr_d, bytes));
+    if (!c->s_h2d) CU(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    if (!c->s_d2h) CU(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    if (!c->s_cmp) CU(cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking));
+    for (int i = 0; i < 8; ++i) {
+        if (!c->ev_in[i]) CU(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+        if (!c->ev_cmp[i]) CU(cudaEventCreateWithFlags(&c->ev_cmp[i], cudaEventDisableTiming));
     }
     const int L = c->M.L;
     const int64_t pd = c->plane_dofs;
@@ -1153,11 +1093,8 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
     const int nch = L >= 8 ? 8 : L;
     int bnd[9];
     for (int i = 0; i <= nch; ++i) bnd[i] = (int)((int64_t)L * i / nch);
-    cudaEvent_t ev_in[9], ev_cmp[9];
-    for (int i = 0; i < nch; ++i) {
-        CU(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&ev_cmp[i], cudaEventDisableTiming));
-    }
+    cudaEvent_t* ev_in = c->ev_in;
+    cudaEvent_t* ev_cmp = c->ev_cmp;
     // H2D: the last plane first (wrap halo of chunk 0), then chunks in order
     CU(cudaMemcpyAsync(c->hx_d + (size_t)(L - 1) * pd, xh + (size_t)(L - 1) * pd, pbytes, cudaMemcpyHostToDevice,
                        c->s_h2d));
@@ -1182,10 +1119,6 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
                            pbytes * (size_t)(bnd[i + 1] - bnd[i]), cudaMemcpyDeviceToHost, c->s_d2h));
     }
     CU(cudaStreamSynchronize(c->s_d2h));
-    for (int i = 0; i < nch; ++i) {
-        cudaEventDestroy(ev_in[i]);
-        cudaEventDestroy(ev_cmp[i]);
-    }
     return DG_OK;
 }
 

@@ -27,7 +27,7 @@
 #include <type_traits>
 
 #include "common.cuh"
-#include "kernel_tile.cuh" // k_geom / GREC records, tl:: mbarrier + bulk-copy helpers
+#include "kernel_geom.cuh" // k_geom / GREC records, tl:: mbarrier + bulk-copy helpers
 
 namespace dg {
 

@@ -119,6 +119,10 @@ def dg_setup(N, k: int, quad: int, *, plane_begin: int = 0, nplanes: int | None 
     m.geom_kind = geom_kind
     if jac is not None:
         jac = np.ascontiguousarray(jac, dtype=np.float64)
+        L_ = m.nplanes
+        need = 9 * (L_ + 2) * int(N[1]) * int(N[2])  # J of the L+2 planes plane_begin-1 .. plane_begin+L
+        if jac.size != need:
+            raise DgError(DG_ERR_INVALID, f"jac has {jac.size} doubles, the slab needs {need} (9 per cell of L+2 planes)")
         m.jac = jac.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     m.coeff_kind = coeff_kind
     m.penalty_scale = float(penalty_scale)
@@ -281,9 +285,11 @@ class Operator:
         return r
 
     def apply_host(self, x_host, r_host):
+        import torch
         for t in (x_host, r_host):
-            if t.is_cuda or t.numel() != self.ndofs or not t.is_contiguous():
-                raise DgError(DG_ERR_INVALID, "expected contiguous host tensors of local_ndofs entries")
+            if (t.is_cuda or t.dtype != torch.float64 or t.numel() != self.ndofs or not t.is_contiguous()
+                    or t.data_ptr() % 16):
+                raise DgError(DG_ERR_INVALID, "expected contiguous 16-B aligned float64 host tensors of local_ndofs entries")
         dg_apply_host(self.ctx, x_host, r_host)
         return r_host
 

@@ -175,10 +175,19 @@ class SlabOperator:
     def launches_per_apply(self) -> int:
         return self._apply.launches_per_apply
 
+    def _follow_current_stream(self):
+        """SlabApply orders the halo events on torch's current stream; the libdg launches must go to the same
+        stream (else a boundary-plane launch would not wait for the halo)."""
+        import torch
+        cur = torch.cuda.current_stream(self.op._stream.device)
+        if cur != self.op._stream:
+            self.op.set_stream(cur)
+
     def apply(self, x, r=None):
         import torch
         if r is None:
             r = torch.empty_like(x)
+        self._follow_current_stream()
         return self._apply(x, r)
 
     def apply_jacobian(self, u0, z, r=None):
@@ -187,6 +196,7 @@ class SlabOperator:
         import torch
         if r is None:
             r = torch.empty_like(z)
+        self._follow_current_stream()
         return self._apply(z, r, fn=lambda zz, zb, za, rr, a, b: self.op.apply_jacobian_planes(u0, zz, zb, za, rr, a, b))
 
     def close(self):
