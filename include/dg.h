@@ -102,10 +102,11 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out);
 
 /* r = A x for a context owning the WHOLE mesh (nplanes == N[0]).
  * x, r: caller-owned DEVICE pointers to dg_local_ndofs() doubles each, not overlapping (else
- * DG_ERR_INVALID). Alignment (else DG_ERR_INVALID, checked before any launch): x, r and the halo
- * planes of dg_apply_planes 16-byte aligned for every kernel (16-B vector / bulk-copy accesses);
- * x additionally 128-byte aligned when dg_kernel_name() is "k_axis8" (the TMA tensor map base).
- * cudaMalloc / PyTorch allocations satisfy both. r is overwritten (every entry written exactly once).
+ * DG_ERR_INVALID). Alignment (else DG_ERR_INVALID, checked before any launch): every pointer
+ * 8-byte aligned; x, r and the halo planes of dg_apply_planes 16-byte aligned when dg_kernel_name()
+ * is "k_gen" or "k_axis8" (16-B vector / bulk-copy accesses; their plane sizes are multiples of
+ * 16 B, so whole-mesh halos inside x qualify); x 128-byte aligned for "k_axis8" (the TMA tensor
+ * map base). cudaMalloc / PyTorch allocations satisfy all of these. r is overwritten (every entry written exactly once).
  * Asynchronous on the context stream; the caller synchronises. */
 int dg_apply(dg_ctx* ctx, const double* x, double* r);
 
@@ -128,7 +129,7 @@ int dg_apply_planes(dg_ctx* ctx, const double* x, const double* x_below, const d
  * u0 and z are evaluated at the quadrature points by the same sum-factorisation sweeps in one
  * kernel (k_quad mode 3). Arguments as dg_apply / dg_apply_planes (z takes x's place, z_below /
  * z_above its halo planes); u0: DEVICE, dg_local_ndofs() doubles of the owned planes only (the
- * Jacobian's u0-dependence is cell-local), 16-byte aligned, must not overlap r.
+ * Jacobian's u0-dependence is cell-local), 8-byte aligned, must not overlap r.
  * DG_ERR_UNSUPPORTED unless the context's problem is DG_PROBLEM_NLREAC. Asynchronous. */
 int dg_apply_jacobian(dg_ctx* ctx, const double* u0, const double* z, double* r);
 int dg_apply_jacobian_planes(dg_ctx* ctx, const double* u0, const double* z, const double* z_below,

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIBDIR, "libdg.so")
+LIB = os.environ.get("DG_LIB_OUT") or os.path.join(LIBDIR, "libdg.so")  # DG_LIB_OUT: experiment variants only
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["dg_capi.cu", "tables.cpp", "fp64_peak.cu"]
@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     extra = os.environ.get("DG_BUILD_FLAGS", "").split()  # experiments only (e.g. -DDG_AX8_TRACE)
     cmd = [NVCC] + ARCH + FLAGS + extra + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(LIBDIR, "build.log")
+    log = LIB + ".build.log" if os.environ.get("DG_LIB_OUT") else os.path.join(LIBDIR, "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:

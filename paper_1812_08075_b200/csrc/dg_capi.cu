@@ -1027,7 +1027,7 @@ int dg_apply_jacobian_planes(dg_ctx* c, const double* u0, const double* z, const
     const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
     const char *us = (const char*)u0, *rs = (const char*)r;
     if (r && us < rs + bytes && rs < us + bytes) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 and r overlap");
-    if ((uintptr_t)u0 & 15) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 must be 16-byte aligned");
+    if ((uintptr_t)u0 & 7) return fail(DG_ERR_INVALID, "dg_apply_jacobian: u0 must be 8-byte aligned");
     return apply_planes_impl(c, z, zb, za, r, p0, p1, u0);
 }
 
@@ -1049,10 +1049,13 @@ static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const
     const size_t bytes = sizeof(double) * (size_t)c->local_dofs;
     const char *xs = (const char*)x, *rs = (const char*)r;
     if (xs < rs + bytes && rs < xs + bytes) return fail(DG_ERR_INVALID, "dg_apply: x and r overlap");
-    // alignment contract (include/dg.h): x, r and both halo planes 16-byte aligned for every kernel (vector /
-    // bulk-copy loads and stores); x 128-byte aligned for k_axis8 (TMA tensor map base)
-    if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 15)
-        return fail(DG_ERR_INVALID, "dg_apply: x, r, x_below and x_above must be 16-byte aligned");
+    // alignment contract (include/dg.h): 8 bytes for every pointer; 16 bytes for x, r and both halo planes of the
+    // marching-tile kernels (k_gen, k_axis8: 16-B vector and bulk-copy accesses); x 128 bytes for k_axis8 (TMA
+    // tensor map base)
+    if (((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 7)
+        return fail(DG_ERR_INVALID, "dg_apply: pointers must be 8-byte aligned");
+    if ((((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 15) && (c->gen || c->ax8))
+        return fail(DG_ERR_INVALID, "dg_apply: x, r, x_below and x_above must be 16-byte aligned (%s)", c->kname);
     if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned (k_axis8)");
     cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream, u0);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));

@@ -1,6 +1,6 @@
 // K_gen: the general sum-factorised SIPG operator (any degree n = k+1 in 2..8, per-cell affine
 // geometry, c(x)) — the path of the affine configs (cfg2 Q5, cfg4 Q4) and of the axis-aligned
-// configs other than Q7. Successor of k_tile (kernel_tile.cuh) with the same mathematics:
+// configs other than Q7. Successor of the round-1 k_tile with the same mathematics:
 //
 //   Alg. assembly per cell, collocation (A = I, reading R8):
 //     stage 1  grad_hat U = (D along d) X,
@@ -11,8 +11,8 @@
 //
 // What is new against k_tile (design notes):
 //  * every global input of a plane step (own blocks of the NEXT plane, ring blocks, geometry
-//    records) arrives asynchronously one step ahead (cp.async.bulk + mbarrier; cp.async for the
-//    odd-sized single ring cells): the compute phases touch only shared memory and registers;
+//    records) arrives asynchronously one step ahead (cp.async.bulk + mbarrier; odd-sized ring
+//    cells as 16-B aligned pairs): the compute phases touch only shared memory and registers;
 //  * line sweeps in even/odd form (D is centro-antisymmetric on the symmetric Gauss nodes): about
 //    half the FMAs of a plain n x n product and half-length dependency chains;
 //  * faces are evaluated once per face (T- side owner), with the tangential parts of both sides
@@ -68,11 +68,6 @@ using tl::mbar_init;
 using tl::mbar_wait;
 using tl::s32;
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // split a line into even/odd halves
 template <int N>
@@ -195,7 +190,11 @@ struct Lay {
     static constexpr int NCG = NC + NRL;               // cells with geometry / c tables (own + ring below)
     // regions
     static constexpr int XS = 0;                                        // [2][NC][N3] own planes
-    static constexpr int RXSZ = (NRL + NRH) * N3;                       // ring blocks: bd1[T2] bd2[T1] ad1[T2] ad2[T1]
+    // ring blocks: bd1[T2] bd2[T1 slots] ad1[T2] ad2[T1 slots]; for odd n^3 a d = 2 ring slot holds the 16-B aligned
+    // PAIR of cells around the needed one (one bulk copy instead of per-element cp.async: N2, T2 even)
+    static constexpr int SL = (N3 % 2) == 0 ? 1 : 2;
+    static constexpr int RB1 = 0, RB2 = T2, RA1 = T2 + SL * T1, RA2 = 2 * T2 + SL * T1;
+    static constexpr int RXSZ = (2 * T2 + 2 * SL * T1) * N3;
     // affine face passes: per face line (N points per thread, 2 buffers, warp-local A -> B -> C) for n <= 6,
     // per face point (3 buffers, CTA barriers between the passes) for n >= 7
     static constexpr bool FACE_LINES = N <= 6;
@@ -419,35 +418,21 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
     };
     constexpr uint32_t GEOB = (AFFINE ? (uint32_t)(NCG * GREC * 8) : 0u) + (COEFF ? (uint32_t)((NC * CXSZ + NCG * CFSZ) * 8) : 0u);
-    // ring blocks of plane lp: rows via bulk copies on barB (thread 0), single d=2 cells via cp.async (all threads)
-    constexpr bool D2BULK = (N3 % 2) == 0;
+    // ring blocks of plane lp: bulk copies on barB (one thread); d = 2 ring cells singly (even n^3) or as aligned pairs
+    constexpr int SL = Y::SL;
+    auto ring_b2 = [&](int c1) { return RX + (Y::RB2 + SL * c1 + (SL - 1)) * N3; }; // ring cell below (i2) of tile row c1
+    auto ring_a2 = [&](int c1) { return RX + (Y::RA2 + SL * c1) * N3; };            // ring cell above (i2) of tile row c1
     auto issue_ring_bulk = [&](int lp) {
         const double* src = x + (long long)lp * PC * N3;
-        uint32_t bytes = 2 * ROWB + (D2BULK ? 2 * T1 * N3 * 8 : 0);
+        const uint32_t bytes = 2 * ROWB + 2 * T1 * SL * N3 * 8;
         gn::mbar_expect_tx(barB, bytes);
-        gn::bulk_g2s(RX, src + ((long long)wrap(ti1 * T1 - 1, M.N1) * M.N2 + ti2 * T2) * N3, ROWB, barB);
-        gn::bulk_g2s(RX + (T2 + T1) * N3, src + ((long long)wrap(ti1 * T1 + T1, M.N1) * M.N2 + ti2 * T2) * N3, ROWB, barB);
-        if (D2BULK) {
+        gn::bulk_g2s(RX + Y::RB1 * N3, src + ((long long)wrap(ti1 * T1 - 1, M.N1) * M.N2 + ti2 * T2) * N3, ROWB, barB);
+        gn::bulk_g2s(RX + Y::RA1 * N3, src + ((long long)wrap(ti1 * T1 + T1, M.N1) * M.N2 + ti2 * T2) * N3, ROWB, barB);
 #pragma unroll
-            for (int c1 = 0; c1 < T1; ++c1) {
-                const long long i1 = ti1 * T1 + c1;
-                gn::bulk_g2s(RX + (T2 + c1) * N3, src + (i1 * M.N2 + wrap(ti2 * T2 - 1, M.N2)) * N3, N3 * 8, barB);
-                gn::bulk_g2s(RX + (2 * T2 + T1 + c1) * N3, src + (i1 * M.N2 + wrap(ti2 * T2 + T2, M.N2)) * N3, N3 * 8, barB);
-            }
-        }
-    };
-    auto issue_ring_cp = [&](int lp) {
-        if (!D2BULK) {
-            const double* src = x + (long long)lp * PC * N3;
-            for (int t = tid; t < 2 * T1 * N3; t += NT) {
-                const int k = t / N3, e = t % N3, c1 = k % T1;
-                const bool above = k >= T1;
-                const long long i1 = ti1 * T1 + c1;
-                const int i2 = above ? wrap(ti2 * T2 + T2, M.N2) : wrap(ti2 * T2 - 1, M.N2);
-                double* dst = RX + ((above ? 2 * T2 + T1 : T2) + c1) * N3 + e;
-                gn::cp_async8(dst, src + (i1 * M.N2 + i2) * N3 + e);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int c1 = 0; c1 < T1; ++c1) {
+            const long long i1 = ti1 * T1 + c1;
+            gn::bulk_g2s(RX + (Y::RB2 + SL * c1) * N3, src + (i1 * M.N2 + wrap(ti2 * T2 - SL, M.N2)) * N3, SL * N3 * 8, barB);
+            gn::bulk_g2s(RX + (Y::RA2 + SL * c1) * N3, src + (i1 * M.N2 + wrap(ti2 * T2 + T2, M.N2)) * N3, SL * N3 * 8, barB);
         }
     };
 
@@ -741,13 +726,13 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto foreign = [&](const double* XN) {
         for (int t = tid; t < 2 * T2 * N2; t += NT) {
             const int k = t / N2, p = t - k * N2;
-            if (k < T2) trace_task(std::integral_constant<int, 1>{}, RX + k * N3, p, 3 * NC + k, 0);
-            else trace_task(std::integral_constant<int, 1>{}, RX + (T1 + k) * N3, p, 3 * ((T1 - 1) * T2 + k - T2) + 1, 1);
+            if (k < T2) trace_task(std::integral_constant<int, 1>{}, RX + (Y::RB1 + k) * N3, p, 3 * NC + k, 0);
+            else trace_task(std::integral_constant<int, 1>{}, RX + (Y::RA1 + k - T2) * N3, p, 3 * ((T1 - 1) * T2 + k - T2) + 1, 1);
         }
         for (int t = tid; t < 2 * T1 * N2; t += NT) {
             const int k = t / N2, p = t - k * N2;
-            if (k < T1) trace_task(std::integral_constant<int, 2>{}, RX + (T2 + k) * N3, p, 3 * NC + T2 + k, 0);
-            else trace_task(std::integral_constant<int, 2>{}, RX + (2 * T2 + k) * N3, p, 3 * ((k - T1) * T2 + T2 - 1) + 2, 1);
+            if (k < T1) trace_task(std::integral_constant<int, 2>{}, ring_b2(k), p, 3 * NC + T2 + k, 0);
+            else trace_task(std::integral_constant<int, 2>{}, ring_a2(k - T1), p, 3 * ((k - T1) * T2 + T2 - 1) + 2, 1);
         }
         for (int t = tid; t < NC * N2; t += NT) {
             const int q = t / N2, p = t - q * N2;
@@ -825,7 +810,6 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             if (AFFINE || COEFF) issue_geo(p_begin, 0);
             issue_ring_bulk(p_begin);
         }
-        issue_ring_cp(p_begin);
     }
 
     for (int s = 0; s < nsteps; ++s) {
@@ -836,7 +820,6 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         GEN_STAMP(0);
         gn::mbar_wait(barA, (s + 1) & 1);
         gn::mbar_wait(barB, s & 1);
-        if (!D2BULK) gn::cp_async_wait_all();
         __syncthreads();
         GEN_STAMP(1);
 
@@ -868,7 +851,6 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                     issue_x(lp + 2, XS + (s & 1) * NC * N3);
                     issue_ring_bulk(lp + 1);
                 }
-                issue_ring_cp(lp + 1);
             }
             // ---- L2: line operators; directions 0, 1 -> shared memory, 2 -> registers ----
             double y2[N];
@@ -1025,7 +1007,6 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         // the ring buffer (aliased by the face buffers) is free: stream the next plane's ring blocks
         if (s + 1 < nsteps) {
             if (tid == PROD) issue_ring_bulk(lp + 1);
-            issue_ring_cp(lp + 1);
         }
 
         // ---------------- P5: stage 3 + face back-projection; d = 0, 1 in place, d = 2 -> r ----------------

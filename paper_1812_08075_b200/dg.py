@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdg.so")
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(_HERE, "lib", "libdg.so")  # DG_LIB: experiment variants only
 
 DG_OK = 0
 DG_ERR_INVALID = -1
