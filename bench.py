@@ -307,6 +307,10 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
+        # NCCL's own init lines (transport, rings / channels over NVLink) on stderr: the communicator the halo
+        # exchange uses is visible in the run log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,P2P")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -518,6 +522,13 @@ def main():
 
     # ---- sanity of the timed result (not a parity claim: tests/ do that): finite, nonzero
     ok = bool(torch.isfinite(r).all().item()) and r.abs().max().item() > 0
+    halo = None
+    if world > 1:
+        ap = sop._apply
+        halo = {"payload": "face traces (u, d_0 u at the n^2 face points, dg_pack_halo)" if ap.traces else "boundary planes",
+                "bytes_per_message": 8 * ap.payload_doubles, "messages_per_rank": 4,
+                "overlap": "interior planes on the compute stream while the exchange runs on a high-priority stream; "
+                           "NVTX ranges slab:pack / slab:interior / slab:halo / slab:boundary"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -529,6 +540,8 @@ def main():
                       "value": w.ndofs / (sustained_ms * 1e-3), "l2": "warm" if flush is not None else "cold (vectors > L2)"},
         "warm_ms_per_step": warm_ms,
     }
+    if halo:
+        line["halo"] = halo
     if args.solve and world == 1 and w.problem == 1:
         from paper_1812_08075_b200 import solve as _solve
         res = _solve.solve_residual(op, sop.ndofs, device=dev, graph=True, timed_iterations=K)

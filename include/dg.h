@@ -122,6 +122,23 @@ int dg_apply(dg_ctx* ctx, const double* x, double* r);
 int dg_apply_planes(dg_ctx* ctx, const double* x, const double* x_below, const double* x_above, double* r,
                     int p_begin, int p_end);
 
+/* Traces-only halo exchange for the x0-slab decomposition (the "traces only" payload): the
+ * face between slabs needs from the neighbour only u and d_0 u at the n^2 face points of each boundary cell
+ * (the 1-point face tables e0/e1, d0/d1 of P:L143-146 applied along the d = 0 lines), 2 n^2 instead of
+ * n^3 doubles per cell (cfg3: 4x less, cfg4: 2.5x less).
+ * dg_halo_ndofs: doubles of one trace halo, N1 N2 2 n^2 (per cell u[n^2] then d_0 u[n^2], point j1 + n j2).
+ * dg_pack_halo: from the slab's x (DEVICE, dg_local_ndofs doubles) write tr_lo = the lower-end traces (e0.x,
+ *   d0.x) of the first local plane (the lower neighbour's tr_above) and tr_hi = the upper-end traces (e1.x,
+ *   d1.x) of the last local plane (the upper neighbour's tr_below); DEVICE, dg_halo_ndofs doubles each, 16-byte
+ *   aligned. Asynchronous on the context stream.
+ * dg_apply_planes_tr: dg_apply_planes with the two halo planes replaced by trace halos as produced by the
+ *   neighbours' dg_pack_halo (16-byte aligned). Interior plane ranges never read them.
+ * Both return DG_ERR_UNSUPPORTED unless dg_kernel_name() is "k_gen" or "k_axis8". */
+int64_t dg_halo_ndofs(const dg_ctx* ctx);
+int dg_pack_halo(dg_ctx* ctx, const double* x, double* tr_lo, double* tr_hi);
+int dg_apply_planes_tr(dg_ctx* ctx, const double* x, const double* tr_below, const double* tr_above, double* r,
+                       int p_begin, int p_end);
+
 /* The action of the Jacobian of a DG_PROBLEM_NLREAC residual at the linearization point u0
  * ("not only the solution needs to be evaluated in step 1 ... but also the given
  * linearization point"; A_i(c, z) = (J z)_i, depending on both c and z):

@@ -116,13 +116,13 @@ template <> struct GenShape<7> { static constexpr int T1 = 2, T2 = 2, MINB = 1; 
 template <> struct GenShape<8> { static constexpr int T1 = 2, T2 = 2, MINB = 1; };
 
 using GenFn = cudaError_t (*)(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                              double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo,
+                              double* r, int p0, int p1, int chunk, int halo_tr, cudaStream_t st, const double* geo,
                               const double* ctab, const double* cface);
 
 template <int N, bool AFF, bool COEF>
 cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
-                       double* r, int p0, int p1, int chunk, cudaStream_t st, const double* geo, const double* ctab,
-                       const double* cface)
+                       double* r, int p0, int p1, int chunk, int halo_tr, cudaStream_t st, const double* geo,
+                       const double* ctab, const double* cface)
 {
     constexpr int T1 = GenShape<N>::T1, T2 = GenShape<N>::T2, MB = GenShape<N>::MINB;
     using Y = dg::gn::Lay<N, AFF, COEF, T1, T2>;
@@ -131,7 +131,7 @@ cudaError_t launch_gen(const void* eot, const dg::MeshArgs& M, const double* x, 
     const int CL = chunk > 0 && chunk < np ? chunk : np;
     const unsigned grid = (unsigned)((M.N1 / T1) * (M.N2 / T2) * ((np + CL - 1) / CL));
     dg::k_gen<N, AFF, COEF, T1, T2, MB><<<grid, Y::NT, Y::BYTES, st>>>(
-        x, xb, xa, r, p0, p1, CL, *static_cast<const dg::EOTab<N>*>(eot), M, geo, ctab, cface);
+        x, xb, xa, r, p0, p1, CL, halo_tr, *static_cast<const dg::EOTab<N>*>(eot), M, geo, ctab, cface);
     return cudaGetLastError();
 }
 
@@ -533,7 +533,7 @@ struct dg_ctx {
 };
 
 static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0,
-                                 int p1, cudaStream_t st, const double* u0 = nullptr)
+                                 int p1, cudaStream_t st, const double* u0 = nullptr, int halo_tr = 0)
 {
     if (p1 <= p0) return cudaSuccess;
     if (u0) { // the Jacobian action of the nonlinear variant (dg_apply_jacobian*)
@@ -560,7 +560,7 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
 #define AX8_LAUNCH(ID, T1, T2, NT, MB)                                                                               \
     case ID:                                                                                                         \
         dg::k_axis8<T1, T2, NT, MB><<<grid, NT, dg::ax8::Cfg<T1, T2, NT>::SMEM_BYTES, st>>>(c->tmap, x, xb, xa, r, p0, p1, \
-                                                                                          CL, c->atab, c->M, c->dbg); \
+                                                                                          CL, halo_tr, c->atab, c->M, c->dbg); \
         break;
             AX8_VARIANTS(AX8_LAUNCH)
 #undef AX8_LAUNCH
@@ -575,7 +575,8 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
         const long long pcq = c->M.plane_cells;
         return c->launch(c->qtab, c->M, x, xb, xa, r, (long long)p0 * pcq, (long long)p1 * pcq, st, nullptr);
     }
-    if (c->gen) return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, st, c->d_geo, c->d_ctab, c->d_cface);
+    if (c->gen)
+        return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, halo_tr, st, c->d_geo, c->d_ctab, c->d_cface);
     const long long pc = c->M.plane_cells;
     return c->launch(c->tab, c->M, x, xb, xa, r, (long long)p0 * pc, (long long)p1 * pc, st, nullptr);
 }
@@ -1010,11 +1011,49 @@ double dg_alg_bytes(const dg_ctx* c)
 }
 
 static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1,
-                             const double* u0);
+                             const double* u0, int halo_tr = 0);
 
 int dg_apply_planes(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1)
 {
     return apply_planes_impl(c, x, xb, xa, r, p0, p1, nullptr);
+}
+
+int64_t dg_halo_ndofs(const dg_ctx* c) { return c ? (int64_t)c->M.plane_cells * 2 * c->n * c->n : -1; }
+
+int dg_apply_planes_tr(dg_ctx* c, const double* x, const double* tr_below, const double* tr_above, double* r, int p0,
+                       int p1)
+{
+    if (!c) return fail(DG_ERR_INVALID, "dg_apply_planes_tr: NULL ctx");
+    if (!(c->gen || c->ax8))
+        return fail(DG_ERR_UNSUPPORTED, "dg_apply_planes_tr: trace halos need k_gen or k_axis8 (context kernel %s)", c->kname);
+    return apply_planes_impl(c, x, tr_below, tr_above, r, p0, p1, nullptr, 3);
+}
+
+int dg_pack_halo(dg_ctx* c, const double* x, double* tr_lo, double* tr_hi)
+{
+    if (!c || !x || !tr_lo || !tr_hi) return fail(DG_ERR_INVALID, "dg_pack_halo: NULL argument");
+    if (!(c->gen || c->ax8))
+        return fail(DG_ERR_UNSUPPORTED, "dg_pack_halo: trace halos need k_gen or k_axis8 (context kernel %s)", c->kname);
+    if (((uintptr_t)x | (uintptr_t)tr_lo | (uintptr_t)tr_hi) & 15)
+        return fail(DG_ERR_INVALID, "dg_pack_halo: pointers must be 16-byte aligned");
+    const long long tot = 2LL * c->M.plane_cells * c->n * c->n;
+    const unsigned g = (unsigned)((tot + 255) / 256);
+    if (c->ax8) {
+        dg::k_pack_traces8<<<g, 256, 0, c->stream>>>(x, tr_lo, tr_hi, c->M.plane_cells, c->M.L, c->atab);
+    } else {
+        switch (c->n) {
+#define PACK_CASE(NN)                                                                                                  \
+    case NN:                                                                                                           \
+        dg::k_pack_traces<NN><<<g, 256, 0, c->stream>>>(x, tr_lo, tr_hi, c->M.plane_cells, c->M.L,                     \
+                                                         *reinterpret_cast<const dg::EOTab<NN>*>(c->eotab));             \
+        break;
+            PACK_CASE(2) PACK_CASE(3) PACK_CASE(4) PACK_CASE(5) PACK_CASE(6) PACK_CASE(7) PACK_CASE(8)
+#undef PACK_CASE
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_pack_halo: launch: %s", cudaGetErrorString(e));
+    return DG_OK;
 }
 
 int dg_apply_jacobian_planes(dg_ctx* c, const double* u0, const double* z, const double* zb, const double* za, double* r,
@@ -1042,7 +1081,7 @@ int dg_apply_jacobian(dg_ctx* c, const double* u0, const double* z, double* r)
 }
 
 static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const double* xa, double* r, int p0, int p1,
-                             const double* u0)
+                             const double* u0, int halo_tr)
 {
     if (!c || !x || !xb || !xa || !r) return fail(DG_ERR_INVALID, "dg_apply_planes: NULL argument");
     if (p0 < 0 || p1 > c->M.L || p0 > p1) return fail(DG_ERR_INVALID, "dg_apply_planes: planes [%d,%d) of %d", p0, p1, c->M.L);
@@ -1057,7 +1096,7 @@ static int apply_planes_impl(dg_ctx* c, const double* x, const double* xb, const
     if ((((uintptr_t)x | (uintptr_t)r | (uintptr_t)xb | (uintptr_t)xa) & 15) && (c->gen || c->ax8))
         return fail(DG_ERR_INVALID, "dg_apply: x, r, x_below and x_above must be 16-byte aligned (%s)", c->kname);
     if (((uintptr_t)x & 127) && c->ax8) return fail(DG_ERR_INVALID, "dg_apply: x must be 128-byte aligned (k_axis8)");
-    cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream, u0);
+    cudaError_t e = launch_planes(c, x, xb, xa, r, p0, p1, c->stream, u0, halo_tr);
     if (e != cudaSuccess) return fail(DG_ERR_CUDA, "dg_apply: launch: %s", cudaGetErrorString(e));
     return DG_OK;
 }

@@ -264,11 +264,48 @@ __device__ __forceinline__ double inplane_scale(const AxisTab8& A, int tid)
 
 } // namespace ax8
 
+// Halo traces of a slab for k_axis8 contexts (dg_pack_halo): lower-end (e0.x, d0.x) of the first plane's d = 0
+// lines, upper-end (e1.x, d1.x) of the last plane's, with k_axis8's own even/odd trace algebra (bitwise the values
+// its pass d = 0 computes from a block halo); per cell u[64] then d_0 u[64], line L = j1 + 8 j2.
+__global__ void k_pack_traces8(const double* __restrict__ x, double* __restrict__ lo, double* __restrict__ hi,
+                               int plane_cells, int L, const AxisTab8 A)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2LL * plane_cells * 64) return;
+    const int side = (int)(t / ((long long)plane_cells * 64));
+    const long long rem = t - (long long)side * plane_cells * 64;
+    const long long c = rem / 64;
+    const int l = (int)(rem - c * 64);
+    const double* src = x + ((long long)(side ? L - 1 : 0) * plane_cells + c) * 512 + 8 * l;
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldg(src + j);
+    double* o = (side ? hi : lo) + c * 128;
+    if (side) { // upper end: pass d = 0 carries these from the even/odd traces of the plane's own lines
+        double xe[4], xo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
+        double u0, u1, g0, g1;
+        ax8::traces_eo(A, xe, xo, u0, u1, g0, g1);
+        o[l] = u1;
+        o[64 + l] = g1;
+    } else {    // lower end: pass d = 0 sums e0.x, d0.x of the next plane's line directly
+        double u = 0.0, g = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            u = fma(A.e0[j], v[j], u);
+            g = fma(A.d0[j], v[j], g);
+        }
+        o[l] = u;
+        o[64 + l] = g;
+    }
+}
+
 // grid: (N1/T1) * (N2/T2) CTAs, block NT, dynamic smem Cfg::SMEM_BYTES
 template <int T1, int T2, int NT, int MB = ax8::Cfg<T1, T2, NT>::MINB>
 __global__ void __launch_bounds__(NT, MB)
 k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, const double* __restrict__ xb,
-        const double* __restrict__ xa, double* __restrict__ r, int p_begin, int p_end, int chunk_len,
+        const double* __restrict__ xa, double* __restrict__ r, int p_begin, int p_end, int chunk_len, int halo_tr,
         const AxisTab8 A, const MeshArgs M, long long* __restrict__ dbg)
 {
     using namespace ax8;
@@ -347,7 +384,15 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
     }
 
     double prevU[LPT], prevG[LPT]; // traces e1.x, d1.x of the lower x0-neighbour, per d=0 line
-    {
+    if (p_begin == 0 && (halo_tr & 1)) {
+        // halo below given as traces (dg_apply_planes_tr): per cell u[64] then d_0 u[64] at the d = 0 face points
+#pragma unroll
+        for (int q = 0; q < LPT; ++q) {
+            const int L = lane + 32 * q + lbase;
+            prevU[q] = __ldg(xb + d0_inplane * 128 + L);
+            prevG[q] = __ldg(xb + d0_inplane * 128 + 64 + L);
+        }
+    } else {
         const double* src = (p_begin == 0) ? xb + d0_inplane * 512 : x + (cell_index(p_begin - 1, 0, 0) + d0_inplane) * 512;
 #pragma unroll
         for (int q = 0; q < LPT; ++q) {
@@ -407,7 +452,10 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
                 const int L = lane + 32 * q + lbase;
                 // upper neighbour's traces e0.x, d0.x
                 double uR = 0.0, gR = 0.0;
-                {
+                if (last && p_end == M.L && (halo_tr & 2)) {
+                    uR = __ldg(xa + d0_inplane * 128 + L); // halo above as traces (e0.x, d0.x)
+                    gR = __ldg(xa + d0_inplane * 128 + 64 + L);
+                } else {
                     double v[8];
                     if (!last) {
                         const uint32_t nb = XN + cb * CELL_BYTES;

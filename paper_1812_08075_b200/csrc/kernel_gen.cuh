@@ -291,6 +291,35 @@ __global__ void k_cface(const double* __restrict__ jac, double* __restrict__ out
     out[t] = 1.0 + 0.5 * sinpi(2.0 * x0) * cospi(2.0 * x1);
 }
 
+// Halo traces of a slab (dg_pack_halo, SURVEY §8(e) traces-only payload): for every cell of the slab's first
+// plane the lower-end traces (e0.x, d0.x) of its d = 0 lines, for its last plane the upper-end traces (e1.x,
+// d1.x) — the 1-point face tables of, computed with the same even/odd line algebra as k_gen so that a
+// neighbour consuming them reproduces the block-halo result bit for bit. Layout per cell: u[N2] then d_0 u[N2],
+// point p = j1 + N j2 (the d = 0 face point order of the kernels).
+template <int N>
+__global__ void k_pack_traces(const double* __restrict__ x, double* __restrict__ lo, double* __restrict__ hi, int plane_cells,
+                              int L, const EOTab<N> E)
+{
+    constexpr int N2 = N * N, N3 = N * N * N, H = EOTab<N>::H, HE = EOTab<N>::HE;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2LL * plane_cells * N2) return;
+    const int side = (int)(t / ((long long)plane_cells * N2)); // 0: first plane -> lo, 1: last plane -> hi
+    const long long rem = t - (long long)side * plane_cells * N2;
+    const long long c = rem / N2;
+    const int p = (int)(rem - c * N2), a = p % N, b = p / N;
+    const double* blk = x + ((long long)(side ? L - 1 : 0) * plane_cells + c) * N3;
+    double v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = blk[pidx<N>(0, j, a, b)];
+    double xe[HE], xo[H > 0 ? H : 1];
+    gn::split<N>(v, xe, xo);
+    double ulo, glo, uhi, ghi;
+    gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
+    double* o = (side ? hi : lo) + c * 2 * N2;
+    o[p] = side ? uhi : ulo;
+    o[N2 + p] = side ? ghi : glo;
+}
+
 #ifdef DG_GEN_TRACE
 // phase timestamps (experiments only): [block < 1024][step < 16][8] clock64 values, thread 0
 __device__ long long* g_gen_dbg = nullptr;
@@ -306,7 +335,7 @@ __device__ long long* g_gen_dbg = nullptr;
 template <int N, bool AFFINE, bool COEFF, int T1, int T2, int MINB>
 __global__ void __launch_bounds__(gn::Lay<N, AFFINE, COEFF, T1, T2>::NT, MINB)
 k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double* __restrict__ xa, double* __restrict__ r,
-      int p_begin, int p_end, int chunk_len, const EOTab<N> E, const MeshArgs M, const double* __restrict__ geo,
+      int p_begin, int p_end, int chunk_len, int halo_tr, const EOTab<N> E, const MeshArgs M, const double* __restrict__ geo,
       const double* __restrict__ ctab, const double* __restrict__ cface)
 {
     using Y = gn::Lay<N, AFFINE, COEFF, T1, T2>;
@@ -352,6 +381,9 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto cidx = [&](int lp, int i1, int i2) -> long long { return (long long)lp * PC + (long long)i1 * M.N2 + i2; };
     // source of plane lp's blocks (-1: halo below, L: halo above), and of its geometry records (L+2 planes from -1)
     auto xplane = [&](int lp) -> const double* { return lp < 0 ? xb : (lp >= M.L ? xa : x + (long long)lp * PC * N3); };
+    // halo_tr bit 0 / 1: the halo plane below / above is given as its face traces only (dg_apply_planes_tr): per
+    // cell of the plane, u[N2] then d_0 u[N2] at the d = 0 face points (upper end below, lower end above)
+    auto is_tr = [&](int lp) { return (lp < 0 && (halo_tr & 1)) || (lp >= M.L && (halo_tr & 2)); };
     auto grec = [&](int lp, int i1, int i2) -> const double* { return geo + (cidx(lp + 1, i1, i2)) * GREC; };
     // face slots: (u, gn) -> (V, G) pairs per face f, side (0: T-, 1: T+), point p
     // TRp(f, side)[p]: (.x = u / V, .y = gn / G) of face f, side, point p, stored in separate arrays
@@ -393,8 +425,16 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
 
     // ---------------- async staging ----------------
     constexpr uint32_t ROWB = T2 * N3 * 8;
-    auto issue_x = [&](int lp, double* dst) { // own blocks of plane lp (T1 rows) on barA (caller adds expect_tx)
+    constexpr uint32_t ROWT = T2 * 2 * N2 * 8; // a tile row of halo traces
+    auto xbytes = [&](int lp) -> uint32_t { return is_tr(lp) ? T1 * ROWT : T1 * ROWB; };
+    auto issue_x = [&](int lp, double* dst) { // own blocks (or halo traces) of plane lp (T1 rows) on barA (caller: expect_tx)
         const double* src = xplane(lp);
+        if (is_tr(lp)) {
+#pragma unroll
+            for (int c1 = 0; c1 < T1; ++c1)
+                gn::bulk_g2s(dst + c1 * T2 * 2 * N2, src + ((long long)(ti1 * T1 + c1) * M.N2 + ti2 * T2) * 2 * N2, ROWT, barA);
+            return;
+        }
 #pragma unroll
         for (int c1 = 0; c1 < T1; ++c1)
             gn::bulk_g2s(dst + c1 * T2 * N3, src + ((long long)(ti1 * T1 + c1) * M.N2 + ti2 * T2) * N3, ROWB, barA);
@@ -723,7 +763,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         gn::traces<N>(E, xe, xo, ulo, glo, uhi, ghi);
         TRp(f, side)[p] = side ? make_double2(ulo, glo) : make_double2(uhi, ghi); // T- faces the tile with its upper end
     };
-    auto foreign = [&](const double* XN) {
+    auto foreign = [&](const double* XN, bool xn_tr) {
         for (int t = tid; t < 2 * T2 * N2; t += NT) {
             const int k = t / N2, p = t - k * N2;
             if (k < T2) trace_task(std::integral_constant<int, 1>{}, RX + (Y::RB1 + k) * N3, p, 3 * NC + k, 0);
@@ -736,7 +776,12 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
         for (int t = tid; t < NC * N2; t += NT) {
             const int q = t / N2, p = t - q * N2;
-            trace_task(std::integral_constant<int, 0>{}, XN + q * N3, p, 3 * q, 1);
+            if (xn_tr) { // halo above given as traces (u, d_0 u at the lower end)
+                const double* tb = XN + q * 2 * N2;
+                TRp(3 * q, 1)[p] = make_double2(tb[p], tb[N2 + p]);
+            } else {
+                trace_task(std::integral_constant<int, 0>{}, XN + q * N3, p, 3 * q, 1);
+            }
         }
     };
 
@@ -744,7 +789,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     double pendV = 0.0, pendG = 0.0; // T+ half of the d=0 face below the thread's line (a, b) of cell mc
     {
         if (tid == PROD) {
-            gn::mbar_expect_tx(barA, 2 * T1 * ROWB + GEOB);
+            gn::mbar_expect_tx(barA, xbytes(p_begin - 1) + xbytes(p_begin) + GEOB);
             issue_x(p_begin - 1, XS + NC * N3);
             issue_x(p_begin, XS);
             if (AFFINE || COEFF) issue_geo(p_begin - 1, 1);
@@ -753,14 +798,24 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         cxcur = CX + NC * CXSZ;
         cfcur = CF + NCG * CFSZ;
         // T- upper-end traces (plane p_begin - 1) -> TR(3c, 0), T+ lower-end traces (plane p_begin) -> TR(3c, 1)
+        const bool below_tr = is_tr(p_begin - 1);
         for (int t = tid; t < NC * N2; t += NT) {
             const int c = t / N2, p = t - c * N2;
-            trace_task(std::integral_constant<int, 0>{}, XS + NC * N3 + c * N3, p, 3 * c, 0);
+            if (below_tr) { // the halo's traces as received (u, d_0 u at the upper end of each d = 0 line)
+                const double* tb = XS + NC * N3 + c * 2 * N2;
+                TRp(3 * c, 0)[p] = make_double2(tb[p], tb[N2 + p]);
+            } else {
+                trace_task(std::integral_constant<int, 0>{}, XS + NC * N3 + c * N3, p, 3 * c, 0);
+            }
             trace_task(std::integral_constant<int, 0>{}, XS + c * N3, p, 3 * c, 1);
         }
         if (LINEOP) {
             // the lower neighbour's (e1.x, d1.x) of the thread's d=0 line, from plane p_begin - 1
-            if (act) {
+            if (act && below_tr) {
+                const double* tb = XS + NC * N3 + mc * 2 * N2;
+                pendV = tb[mab];
+                pendG = tb[N2 + mab];
+            } else if (act) {
                 double v[N];
 #pragma unroll
                 for (int j = 0; j < N; ++j) v[j] = XS[NC * N3 + mc * N3 + pidx<N>(0, j, ma, mb)];
@@ -805,7 +860,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         }
         __syncthreads();
         if (tid == PROD) {
-            gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
+            gn::mbar_expect_tx(barA, xbytes(p_begin + 1) + GEOB);
             issue_x(p_begin + 1, XS + NC * N3);
             if (AFFINE || COEFF) issue_geo(p_begin, 0);
             issue_ring_bulk(p_begin);
@@ -843,11 +898,11 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                     if (d == 2) TRp(flo2, 1)[mab] = make_double2(ulo, glo);
                 }
             }
-            foreign(XN);
+            foreign(XN, is_tr(lp + 1));
             __syncthreads();
             if (s + 1 < nsteps) { // own plane buffer and ring buffer are free
                 if (tid == PROD) {
-                    gn::mbar_expect_tx(barA, T1 * ROWB);
+                    gn::mbar_expect_tx(barA, xbytes(lp + 2));
                     issue_x(lp + 2, XS + (s & 1) * NC * N3);
                     issue_ring_bulk(lp + 1);
                 }
@@ -919,7 +974,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 }
             }
         }
-        foreign(XN);
+        foreign(XN, is_tr(lp + 1));
         cxcur = CX + (s & 1) * NC * CXSZ;
         cfcur = CF + (s & 1) * NCG * CFSZ;
         __syncthreads();
@@ -927,7 +982,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
 
         // stream the next step's own blocks (plane lp + 2) and geometry (plane lp + 1) behind the compute
         if (tid == PROD && s + 1 < nsteps) {
-            gn::mbar_expect_tx(barA, T1 * ROWB + GEOB);
+            gn::mbar_expect_tx(barA, xbytes(lp + 2) + GEOB);
             issue_x(lp + 2, XS + (s & 1) * NC * N3);
             if (AFFINE || COEFF) issue_geo(lp + 1, (s + 1) & 1);
         }

@@ -55,7 +55,7 @@ class dg_mesh(ctypes.Structure):
 EXPORTS = ["dg_setup", "dg_apply", "dg_apply_planes", "dg_apply_host", "dg_destroy", "dg_set_stream",
            "dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs", "dg_alg_flops", "dg_alg_bytes",
            "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops",
-           "dg_apply_jacobian", "dg_apply_jacobian_planes"]
+           "dg_apply_jacobian", "dg_apply_jacobian_planes", "dg_halo_ndofs", "dg_pack_halo", "dg_apply_planes_tr"]
 
 _lib = None
 
@@ -73,12 +73,14 @@ def load(path: str = LIB_PATH):
     L.dg_setup.argtypes = [ctypes.POINTER(dg_mesh), ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.dg_apply.argtypes = [vp, vp, vp]
     L.dg_apply_planes.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
+    L.dg_apply_planes_tr.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
+    L.dg_pack_halo.argtypes = [vp, vp, vp, vp]
     L.dg_apply_host.argtypes = [vp, vp, vp]
     L.dg_apply_jacobian.argtypes = [vp, vp, vp, vp]
     L.dg_apply_jacobian_planes.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
     L.dg_destroy.argtypes = [vp]
     L.dg_set_stream.argtypes = [vp, vp]
-    for f in ("dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs"):
+    for f in ("dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs", "dg_halo_ndofs"):
         getattr(L, f).argtypes = [vp]
         getattr(L, f).restype = ctypes.c_int64
     for f in ("dg_alg_flops", "dg_alg_bytes"):
@@ -140,6 +142,18 @@ def dg_apply(ctx: int, x, r):
 
 def dg_apply_planes(ctx: int, x, x_below, x_above, r, p_begin: int, p_end: int):
     _check(load().dg_apply_planes(ctx, _ptr(x), _ptr(x_below), _ptr(x_above), _ptr(r), p_begin, p_end))
+
+
+def dg_apply_planes_tr(ctx: int, x, tr_below, tr_above, r, p_begin: int, p_end: int):
+    _check(load().dg_apply_planes_tr(ctx, _ptr(x), _ptr(tr_below), _ptr(tr_above), _ptr(r), p_begin, p_end))
+
+
+def dg_pack_halo(ctx: int, x, tr_lo, tr_hi):
+    _check(load().dg_pack_halo(ctx, _ptr(x), _ptr(tr_lo), _ptr(tr_hi)))
+
+
+def dg_halo_ndofs(ctx: int) -> int:
+    return load().dg_halo_ndofs(ctx)
 
 
 def dg_apply_jacobian(ctx: int, u0, z, r):
@@ -234,6 +248,7 @@ class Operator:
         self.ndofs = dg_local_ndofs(self.ctx)
         self.offset = dg_local_offset(self.ctx)
         self.plane_ndofs = dg_plane_ndofs(self.ctx)
+        self.halo_ndofs = dg_halo_ndofs(self.ctx)
         self.nplanes = self.ndofs // self.plane_ndofs
 
     def _chk(self, t, n=None):
@@ -283,6 +298,23 @@ class Operator:
         self._chk(x_above, self.plane_ndofs)
         dg_apply_planes(self.ctx, x, x_below, x_above, r, p_begin, p_end)
         return r
+
+    def apply_planes_tr(self, x, tr_below, tr_above, r, p_begin: int, p_end: int):
+        """dg_apply_planes with trace halos (include/dg.h)."""
+        self._chk(x)
+        self._chk(r)
+        self._chk(tr_below, self.halo_ndofs)
+        self._chk(tr_above, self.halo_ndofs)
+        dg_apply_planes_tr(self.ctx, x, tr_below, tr_above, r, p_begin, p_end)
+        return r
+
+    def pack_halo(self, x, tr_lo, tr_hi):
+        """The slab's boundary traces for the neighbours (dg_pack_halo)."""
+        self._chk(x)
+        self._chk(tr_lo, self.halo_ndofs)
+        self._chk(tr_hi, self.halo_ndofs)
+        dg_pack_halo(self.ctx, x, tr_lo, tr_hi)
+        return tr_lo, tr_hi
 
     def apply_host(self, x_host, r_host):
         import torch
