@@ -171,7 +171,7 @@ int64_t dg_plane_ndofs(const dg_ctx* ctx);  /* N1 N2 n^3: size of one x0-plane (
 
 /* Algorithmic work of one application over the local slab:
  * flops = F_alg(n) * local DOFs, with F_alg the collocated sum-factorisation count with
- * each face once; bytes = 16 B per DOF (read x, write r) + geometry bytes. */
+ * each face once; bytes = 16 B per DOF (read x, write r) + 120 B per affine cell (J, G~). */
 double dg_alg_flops(const dg_ctx* ctx);
 double dg_alg_bytes(const dg_ctx* ctx);
 

@@ -46,4 +46,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--bounds" in sys.argv:
+        # bounds-checked debug library (-DDG_BOUNDS) next to the release one; select it with DG_LIB
+        os.environ["DG_BUILD_FLAGS"] = (os.environ.get("DG_BUILD_FLAGS", "") + " -DDG_BOUNDS").strip()
+        os.environ.setdefault("DG_LIB_OUT", os.path.join(LIBDIR, "libdg_bounds.so"))
+        LIB = os.environ["DG_LIB_OUT"]
+    print(build(force="--force" in sys.argv or "--bounds" in sys.argv, verbose="-v" in sys.argv))

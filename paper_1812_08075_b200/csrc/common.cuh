@@ -3,6 +3,24 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
+
+// Debug builds (-DDG_BOUNDS, `python -m paper_1812_08075_b200.build --bounds`): every global access and every
+// bulk-copy destination of the marching-tile kernels is checked against the array / shared-memory extents
+// derived from the launch arguments; a violation prints the site and traps (compute-sanitizer is not available
+// on this GPU pool). Release builds compile the checks away.
+#ifdef DG_BOUNDS
+#define DG_CHECK(cond)                                                                                             \
+    do {                                                                                                           \
+        if (!(cond)) {                                                                                             \
+            printf("DG_BOUNDS violation %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, blockIdx.x, \
+                   threadIdx.x);                                                                                   \
+            __trap();                                                                                              \
+        }                                                                                                          \
+    } while (0)
+#else
+#define DG_CHECK(cond) do { } while (0)
+#endif
 
 namespace dg {
 

@@ -5,7 +5,6 @@
 #include "kernel_cell.cuh"
 #include "kernel_gen.cuh"
 #include "kernel_quad.cuh"
-#include "kernel_quadw.cuh"
 #include "kernel_stokes.cuh"
 #include "tables.h"
 
@@ -261,56 +260,31 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
 }
 
 // ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
-// (WARP = true and n = 5: the warp-per-cell k_quadw, selected by DG_QUAD_WARP)
-template <int N, bool AFF, bool COEF, int PR = 0, bool WARP = true>
+template <int N, bool AFF, bool COEF, int PR = 0>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                         double* r, long long c0, long long c1, cudaStream_t st, const double* u0)
 {
     if (c1 <= c0) return cudaSuccess;
-    if constexpr (N == 5 && WARP && PR <= 1) {
-        using W = dg::qw::WLay<N, N + 1>;
-        const long long grid = (c1 - c0 + W::WPB - 1) / W::WPB;
-        dg::k_quadw<N, N + 1, AFF, COEF, PR == 1><<<(unsigned)grid, W::WPB * 32, W::BYTES, st>>>(
-            x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M);
-        return cudaGetLastError();
-    } else {
-        using L = dg::qd::QLay<N, N + 1, PR == 3>;
-        const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
-        dg::k_quad<N, N + 1, AFF, COEF, PR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
-            x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M, u0);
-        return cudaGetLastError();
-    }
+    using L = dg::qd::QLay<N, N + 1, PR == 3>;
+    const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
+    dg::k_quad<N, N + 1, AFF, COEF, PR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
+        x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M, u0);
+    return cudaGetLastError();
 }
 template <int N, bool AFF, bool COEF, int PR = 0>
 cudaError_t attr_quad()
 {
-    if constexpr (N == 5 && PR <= 1) {
-        cudaError_t e = cudaFuncSetAttribute(dg::k_quadw<N, N + 1, AFF, COEF, PR == 1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, dg::qw::WLay<N, N + 1>::BYTES);
-        if (e != cudaSuccess) return e;
-    }
     return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 dg::qd::QLay<N, N + 1, PR == 3>::BYTES);
 }
 // pr: the problem mode of k_quad (0 periodic, 1 diffusion-reaction, 2 its nonlinear variant, 3 the Jacobian
-// action of the nonlinear variant; 2 and 3 always use the CTA kernel)
+// action of the nonlinear variant)
 template <int N>
-LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0, bool cta = false)
+LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0)
 {
-    if (pr == 1) {
-        *err = attr_quad<N, false, false, 1>();
-        return cta ? launch_quad<N, false, false, 1, false> : launch_quad<N, false, false, 1>;
-    }
-    if (pr == 2) { *err = attr_quad<N, false, false, 2>(); return launch_quad<N, false, false, 2, false>; }
-    if (pr == 3) { *err = attr_quad<N, false, false, 3>(); return launch_quad<N, false, false, 3, false>; }
-    if (cta) {
-        if (aff) {
-            *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
-            return coef ? launch_quad<N, true, true, 0, false> : launch_quad<N, true, false, 0, false>;
-        }
-        *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
-        return coef ? launch_quad<N, false, true, 0, false> : launch_quad<N, false, false, 0, false>;
-    }
+    if (pr == 1) { *err = attr_quad<N, false, false, 1>(); return launch_quad<N, false, false, 1>; }
+    if (pr == 2) { *err = attr_quad<N, false, false, 2>(); return launch_quad<N, false, false, 2>; }
+    if (pr == 3) { *err = attr_quad<N, false, false, 3>(); return launch_quad<N, false, false, 3>; }
     if (aff) {
         *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
         return coef ? launch_quad<N, true, true> : launch_quad<N, true, false>;
@@ -318,16 +292,16 @@ LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0, bool cta
     *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
     return coef ? launch_quad<N, false, true> : launch_quad<N, false, false>;
 }
-LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, int pr = 0, bool cta = false)
+LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, int pr = 0)
 {
     switch (n) {
-    case 2: return pick_quad_n<2>(aff, coef, err, pr, cta);
-    case 3: return pick_quad_n<3>(aff, coef, err, pr, cta);
-    case 4: return pick_quad_n<4>(aff, coef, err, pr, cta);
-    case 5: return pick_quad_n<5>(aff, coef, err, pr, cta);
-    case 6: return pick_quad_n<6>(aff, coef, err, pr, cta);
-    case 7: return pick_quad_n<7>(aff, coef, err, pr, cta);
-    default: return pick_quad_n<8>(aff, coef, err, pr, cta);
+    case 2: return pick_quad_n<2>(aff, coef, err, pr);
+    case 3: return pick_quad_n<3>(aff, coef, err, pr);
+    case 4: return pick_quad_n<4>(aff, coef, err, pr);
+    case 5: return pick_quad_n<5>(aff, coef, err, pr);
+    case 6: return pick_quad_n<6>(aff, coef, err, pr);
+    case 7: return pick_quad_n<7>(aff, coef, err, pr);
+    default: return pick_quad_n<8>(aff, coef, err, pr);
     }
 }
 // ---- the paper's Stokes problem: k_stokes, one cell per CTA
@@ -724,19 +698,13 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
         case 8: fill_qtab<8>(H, Hm, c->qtab); break;
         }
         cudaError_t e = cudaSuccess;
-        // k_quad (per-cell thread groups) is the default; DG_QUAD_WARP selects the warp-per-cell k_quadw for
-        // n = 5 (tests compare the two; measured slower since k_quad's cells progress independently)
-        const bool cta = getenv("DG_QUAD_WARP") == nullptr;
         const int pr = mesh->problem == DG_PROBLEM_DIFFREAC ? 1 : (mesh->problem == DG_PROBLEM_NLREAC ? 2 : 0);
-        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr, cta);
-        if (e == cudaSuccess && pr == 2) c->launch_jac = pick_quad(n, false, false, &e, 3, true);
-        if (e != cudaSuccess) {
-            return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
-        }
-        const bool warp = n == 5 && !cta;
-        c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? (warp ? "k_quadw_diffreac" : "k_quad_diffreac")
+        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr);
+        if (e == cudaSuccess && pr == 2) c->launch_jac = pick_quad(n, false, false, &e, 3);
+        if (e != cudaSuccess) return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
+        c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? "k_quad_diffreac"
                    : mesh->problem == DG_PROBLEM_NLREAC ? "k_quad_nlreac"
-                                                        : (warp ? "k_quadw" : "k_quad");
+                                                        : "k_quad";
     }
     if (mesh->problem == DG_PROBLEM_STOKES) {
         dg::HostTables Hp;
@@ -1006,7 +974,8 @@ double dg_alg_bytes(const dg_ctx* c)
 {
     if (!c) return -1.0;
     double b = 16.0 * (double)c->local_dofs;
-    if (c->mesh.geom_kind == DG_GEOM_AFFINE) b += 72.0 * (double)c->M.plane_cells * c->M.L;
+    // 120 B per affine cell (J and the symmetric G~ = |det J| J^-1 J^-T)
+    if (c->mesh.geom_kind == DG_GEOM_AFFINE) b += 120.0 * (double)c->M.plane_cells * c->M.L;
     return b;
 }
 

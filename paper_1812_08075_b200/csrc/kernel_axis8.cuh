@@ -180,6 +180,8 @@ __device__ __forceinline__ void inplane_pass(const AxisTab8& A, const MeshArgs& 
         rhi = cidx(ti1 * T1 + tw, (ti2 * T2 + T2) % M.N2);
     }
     constexpr int NR = (G == 1) ? 2 : 1;
+    DG_CHECK(lp >= 0 && lp < M.L && rlo >= 0 && rlo < (long long)M.L * M.plane_cells && rhi >= 0 &&
+             rhi < (long long)M.L * M.plane_cells);
     double rv[NR][8];
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -350,6 +352,7 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
         // TMA the T1 x T2 blocks of plane p_begin + step into buffer (step & 1): one box per tile row
         const int lp = p_begin + step;
         const uint32_t b = bar(step & 1);
+        DG_CHECK(lp >= 0 && lp < M.L && (ti1 + 1) * T1 <= M.N1 && (ti2 + 1) * T2 <= M.N2);
         mbar_expect_tx(b, C::BUF_BYTES);
 #pragma unroll
         for (int c1 = 0; c1 < T1; ++c1) {
@@ -498,6 +501,7 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
                     o[i] = fma(S0[q], ye[i] + yo[i], o[i]);
                     o[7 - i] = fma(S0[q], ye[i] - yo[i], o[7 - i]);
                 }
+                DG_CHECK(lp >= 0 && lp < M.L && d0_inplane < PC && L < 64);
                 double2* dst = reinterpret_cast<double2*>(r + (cell_index(lp, 0, 0) + d0_inplane) * 512 + 8 * L);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) dst[k] = make_double2(o[2 * k], o[2 * k + 1]);

@@ -392,6 +392,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto fslot = [&](int f) { return f < 3 * NC ? (f % 3) * NC + f / 3 : f; };
     auto TRp = [&](int f, int side) {
         const int o = fslot(f);
+        DG_CHECK(f >= 0 && f < NF && o >= 0 && o < NF && (side == 0 || side == 1));
         return gn::TRView{TRB + o * FSD + side * N2, TRB + o * FSD + (2 + side) * N2};
     };
 
@@ -410,8 +411,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto gixs = [&](int S, int d, int j) -> int {
         return d == 0 ? mb * S + mc * N2 + j + N * ma : (d == 1 ? mb * S + mc * N2 + ma + N * j : j * S + mc * N2 + mab);
     };
-    auto gix0 = [&](int d, int j) { return gixs(Y::S0, d, j); }; // G0 index
-    auto gix1 = [&](int d, int j) { return gixs(Y::S1, d, j); }; // G1 index
+    auto gix0 = [&](int d, int j) { const int i = gixs(Y::S0, d, j); DG_CHECK(i >= 0 && i < N * Y::S0); return i; }; // G0 index
+    auto gix1 = [&](int d, int j) { const int i = gixs(Y::S1, d, j); DG_CHECK(i >= 0 && i < N * Y::S1); return i; }; // G1 index
 
     if (tid < N) { sXi[tid] = E.xi[tid]; sW[tid] = E.w[tid]; }
     for (int i = tid; i < N * N; i += NT) sD[i] = E.D[i];
@@ -429,6 +430,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto xbytes = [&](int lp) -> uint32_t { return is_tr(lp) ? T1 * ROWT : T1 * ROWB; };
     auto issue_x = [&](int lp, double* dst) { // own blocks (or halo traces) of plane lp (T1 rows) on barA (caller: expect_tx)
         const double* src = xplane(lp);
+        DG_CHECK(lp >= -1 && lp <= M.L && dst >= XS && dst + NC * N3 <= XS + 2 * NC * N3);
+        DG_CHECK((ti1 + 1) * T1 <= M.N1 && (ti2 + 1) * T2 <= M.N2);
         if (is_tr(lp)) {
 #pragma unroll
             for (int c1 = 0; c1 < T1; ++c1)
@@ -441,6 +444,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     };
     // records (AFFINE) and c(x) factor tables (COEFF) of own + ring-below cells of plane lp into buffer `buf`
     auto issue_geo = [&](int lp, int buf) {
+        DG_CHECK(lp >= -1 && lp <= M.L - 1 && (buf == 0 || buf == 1));
         auto rows = [&](const double* base, int per, double* dst, bool ring) {
             auto at = [&](int i1, int i2) { return base + cidx(lp + 1, i1, i2) * per; };
 #pragma unroll
@@ -463,6 +467,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     auto ring_b2 = [&](int c1) { return RX + (Y::RB2 + SL * c1 + (SL - 1)) * N3; }; // ring cell below (i2) of tile row c1
     auto ring_a2 = [&](int c1) { return RX + (Y::RA2 + SL * c1) * N3; };            // ring cell above (i2) of tile row c1
     auto issue_ring_bulk = [&](int lp) {
+        DG_CHECK(lp >= 0 && lp < M.L);
         const double* src = x + (long long)lp * PC * N3;
         const uint32_t bytes = 2 * ROWB + 2 * T1 * SL * N3 * 8;
         gn::mbar_expect_tx(barB, bytes);
@@ -938,6 +943,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             // ---- L3: sum of the three directions, write r once ----
             if (act) {
                 double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
+            DG_CHECK(lp >= 0 && lp < M.L && cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2) < (long long)M.L * PC);
+                DG_CHECK(lp >= 0 && lp < M.L && cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2) < (long long)M.L * PC);
 #pragma unroll
                 for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y2[j] + G0[gix0(2, j)] + G1[gix1(2, j)];
             }
@@ -1103,6 +1110,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             const double2 lo = TRp(flo2, 1)[mab], hi = TRp(3 * mc + 2, 0)[mab];
             gn::sweep<N, true, true>(E, xe, xo, y, lo.x, lo.y, hi.x, hi.y);
             double* dst = r + (cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2)) * N3;
+            DG_CHECK(lp >= 0 && lp < M.L && cidx(lp, ti1 * T1 + mc1, ti2 * T2 + mc2) < (long long)M.L * PC);
 #pragma unroll
             for (int j = 0; j < N; ++j) dst[pidx<N>(2, j, ma, mb)] = y[j] + G0[gix0(2, j)] + G1[gix1(2, j)];
         }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--coeff", type=int, default=1)
     ap.add_argument("--R", type=int, default=20)
     ap.add_argument("--parity", action="store_true", help="also check a small mesh against the oracle")
+    ap.add_argument("--graph", action="store_true", help="replay the R applies from one CUDA graph")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -36,10 +37,25 @@ def main():
         op.apply(x, r)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.R):
-        op.apply(x, r)
-    e1.record()
+    if a.graph:
+        gs = torch.cuda.Stream()
+        with torch.cuda.stream(gs):
+            op.set_stream(gs)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(a.R):
+                    op.apply(x, r)
+        op.set_stream(torch.cuda.current_stream())
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        e0.record()
+        for _ in range(a.R):
+            op.apply(x, r)
+        e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.R
     F = op.alg_flops
