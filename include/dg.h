@@ -94,7 +94,8 @@ typedef struct dg_mesh {
  * DG_COEFF_SINCOS: c(x) factor tables (96 (n+1) B/cell) and c at the upper-face points
  * (8 (3n^2 rounded up to even) B/cell); DG_GEOM_AXIS + DG_COEFF_ONE: nothing. *out owned by
  * the caller, release with dg_destroy. Synchronous. Kernel selection is deterministic: k_axis8 for
- * axis-aligned Q7 with c = 1 and N1 % 2 == N2 % 4 == 0; k_gen when its (i1, i2) tile divides the mesh;
+ * axis-aligned Q7 with c = 1 and N1 % 2 == N2 % 4 == 0; k_line for other axis-aligned c = 1 slabs whose x
+ * is at most 32 MB (L2-resident); k_gen when its (i1, i2) tile divides the mesh;
  * k_cell_general otherwise; k_quad / k_stokes for the other problems. A failing kernel attribute
  * call or allocation returns DG_ERR_CUDA / DG_ERR_OOM (no silent switch to another kernel) and
  * releases everything allocated so far. */
@@ -133,7 +134,7 @@ int dg_apply_planes(dg_ctx* ctx, const double* x, const double* x_below, const d
  *   aligned. Asynchronous on the context stream.
  * dg_apply_planes_tr: dg_apply_planes with the two halo planes replaced by trace halos as produced by the
  *   neighbours' dg_pack_halo (16-byte aligned). Interior plane ranges never read them.
- * Both return DG_ERR_UNSUPPORTED unless dg_kernel_name() is "k_gen" or "k_axis8". */
+ * Both return DG_ERR_UNSUPPORTED unless dg_kernel_name() is "k_gen", "k_axis8" or "k_line". */
 int64_t dg_halo_ndofs(const dg_ctx* ctx);
 int dg_pack_halo(dg_ctx* ctx, const double* x, double* tr_lo, double* tr_hi);
 int dg_apply_planes_tr(dg_ctx* ctx, const double* x, const double* tr_below, const double* tr_above, double* r,

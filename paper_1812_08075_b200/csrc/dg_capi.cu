@@ -4,6 +4,7 @@
 #include "kernel_axis8.cuh"
 #include "kernel_cell.cuh"
 #include "kernel_gen.cuh"
+#include "kernel_line.cuh"
 #include "kernel_quad.cuh"
 #include "kernel_stokes.cuh"
 #include "tables.h"
@@ -481,6 +482,7 @@ struct dg_ctx {
     // axis-aligned n = 8 fast path (k_axis8)
     bool ax8;
     bool gen;
+    bool line; // k_line: axis-aligned c = 1, L2-resident vectors
     GenInfo ginfo;
     int m;     // Gauss points per direction
     bool quad; // m = n + 1: k_quad
@@ -548,6 +550,21 @@ static cudaError_t launch_planes(dg_ctx* c, const double* x, const double* xb, c
     if (c->quad) {
         const long long pcq = c->M.plane_cells;
         return c->launch(c->qtab, c->M, x, xb, xa, r, (long long)p0 * pcq, (long long)p1 * pcq, st, nullptr);
+    }
+    if (c->line) {
+        const long long ncell = (long long)(p1 - p0) * c->M.plane_cells;
+        switch (c->n) {
+#define LINE_CASE(NN)                                                                                                  \
+    case NN: {                                                                                                         \
+        const unsigned grid = (unsigned)((ncell + dg::LineCfg<NN>::CPB - 1) / dg::LineCfg<NN>::CPB);                   \
+        dg::k_line<NN><<<grid, dg::LineCfg<NN>::NT, 0, st>>>(x, xb, xa, r, p0, p1, halo_tr,                            \
+                                                            *reinterpret_cast<const dg::EOTab<NN>*>(c->eotab), c->M); \
+        break;                                                                                                         \
+    }
+            LINE_CASE(2) LINE_CASE(3) LINE_CASE(4) LINE_CASE(5) LINE_CASE(6) LINE_CASE(7) LINE_CASE(8)
+#undef LINE_CASE
+        }
+        return cudaGetLastError();
     }
     if (c->gen)
         return c->ginfo.fn(c->eotab, c->M, x, xb, xa, r, p0, p1, c->gen_chunk, halo_tr, st, c->d_geo, c->d_ctab, c->d_cface);
@@ -752,7 +769,12 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             ch = ch < 2 ? 2 : (ch > 32 ? 32 : ch);
             c->gen_chunk = gc ? atoi(gc) : ch;
         }
-        if (c->gen) {
+        // k_line for axis-aligned c = 1 meshes whose vectors are L2-resident (<= 32 MB; cfg0, cfg1): no plane pipeline
+        c->line = mesh->geom_kind == DG_GEOM_AXIS && mesh->coeff_kind == DG_COEFF_ONE && mesh->problem == DG_PROBLEM_PERIODIC &&
+                  8.0 * (double)c->local_dofs <= 32.0 * 1024 * 1024 && getenv("DG_FORCE_GENERAL") == nullptr &&
+                  getenv("DG_NO_LINE") == nullptr;
+        if (c->line) c->gen = false;
+        if (c->gen || c->line) {
             switch (n) {
             case 2: fill_eotab<2>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
             case 3: fill_eotab<3>(H, mesh->penalty_scale * k * (k + 1), M.h, c->eotab); break;
@@ -809,6 +831,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             if (e != cudaSuccess) return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_ctab / k_cface: %s", cudaGetErrorString(e));
         }
         if (c->gen) c->kname = "k_gen";
+        if (c->line) c->kname = "k_line";
 #ifdef DG_GEN_TRACE
         if (c->gen && getenv("DG_TRACE") && !c->dbg) {
             if (cudaMalloc(&c->dbg, sizeof(long long) * 1024 * 16 * 8) == cudaSuccess) {
@@ -849,6 +872,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             AX8_VARIANTS(AX8_ATTR)
 #undef AX8_ATTR
         }
+        c->line = false; // the Q7 marching kernel on every size
         if (e != cudaSuccess)
             return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_axis8 shared-memory attribute: %s", cudaGetErrorString(e));
         if (!get_encode()) return setup_fail(c, DG_ERR_CUDA, "dg_setup: cuTensorMapEncodeTiled unavailable (driver)");
@@ -993,16 +1017,17 @@ int dg_apply_planes_tr(dg_ctx* c, const double* x, const double* tr_below, const
                        int p1)
 {
     if (!c) return fail(DG_ERR_INVALID, "dg_apply_planes_tr: NULL ctx");
-    if (!(c->gen || c->ax8))
-        return fail(DG_ERR_UNSUPPORTED, "dg_apply_planes_tr: trace halos need k_gen or k_axis8 (context kernel %s)", c->kname);
+    if (!(c->gen || c->ax8 || c->line))
+        return fail(DG_ERR_UNSUPPORTED, "dg_apply_planes_tr: trace halos need k_gen, k_axis8 or k_line (context kernel %s)",
+                    c->kname);
     return apply_planes_impl(c, x, tr_below, tr_above, r, p0, p1, nullptr, 3);
 }
 
 int dg_pack_halo(dg_ctx* c, const double* x, double* tr_lo, double* tr_hi)
 {
     if (!c || !x || !tr_lo || !tr_hi) return fail(DG_ERR_INVALID, "dg_pack_halo: NULL argument");
-    if (!(c->gen || c->ax8))
-        return fail(DG_ERR_UNSUPPORTED, "dg_pack_halo: trace halos need k_gen or k_axis8 (context kernel %s)", c->kname);
+    if (!(c->gen || c->ax8 || c->line))
+        return fail(DG_ERR_UNSUPPORTED, "dg_pack_halo: trace halos need k_gen, k_axis8 or k_line (context kernel %s)", c->kname);
     if (((uintptr_t)x | (uintptr_t)tr_lo | (uintptr_t)tr_hi) & 15)
         return fail(DG_ERR_INVALID, "dg_pack_halo: pointers must be 16-byte aligned");
     const long long tot = 2LL * c->M.plane_cells * c->n * c->n;

@@ -222,8 +222,8 @@ class SlabOperator:
         self.ndofs = self.op.ndofs
         self.offset = self.op.offset
         self.plane_ndofs = self.op.plane_ndofs
-        # traces-only halos where the kernel supports them (k_gen, k_axis8), full boundary planes otherwise
-        use_tr = traces and self.op.kernel_name in ("k_gen", "k_axis8")
+        # traces-only halos where the kernel supports them (k_gen, k_axis8, k_line), full boundary planes otherwise
+        use_tr = traces and self.op.kernel_name in ("k_gen", "k_axis8", "k_line")
         self._apply = SlabApply(self.plan, self.plane_ndofs, self.op.apply_planes, group=group,
                                 device=f"cuda:{device}", pack_fn=self.op.pack_halo if use_tr else None,
                                 planes_tr_fn=self.op.apply_planes_tr if use_tr else None,

@@ -34,7 +34,8 @@ CASES = [
     (2, (6, 4, 8), 1, 1, "k_gen"),
     (4, (6, 4, 8), 1, 1, "k_gen"),
     (5, (7, 2, 4), 1, 1, "k_gen"),
-    (3, (6, 4, 8), 0, 0, "k_gen"),
+    (3, (6, 4, 8), 0, 0, "k_line"),
+    (1, (5, 3, 4), 0, 0, "k_line"),
     (3, (6, 4, 8), 0, 1, "k_gen"),
     (7, (6, 2, 4), 0, 0, "k_axis8"),
 ]

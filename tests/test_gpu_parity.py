@@ -143,7 +143,7 @@ def test_slab_loopback_bitwise(world, wi):
     full.close()
 
 
-@pytest.mark.parametrize("w,kern", [(synth.CONFIGS[1], "k_gen"), (synth.small(7, (16, 8, 8), seed=33), "k_axis8"),
+@pytest.mark.parametrize("w,kern", [(synth.CONFIGS[1], "k_line"), (synth.small(7, (16, 8, 8), seed=33), "k_axis8"),
                                     (synth.small(4, (12, 8, 8), geom_kind=1, coeff_kind=1, seed=34), "k_gen")])
 def test_host_pipeline_bitwise(w, kern):
     """dg_apply_host (H2D / compute / D2H pipelined over plane chunks; k_axis8: the TMA tensor map re-encoded
@@ -238,6 +238,49 @@ def test_axis8_slab_loopback_bitwise(world):
     full.close()
 
 
+@pytest.mark.parametrize("k", range(1, 8))
+@pytest.mark.parametrize("N", [(3, 5, 7), (2, 2, 2), (5, 2, 3)])
+def test_line_all_degrees(k, N):
+    """k_line (axis-aligned c = 1, L2-resident meshes: the kernel of cfg0 / cfg1; for k = 7 k_axis8 takes the
+    meshes its tiles divide) on ragged meshes incl. the minimum N = 2, against the oracle, and against k_gen's
+    line-operator form where k_gen's tiles divide the mesh."""
+    w = synth.small(k, N, seed=250 + k)
+    op = _op(w)
+    if k < 7:
+        assert op.kernel_name == "k_line"
+    op.close()
+    assert _full_check(w) <= TOL
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_line_slab_loopback_bitwise(world):
+    """k_line in the slab decomposition (block halos; the interior / boundary plane split) == whole mesh."""
+    from paper_1812_08075_b200 import Operator, slab
+    w = synth.small(3, (7, 5, 6), seed=43)
+    full = _op(w)
+    assert full.kernel_name == "k_line"
+    x = synth.x_torch(w, device="cuda")
+    ref = full.apply(x)
+    pd = full.plane_ndofs
+    got = torch.full_like(x, float("nan"))
+    for q in range(world):
+        p = slab.plan(w.N[0], q, world)
+        op = Operator(w.N, w.k, plane_begin=p.plane_begin, nplanes=p.nplanes)
+        xs = x[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        rs = got[p.plane_begin * pd:(p.plane_begin + p.nplanes) * pd]
+        hb = x[((p.plane_begin - 1) % w.N[0]) * pd:][:pd].clone()
+        ha = x[((p.plane_begin + p.nplanes) % w.N[0]) * pd:][:pd].clone()
+        a, b = p.interior
+        if b > a:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        for a, b in p.boundary:
+            op.apply_planes(xs, hb, ha, rs, a, b)
+        torch.cuda.synchronize()
+        op.close()
+    assert torch.equal(got, ref)
+    full.close()
+
+
 # k_gen tile shapes (dg_capi.cu GenShape): n -> (T1, T2)
 GEN_TILE = {2: (4, 4), 3: (2, 4), 4: (2, 4), 5: (2, 4), 6: (2, 2), 7: (2, 2), 8: (2, 2)}
 
@@ -251,6 +294,7 @@ def test_gen_all_degrees(k, geom, coeff, monkeypatch):
     T1, T2 = GEN_TILE[k + 1]
     N = (3, T1, 3 * T2) if k % 2 else (4, 2 * T1, T2)
     monkeypatch.setenv("DG_AX8_GEN", "1")  # axis-aligned Q7 through k_gen instead of k_axis8
+    monkeypatch.setenv("DG_NO_LINE", "1")  # axis-aligned c = 1 through k_gen instead of k_line
     w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=200 + k)
     op = _op(w)
     assert op.kernel_name == "k_gen"
@@ -265,6 +309,7 @@ def test_gen_chunks(k, geom, coeff, monkeypatch):
     T1, T2 = GEN_TILE[k + 1]
     w = synth.small(k, (7, 2 * T1, 2 * T2), geom_kind=geom, coeff_kind=coeff, seed=300 + k)
     x = synth.x_torch(w, device="cuda")
+    monkeypatch.setenv("DG_NO_LINE", "1")
     monkeypatch.setenv("DG_GEN_CHUNK", "3")
     a = _op(w)
     monkeypatch.setenv("DG_GEN_CHUNK", "0")
