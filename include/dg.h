@@ -40,7 +40,7 @@ extern "C" {
 
 #define DG_OK 0
 #define DG_ERR_INVALID (-1)     /* bad argument (sizes, pointers, aliasing, unsupported k) */
-#define DG_ERR_UNSUPPORTED (-2) /* valid request this build does not implement (quad != k+1) */
+#define DG_ERR_UNSUPPORTED (-2) /* valid request this build does not implement (e.g. quad outside k+1..k+3) */
 #define DG_ERR_CUDA (-3)        /* CUDA runtime failure (no device, launch error, ...) */
 #define DG_ERR_OOM (-5)         /* device or pinned-host allocation failed */
 
@@ -87,8 +87,9 @@ typedef struct dg_mesh {
 
 /* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,
  * boundary vectors e0,e1,d0,d1), device copy of the slab's
- * geometry, kernel selection. k in [1,7]; quad = Gauss points per direction, must equal k+1
- * (collocation; other values -> DG_ERR_UNSUPPORTED). Allocates device memory for the L+2 planes
+ * geometry, kernel selection. k in [1,7]; quad = Gauss points per direction: k+1 (collocation), k+2
+ * (overintegration, A != I: k_quad), k+3 (periodic problem, k <= 6: k_quad); other values ->
+ * DG_ERR_UNSUPPORTED (P:L604-616 raised quadrature counts). Allocates device memory for the L+2 planes
  * plane_begin-1 .. plane_begin+L: DG_GEOM_AFFINE: J (72 B/cell) and per-cell geometry records
  * (288 B/cell: |det J| J^-1 J^-T, rows of J, upper-face normals / surface elements);
  * DG_COEFF_SINCOS: c(x) factor tables (96 (n+1) B/cell) and c at the upper-face points

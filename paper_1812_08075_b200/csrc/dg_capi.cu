@@ -260,32 +260,43 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
     E->Sc[2] = h[0] * h[1] / h[2];
 }
 
-// ---- general quadrature (M = n + 1 Gauss points per direction): k_quad
-template <int N, bool AFF, bool COEF, int PR = 0>
+// ---- general quadrature (M = n + MQ Gauss points per direction, MQ = 1 or 2): k_quad
+template <int N, bool AFF, bool COEF, int PR = 0, int MQ = 1>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                         double* r, long long c0, long long c1, cudaStream_t st, const double* u0)
 {
     if (c1 <= c0) return cudaSuccess;
-    using L = dg::qd::QLay<N, N + 1, PR == 3>;
+    using L = dg::qd::QLay<N, N + MQ, PR == 3>;
     const long long grid = (c1 - c0 + L::CPB - 1) / L::CPB;
-    dg::k_quad<N, N + 1, AFF, COEF, PR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
-        x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + 1>*>(qt), M, u0);
+    dg::k_quad<N, N + MQ, AFF, COEF, PR><<<(unsigned)grid, L::NT, L::BYTES, st>>>(
+        x, xb, xa, r, c0, c1, *static_cast<const dg::QTab<N, N + MQ>*>(qt), M, u0);
     return cudaGetLastError();
 }
-template <int N, bool AFF, bool COEF, int PR = 0>
+template <int N, bool AFF, bool COEF, int PR = 0, int MQ = 1>
 cudaError_t attr_quad()
 {
-    return cudaFuncSetAttribute(dg::k_quad<N, N + 1, AFF, COEF, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                dg::qd::QLay<N, N + 1, PR == 3>::BYTES);
+    if (dg::qd::QLay<N, N + MQ, PR == 3>::BYTES > 227 * 1024) return cudaErrorInvalidValue; // does not fit an SM
+    return cudaFuncSetAttribute(dg::k_quad<N, N + MQ, AFF, COEF, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dg::qd::QLay<N, N + MQ, PR == 3>::BYTES);
 }
 // pr: the problem mode of k_quad (0 periodic, 1 diffusion-reaction, 2 its nonlinear variant, 3 the Jacobian
-// action of the nonlinear variant)
+// action of the nonlinear variant); mq = m - n (2: the periodic problem only)
 template <int N>
-LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0)
+LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0, int mq = 1)
 {
     if (pr == 1) { *err = attr_quad<N, false, false, 1>(); return launch_quad<N, false, false, 1>; }
     if (pr == 2) { *err = attr_quad<N, false, false, 2>(); return launch_quad<N, false, false, 2>; }
     if (pr == 3) { *err = attr_quad<N, false, false, 3>(); return launch_quad<N, false, false, 3>; }
+    if constexpr (N <= 7) {
+        if (mq == 2) {
+            if (aff) {
+                *err = coef ? attr_quad<N, true, true, 0, 2>() : attr_quad<N, true, false, 0, 2>();
+                return coef ? launch_quad<N, true, true, 0, 2> : launch_quad<N, true, false, 0, 2>;
+            }
+            *err = coef ? attr_quad<N, false, true, 0, 2>() : attr_quad<N, false, false, 0, 2>();
+            return coef ? launch_quad<N, false, true, 0, 2> : launch_quad<N, false, false, 0, 2>;
+        }
+    }
     if (aff) {
         *err = coef ? attr_quad<N, true, true>() : attr_quad<N, true, false>();
         return coef ? launch_quad<N, true, true> : launch_quad<N, true, false>;
@@ -293,16 +304,16 @@ LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0)
     *err = coef ? attr_quad<N, false, true>() : attr_quad<N, false, false>();
     return coef ? launch_quad<N, false, true> : launch_quad<N, false, false>;
 }
-LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, int pr = 0)
+LaunchFn pick_quad(int n, bool aff, bool coef, cudaError_t* err, int pr = 0, int mq = 1)
 {
     switch (n) {
-    case 2: return pick_quad_n<2>(aff, coef, err, pr);
-    case 3: return pick_quad_n<3>(aff, coef, err, pr);
-    case 4: return pick_quad_n<4>(aff, coef, err, pr);
-    case 5: return pick_quad_n<5>(aff, coef, err, pr);
-    case 6: return pick_quad_n<6>(aff, coef, err, pr);
-    case 7: return pick_quad_n<7>(aff, coef, err, pr);
-    default: return pick_quad_n<8>(aff, coef, err, pr);
+    case 2: return pick_quad_n<2>(aff, coef, err, pr, mq);
+    case 3: return pick_quad_n<3>(aff, coef, err, pr, mq);
+    case 4: return pick_quad_n<4>(aff, coef, err, pr, mq);
+    case 5: return pick_quad_n<5>(aff, coef, err, pr, mq);
+    case 6: return pick_quad_n<6>(aff, coef, err, pr, mq);
+    case 7: return pick_quad_n<7>(aff, coef, err, pr, mq);
+    default: return pick_quad_n<8>(aff, coef, err, pr, mq);
     }
 }
 // ---- the paper's Stokes problem: k_stokes, one cell per CTA
@@ -363,12 +374,12 @@ void fill_stab(const dg::HostTables& H, const dg::HostTables& Hp, void* out)
     }
 }
 
-// interpolation / derivative of the n-node Lagrange basis at the m = n+1 Gauss points (long double
+// interpolation / derivative of the n-node Lagrange basis at the m = n + MQ Gauss points (long double
 // product formulas, no division by (s - x_a): robust when a quadrature point is close to a node)
-template <int N>
+template <int N, int MQ = 1>
 void fill_qtab(const dg::HostTables& Hn, const dg::HostTables& Hm, void* out)
 {
-    constexpr int M = N + 1;
+    constexpr int M = N + MQ;
     dg::QTab<N, M>* Q = static_cast<dg::QTab<N, M>*>(out);
     for (int q = 0; q < M; ++q) {
         const long double s = Hm.xi[q];
@@ -617,8 +628,10 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (!mesh || !out) return fail(DG_ERR_INVALID, "dg_setup: NULL argument");
     *out = nullptr;
     if (k < 1 || k > 7) return fail(DG_ERR_INVALID, "dg_setup: k=%d outside [1,7]", k);
-    if (quad != k + 1 && quad != k + 2)
-        return fail(DG_ERR_UNSUPPORTED, "dg_setup: quad=%d (supported: k+1 collocation, k+2 overintegration)", quad);
+    if (quad != k + 1 && quad != k + 2 && !(quad == k + 3 && k <= 6 && mesh->problem == DG_PROBLEM_PERIODIC))
+        return fail(DG_ERR_UNSUPPORTED,
+                    "dg_setup: quad=%d (supported: k+1 collocation, k+2 overintegration, k+3 for the periodic problem "
+                    "with k <= 6)", quad);
     for (int d = 0; d < 3; ++d)
         if (mesh->N[d] < 2) return fail(DG_ERR_INVALID, "dg_setup: N[%d]=%d < 2", d, mesh->N[d]);
     if (mesh->plane_begin < 0 || mesh->plane_begin >= mesh->N[0] || mesh->nplanes < 1 || mesh->nplanes > mesh->N[0])
@@ -698,26 +711,29 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
     c->kname = "k_cell_general";
     c->m = quad;
-    c->quad = quad == k + 2;
+    c->quad = quad >= k + 2;
     if (c->quad) {
-        // overintegration: m = n + 1 Gauss points, interpolation A != I -> k_quad
+        // overintegration: m = n + 1 or n + 2 Gauss points, interpolation A != I -> k_quad
         dg::HostTables Hm;
         if (dg::build_tables(quad, &Hm)) {
             return setup_fail(c, DG_ERR_INVALID, "tables m=%d", quad);
         }
+        const int mq = quad - k - 1;
         switch (n) {
-        case 2: fill_qtab<2>(H, Hm, c->qtab); break;
-        case 3: fill_qtab<3>(H, Hm, c->qtab); break;
-        case 4: fill_qtab<4>(H, Hm, c->qtab); break;
-        case 5: fill_qtab<5>(H, Hm, c->qtab); break;
-        case 6: fill_qtab<6>(H, Hm, c->qtab); break;
-        case 7: fill_qtab<7>(H, Hm, c->qtab); break;
-        case 8: fill_qtab<8>(H, Hm, c->qtab); break;
+#define QTAB_CASE(NN)                                                                                                  \
+    case NN:                                                                                                           \
+        if (mq == 2) fill_qtab<NN, (NN <= 7 ? 2 : 1)>(H, Hm, c->qtab);                                                 \
+        else fill_qtab<NN>(H, Hm, c->qtab);                                                                            \
+        break;
+            QTAB_CASE(2) QTAB_CASE(3) QTAB_CASE(4) QTAB_CASE(5) QTAB_CASE(6) QTAB_CASE(7) QTAB_CASE(8)
+#undef QTAB_CASE
         }
         cudaError_t e = cudaSuccess;
         const int pr = mesh->problem == DG_PROBLEM_DIFFREAC ? 1 : (mesh->problem == DG_PROBLEM_NLREAC ? 2 : 0);
-        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr);
+        c->launch = pick_quad(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS, &e, pr, mq);
         if (e == cudaSuccess && pr == 2) c->launch_jac = pick_quad(n, false, false, &e, 3);
+        if (e == cudaErrorInvalidValue)
+            return setup_fail(c, DG_ERR_UNSUPPORTED, "dg_setup: k_quad with n=%d, m=%d does not fit in shared memory", n, quad);
         if (e != cudaSuccess) return setup_fail(c, DG_ERR_CUDA, "dg_setup: k_quad attributes: %s", cudaGetErrorString(e));
         c->kname = mesh->problem == DG_PROBLEM_DIFFREAC ? "k_quad_diffreac"
                    : mesh->problem == DG_PROBLEM_NLREAC ? "k_quad_nlreac"

@@ -401,9 +401,36 @@ def test_quad_equals_collocation_for_polynomial_integrands(k):
 
 def test_quad_rejects_unsupported_rules():
     from paper_1812_08075_b200 import DgError, dg
-    with pytest.raises(DgError) as ei:
-        dg.dg_setup((4, 4, 4), 2, 5)
-    assert ei.value.code == dg.DG_ERR_UNSUPPORTED
+    for k, q in ((2, 6), (2, 2), (7, 10)):  # k+4, fewer points than k+1, k+3 beyond k = 6
+        with pytest.raises(DgError) as ei:
+            dg.dg_setup((4, 4, 4), k, q)
+        assert ei.value.code == dg.DG_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("k", range(1, 7))
+@pytest.mark.parametrize("geom,coeff", [(0, 0), (1, 1)])
+def test_quad_k3_overintegration(k, geom, coeff):
+    """k+3 Gauss points per direction (SURVEY §8(f2), P:L604-616 raised quadrature counts): k_quad with
+    m = n + 2 against the oracle evaluated with the same rule."""
+    N = (3, 2, 5) if k >= 5 else (3, 3, 5)
+    w = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=520 + k, quad=k + 3)
+    op = _op(w)
+    assert op.kernel_name == "k_quad"
+    op.close()
+    assert _full_check(w) <= TOL
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_quad_k3_equals_collocation_for_polynomial_integrands(k):
+    """With c = 1 every rule with >= k+1 points integrates exactly: the k+3-point operator equals the collocated one."""
+    w1 = synth.small(k, (4, 4, 4), geom_kind=1, coeff_kind=0, seed=78)
+    w3 = synth.small(k, (4, 4, 4), geom_kind=1, coeff_kind=0, seed=78, quad=k + 3)
+    x = synth.x_torch(w1, device="cuda")
+    a, b = _op(w1), _op(w3)
+    ra, rb = a.apply(x), b.apply(x)
+    assert (ra - rb).abs().max().item() <= 1e-12 * ra.abs().max().item()
+    a.close()
+    b.close()
 
 
 @pytest.mark.parametrize("world", [2, 3])
