@@ -180,6 +180,18 @@ __device__ __forceinline__ void inplane_pass(const AxisTab8& A, const MeshArgs& 
         rhi = cidx(ti1 * T1 + tw, (ti2 * T2 + T2) % M.N2);
     }
     constexpr int NR = (G == 1) ? 2 : 1;
+#ifndef DG_AX8_NO_RING_PREFETCH
+    // the next plane's ring lines into L2 (evict_last) one plane ahead: about 40 % of the ring-line reads missed
+    // L2 (ncu: 1.14 GB of DRAM reads above the algorithmic 7.25 GB per cfg3 launch) and stalled the pass
+    if (lp + 1 < M.L) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const long long rc = (G == 1 ? (k ? rhi : rlo) : (half ? rhi : rlo)) + M.plane_cells;
+            // thread j0 of each 8-lane group touches row j = j0: together they cover the whole line
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(x + rc * 512 + eoff(j0)));
+        }
+    }
+#endif
     DG_CHECK(lp >= 0 && lp < M.L && rlo >= 0 && rlo < (long long)M.L * M.plane_cells && rhi >= 0 &&
              rhi < (long long)M.L * M.plane_cells);
     double rv[NR][8];
