@@ -219,6 +219,23 @@ def run_reference(args, w, rank):
     return 0
 
 
+class _DistSlab:
+    """bench.py's view of a DistOperator (the same attributes it uses of slab.SlabOperator)."""
+
+    def __init__(self, op):
+        self.op = op
+        self.ndofs, self.offset, self.plane_ndofs = op.ndofs, op.offset, op.plane_ndofs
+        self.launches_per_apply = op.launches_per_apply
+        self.traces = op.kernel_name in ("k_gen", "k_axis8", "k_line")
+        self.payload_doubles = op.halo_ndofs if self.traces else op.plane_ndofs
+
+    def apply(self, x, r=None):
+        return self.op.apply(x, r)
+
+    def close(self):
+        self.op.close()
+
+
 def _profile_record(workload, kernel):
     """ncu numbers of this kernel on this workload from the newest profiles/<round>/ncu_counters.json
     (written by tools/ncu_summary.py from an `ncu --set full` capture of the same command)."""
@@ -257,6 +274,9 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--comm", default="libdg", choices=["libdg", "torch"],
+                    help="N > 1: the halo exchange of libdg's collective C-ABI (dg_apply_dist, its own NCCL "
+                         "communicator; default) or of slab.py over torch.distributed")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -317,9 +337,19 @@ def main():
     def jac_fn(pb, npl):
         return synth.jac_planes_torch(w, pb, npl, device=dev).cpu().numpy()
 
-    sop = slab.SlabOperator(w.N, w.k, rank, world, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
-                            penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank, quad=w.m,
-                            problem=w.problem)
+    if world > 1 and args.comm == "libdg" and not args.jacobian:
+        # the collective C-ABI (dg_setup_dist / dg_apply_dist): libdg's own NCCL communicator and halo step
+        uid = [dg.dg_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        pb, npl = dg.dg_slab_range(w.N[0], rank, world)
+        jac = jac_fn(pb - 1, npl + 2) if w.geom_kind else None
+        sop = _DistSlab(dg.DistOperator(w.N, w.k, rank, world, uid[0], geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
+                                        penalty_scale=w.penalty_scale, jac=jac, device=local_rank, quad=w.m,
+                                        problem=w.problem))
+    else:
+        sop = slab.SlabOperator(w.N, w.k, rank, world, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
+                                penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank, quad=w.m,
+                                problem=w.problem)
     op = sop.op
     x = synth.x_torch(w, start=sop.offset, count=sop.ndofs, device=dev)
     r = torch.empty_like(x)
@@ -373,7 +403,7 @@ def main():
         #      replayed from one CUDA graph when an apply is short (cfg0 / cfg1: launch latency), under the same
         #      clock sampler; the roofline below uses this per-apply time (warm L2 for L2-resident vectors)
         est = max(statistics.median(step_ms), 1e-3)
-        R = int(min(20000, max(K, 200.0 / est)))
+        R = int(min(400000, max(K, 200.0 / est)))
         graph = None
         if est < 1.0 and world == 1:
             gs = torch.cuda.Stream(dev)
@@ -524,9 +554,11 @@ def main():
     ok = bool(torch.isfinite(r).all().item()) and r.abs().max().item() > 0
     halo = None
     if world > 1:
-        ap = sop._apply
+        ap = sop if isinstance(sop, _DistSlab) else sop._apply
         halo = {"payload": "face traces (u, d_0 u at the n^2 face points, dg_pack_halo)" if ap.traces else "boundary planes",
                 "bytes_per_message": 8 * ap.payload_doubles, "messages_per_rank": 4,
+                "exchange": "libdg dg_apply_dist (own NCCL communicator)" if isinstance(sop, _DistSlab)
+                else "slab.py over torch.distributed (NCCL)",
                 "overlap": "interior planes on the compute stream while the exchange runs on a high-priority stream; "
                            "NVTX ranges slab:pack / slab:interior / slab:halo / slab:boundary"}
     line = {

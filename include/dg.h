@@ -42,6 +42,7 @@ extern "C" {
 #define DG_ERR_INVALID (-1)     /* bad argument (sizes, pointers, aliasing, unsupported k) */
 #define DG_ERR_UNSUPPORTED (-2) /* valid request this build does not implement (e.g. quad outside k+1..k+3) */
 #define DG_ERR_CUDA (-3)        /* CUDA runtime failure (no device, launch error, ...) */
+#define DG_ERR_NCCL (-4)        /* NCCL unavailable or failed (collective entry points only) */
 #define DG_ERR_OOM (-5)         /* device or pinned-host allocation failed */
 
 #define DG_GEOM_AXIS 0   /* J_T = diag(1/N0, 1/N1, 1/N2) */
@@ -141,6 +142,24 @@ int dg_pack_halo(dg_ctx* ctx, const double* x, double* tr_lo, double* tr_hi);
 int dg_apply_planes_tr(dg_ctx* ctx, const double* x, const double* tr_below, const double* tr_above, double* r,
                        int p_begin, int p_end);
 
+/* Collective form: the mesh split into x0-slabs over nranks processes (one GPU each),
+ * rank q owning planes [q N0 / nranks, (q+1) N0 / nranks) — a contiguous range of the canonical vector, the
+ * periodic wrap making the ranks a ring. The context owns an NCCL communicator (libnccl.so.2 is loaded at run
+ * time); one application is ONE point-to-point exchange step (ncclSend / ncclRecv of the two boundary payloads
+ * with ranks q -+ 1 on a high-priority stream) overlapped with the interior planes, then the two boundary planes.
+ * Payload: the face traces of dg_pack_halo for k_gen / k_axis8 / k_line, the full boundary planes otherwise.
+ * dg_slab_range: the planes of a rank (plane_begin, nplanes) — use it to fill the mesh (and its jac, L+2 planes).
+ * dg_get_unique_id: a 128-byte ncclUniqueId (one rank creates it and broadcasts it by its own means).
+ * dg_setup_dist: COLLECTIVE (every rank, same arguments but rank); mesh->plane_begin / nplanes must be the
+ *   rank's slab. nranks = 1 is valid (the exchange is a send / receive to itself: a loopback of the same code).
+ * dg_apply_dist: COLLECTIVE, every rank in the same order; x, r DEVICE, dg_local_ndofs doubles (the slab), as
+ *   dg_apply. Asynchronous on the context stream (the exchange runs on the context's own comm stream).
+ * DG_ERR_NCCL if NCCL is missing or fails. dg_destroy releases the communicator. */
+int dg_slab_range(int N0, int rank, int nranks, int32_t* plane_begin, int32_t* nplanes);
+int dg_get_unique_id(void* nccl_id_128);
+int dg_setup_dist(const dg_mesh* mesh, int k, int quad, int rank, int nranks, const void* nccl_id_128, dg_ctx** out);
+int dg_apply_dist(dg_ctx* ctx, const double* x, double* r);
+
 /* The action of the Jacobian of a DG_PROBLEM_NLREAC residual at the linearization point u0
  * ("not only the solution needs to be evaluated in step 1 ... but also the given
  * linearization point"; A_i(c, z) = (J z)_i, depending on both c and z):
@@ -177,7 +196,8 @@ int64_t dg_plane_ndofs(const dg_ctx* ctx);  /* N1 N2 n^3: size of one x0-plane (
 double dg_alg_flops(const dg_ctx* ctx);
 double dg_alg_bytes(const dg_ctx* ctx);
 
-/* Kernel launches enqueued by one dg_apply / dg_apply_planes call, and the name of the kernel. */
+/* Kernel launches enqueued by one dg_apply / dg_apply_planes call (dg_apply_dist: pack + interior + 2
+ * boundary launches), and the name of the kernel. */
 int dg_launches_per_apply(const dg_ctx* ctx);
 const char* dg_kernel_name(const dg_ctx* ctx);
 

@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["dg_capi.cu", "tables.cpp", "fp64_peak.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-ldl"]
 
 
 def _stale() -> bool:

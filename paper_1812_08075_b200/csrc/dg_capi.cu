@@ -10,6 +10,8 @@
 #include "tables.h"
 
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only: the library is dlopen'ed (a process may already hold torch's libnccl.so.2)
 
 #include <cstdarg>
 #include <cstdio>
@@ -516,6 +518,14 @@ struct dg_ctx {
     double* hr_d;
     cudaStream_t s_h2d, s_d2h, s_cmp;
     cudaEvent_t ev_in[8], ev_cmp[8]; // created with the streams, destroyed by dg_destroy (no per-call events)
+    // collective form (dg_setup_dist / dg_apply_dist): library-owned NCCL communicator and halo state
+    ncclComm_t comm;
+    int rank, nranks;
+    bool dist_tr;                  // trace halos (k_gen, k_axis8, k_line) or full boundary planes
+    int64_t halo_n;                // doubles per halo message
+    double *d_hb, *d_ha, *d_tlo, *d_thi;
+    cudaStream_t s_comm;
+    cudaEvent_t ev_x, ev_halo;
     int64_t plane_dofs, local_dofs;
 };
 
@@ -604,6 +614,61 @@ int host_line_ops(const dg::HostTables& Ht, double P, const double* x, const dou
     return DG_OK;
 }
 } // namespace
+
+// ---- NCCL, loaded at run time (dlopen of libnccl.so.2: the process's already-loaded instance, e.g. torch's, or the
+// system one); only the collective entry points need it
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+static const NcclApi* nccl_api()
+{
+    static NcclApi api;
+    static int state = 0; // 0 untried, 1 ok, -1 unavailable
+    if (state == 0) {
+        state = -1;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+        if (h) {
+            api.GetUniqueId = (ncclResult_t(*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+            api.CommInitRank = (ncclResult_t(*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (ncclResult_t(*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+            api.Send = (ncclResult_t(*)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclSend");
+            api.Recv = (ncclResult_t(*)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclRecv");
+            api.GroupStart = (ncclResult_t(*)())dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (ncclResult_t(*)())dlsym(h, "ncclGroupEnd");
+            api.GetErrorString = (const char* (*)(ncclResult_t))dlsym(h, "ncclGetErrorString");
+            if (api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+                api.GroupEnd && api.GetErrorString)
+                state = 1;
+        }
+    }
+    return state == 1 ? &api : nullptr;
+}
+
+static void dist_release(dg_ctx* c)
+{
+    if (c->comm) {
+        if (const NcclApi* N = nccl_api()) N->CommDestroy(c->comm);
+        c->comm = nullptr;
+    }
+    if (c->d_hb) cudaFree(c->d_hb);
+    if (c->d_ha) cudaFree(c->d_ha);
+    if (c->d_tlo) cudaFree(c->d_tlo);
+    if (c->d_thi) cudaFree(c->d_thi);
+    if (c->s_comm) cudaStreamDestroy(c->s_comm);
+    if (c->ev_x) cudaEventDestroy(c->ev_x);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    c->d_hb = c->d_ha = c->d_tlo = c->d_thi = nullptr;
+    c->s_comm = nullptr;
+    c->ev_x = c->ev_halo = nullptr;
+}
 
 // release a partially built context and report the failure (dg_setup never leaks on an error path)
 static int setup_fail(dg_ctx* c, int code, const char* fmt, ...)
@@ -928,6 +993,7 @@ int dg_destroy(dg_ctx* c)
         if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
         if (c->ev_cmp[i]) cudaEventDestroy(c->ev_cmp[i]);
     }
+    dist_release(c);
     free(c);
     return DG_OK;
 }
@@ -942,7 +1008,13 @@ int dg_set_stream(dg_ctx* c, void* stream)
 int64_t dg_local_ndofs(const dg_ctx* c) { return c ? c->local_dofs : -1; }
 int64_t dg_local_offset(const dg_ctx* c) { return c ? (int64_t)c->mesh.plane_begin * c->plane_dofs : -1; }
 int64_t dg_plane_ndofs(const dg_ctx* c) { return c ? c->plane_dofs : -1; }
-int dg_launches_per_apply(const dg_ctx* c) { return c ? 1 : -1; }
+int dg_launches_per_apply(const dg_ctx* c)
+{
+    if (!c) return -1;
+    if (!c->comm) return 1;
+    // collective: (pack) + interior + 2 boundary launches (L <= 2: one launch after the exchange)
+    return (c->M.L > 2 ? 3 : 1) + (c->dist_tr ? 1 : 0);
+}
 const char* dg_kernel_name(const dg_ctx* c) { return c ? c->kname : ""; }
 
 int dg_line_ops(int k, double penalty_scale, const double* x, const double* nb, double* out)
@@ -1172,6 +1244,121 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
     }
     CU(cudaStreamSynchronize(c->s_d2h));
     return DG_OK;
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// Collective form: x0-slabs over nranks processes, one NCCL point-to-point halo step per
+// application, overlapped with the interior planes (include/dg.h).
+
+int dg_slab_range(int N0, int rank, int nranks, int32_t* plane_begin, int32_t* nplanes)
+{
+    if (!plane_begin || !nplanes) return fail(DG_ERR_INVALID, "dg_slab_range: NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks || N0 < nranks)
+        return fail(DG_ERR_INVALID, "dg_slab_range: rank %d of %d on %d planes", rank, nranks, N0);
+    const int b = (int)((int64_t)rank * N0 / nranks), e = (int)((int64_t)(rank + 1) * N0 / nranks);
+    *plane_begin = b;
+    *nplanes = e - b;
+    return DG_OK;
+}
+
+int dg_get_unique_id(void* id)
+{
+    if (!id) return fail(DG_ERR_INVALID, "dg_get_unique_id: NULL argument");
+    const NcclApi* N = nccl_api();
+    if (!N) return fail(DG_ERR_NCCL, "dg_get_unique_id: libnccl.so.2 not found");
+    ncclUniqueId u;
+    const ncclResult_t e = N->GetUniqueId(&u);
+    if (e != ncclSuccess) return fail(DG_ERR_NCCL, "ncclGetUniqueId: %s", N->GetErrorString(e));
+    memcpy(id, &u, sizeof u);
+    return DG_OK;
+}
+
+int dg_setup_dist(const dg_mesh* mesh, int k, int quad, int rank, int nranks, const void* nccl_id, dg_ctx** out)
+{
+    g_err.clear();
+    if (!mesh || !out || !nccl_id) return fail(DG_ERR_INVALID, "dg_setup_dist: NULL argument");
+    *out = nullptr;
+    int32_t pb = 0, np = 0;
+    int rc = dg_slab_range(mesh->N[0], rank, nranks, &pb, &np);
+    if (rc != DG_OK) return rc;
+    if (mesh->plane_begin != pb || mesh->nplanes != np)
+        return fail(DG_ERR_INVALID, "dg_setup_dist: mesh slab [%d, +%d) is not rank %d's slab [%d, +%d) (dg_slab_range)",
+                    mesh->plane_begin, mesh->nplanes, rank, pb, np);
+    const NcclApi* N = nccl_api();
+    if (!N) return fail(DG_ERR_NCCL, "dg_setup_dist: libnccl.so.2 not found");
+    dg_ctx* c = nullptr;
+    rc = dg_setup(mesh, k, quad, &c);
+    if (rc != DG_OK) return rc;
+    c->rank = rank;
+    c->nranks = nranks;
+    // trace halos where the kernel consumes them (dg_apply_planes_tr), else full boundary planes
+    c->dist_tr = c->gen || c->ax8 || c->line;
+    c->halo_n = c->dist_tr ? dg_halo_ndofs(c) : c->plane_dofs;
+    const size_t hb = sizeof(double) * (size_t)c->halo_n;
+    cudaError_t e = cudaMalloc(&c->d_hb, hb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_ha, hb);
+    if (e == cudaSuccess && c->dist_tr) e = cudaMalloc(&c->d_tlo, hb);
+    if (e == cudaSuccess && c->dist_tr) e = cudaMalloc(&c->d_thi, hb);
+    if (e != cudaSuccess) return setup_fail(c, DG_ERR_OOM, "dg_setup_dist: halo buffers: %s", cudaGetErrorString(e));
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    e = cudaStreamCreateWithPriority(&c->s_comm, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
+    if (e != cudaSuccess) return setup_fail(c, DG_ERR_CUDA, "dg_setup_dist: streams / events: %s", cudaGetErrorString(e));
+    ncclUniqueId u;
+    memcpy(&u, nccl_id, sizeof u);
+    const ncclResult_t ne = N->CommInitRank(&c->comm, nranks, u, rank);
+    if (ne != ncclSuccess) {
+        c->comm = nullptr;
+        return setup_fail(c, DG_ERR_NCCL, "ncclCommInitRank(rank %d of %d): %s", rank, nranks, N->GetErrorString(ne));
+    }
+    *out = c;
+    return DG_OK;
+}
+
+int dg_apply_dist(dg_ctx* c, const double* x, double* r)
+{
+    if (!c || !x || !r) return fail(DG_ERR_INVALID, "dg_apply_dist: NULL argument");
+    if (!c->comm) return fail(DG_ERR_INVALID, "dg_apply_dist: context was not created by dg_setup_dist");
+    const NcclApi* N = nccl_api();
+    const int L = c->M.L;
+    const int below = (c->rank + c->nranks - 1) % c->nranks, above = (c->rank + 1) % c->nranks;
+    const int halo_tr = c->dist_tr ? 3 : 0;
+    CU(cudaSetDevice(c->device));
+    const double *send_lo, *send_hi;
+    if (c->dist_tr) {
+        const int rc = dg_pack_halo(c, x, c->d_tlo, c->d_thi);
+        if (rc != DG_OK) return rc;
+        send_lo = c->d_tlo;
+        send_hi = c->d_thi;
+    } else {
+        send_lo = x;
+        send_hi = x + (size_t)(L - 1) * c->plane_dofs;
+    }
+    CU(cudaEventRecord(c->ev_x, c->stream));
+    CU(cudaStreamWaitEvent(c->s_comm, c->ev_x, 0));
+    // interior planes (their x0-neighbours are local; the halos are not read) overlap the exchange
+    if (L > 2) {
+        const int rc = apply_planes_impl(c, x, c->d_hb, c->d_ha, r, 1, L - 1, nullptr, halo_tr);
+        if (rc != DG_OK) return rc;
+    }
+    // one exchange step: my lowest plane's payload -> rank below (its halo above), my highest -> rank above;
+    // NCCL pairs the point-to-point operations between two ranks in posting order (also rank == peer)
+    ncclResult_t ne = N->GroupStart();
+    if (ne == ncclSuccess) ne = N->Send(send_lo, (size_t)c->halo_n, ncclDouble, below, c->comm, c->s_comm);
+    if (ne == ncclSuccess) ne = N->Send(send_hi, (size_t)c->halo_n, ncclDouble, above, c->comm, c->s_comm);
+    if (ne == ncclSuccess) ne = N->Recv(c->d_ha, (size_t)c->halo_n, ncclDouble, above, c->comm, c->s_comm);
+    if (ne == ncclSuccess) ne = N->Recv(c->d_hb, (size_t)c->halo_n, ncclDouble, below, c->comm, c->s_comm);
+    const ncclResult_t ge = N->GroupEnd();
+    if (ne == ncclSuccess) ne = ge;
+    if (ne != ncclSuccess) return fail(DG_ERR_NCCL, "dg_apply_dist: halo exchange: %s", N->GetErrorString(ne));
+    CU(cudaEventRecord(c->ev_halo, c->s_comm));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    if (L <= 2) return apply_planes_impl(c, x, c->d_hb, c->d_ha, r, 0, L, nullptr, halo_tr);
+    int rc = apply_planes_impl(c, x, c->d_hb, c->d_ha, r, 0, 1, nullptr, halo_tr);
+    if (rc == DG_OK) rc = apply_planes_impl(c, x, c->d_hb, c->d_ha, r, L - 1, L, nullptr, halo_tr);
+    return rc;
 }
 
 } // extern "C"

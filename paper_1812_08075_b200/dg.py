@@ -18,6 +18,7 @@ DG_OK = 0
 DG_ERR_INVALID = -1
 DG_ERR_UNSUPPORTED = -2
 DG_ERR_CUDA = -3
+DG_ERR_NCCL = -4
 DG_ERR_OOM = -5
 DG_GEOM_AXIS = 0
 DG_GEOM_AFFINE = 1
@@ -28,7 +29,7 @@ DG_PROBLEM_DIFFREAC = 1
 DG_PROBLEM_NLREAC = 2
 DG_PROBLEM_STOKES = 3
 
-_ERRNAMES = {-1: "DG_ERR_INVALID", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_CUDA", -5: "DG_ERR_OOM"}
+_ERRNAMES = {-1: "DG_ERR_INVALID", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_CUDA", -4: "DG_ERR_NCCL", -5: "DG_ERR_OOM"}
 
 
 class DgError(RuntimeError):
@@ -55,7 +56,8 @@ class dg_mesh(ctypes.Structure):
 EXPORTS = ["dg_setup", "dg_apply", "dg_apply_planes", "dg_apply_host", "dg_destroy", "dg_set_stream",
            "dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs", "dg_alg_flops", "dg_alg_bytes",
            "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops",
-           "dg_apply_jacobian", "dg_apply_jacobian_planes", "dg_halo_ndofs", "dg_pack_halo", "dg_apply_planes_tr"]
+           "dg_apply_jacobian", "dg_apply_jacobian_planes", "dg_halo_ndofs", "dg_pack_halo", "dg_apply_planes_tr", "dg_slab_range", "dg_get_unique_id",
+           "dg_setup_dist", "dg_apply_dist"]
 
 _lib = None
 
@@ -75,6 +77,12 @@ def load(path: str = LIB_PATH):
     L.dg_apply_planes.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
     L.dg_apply_planes_tr.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
     L.dg_pack_halo.argtypes = [vp, vp, vp, vp]
+    L.dg_slab_range.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_int32)]
+    L.dg_get_unique_id.argtypes = [vp]
+    L.dg_setup_dist.argtypes = [ctypes.POINTER(dg_mesh), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                                ctypes.POINTER(vp)]
+    L.dg_apply_dist.argtypes = [vp, vp, vp]
     L.dg_apply_host.argtypes = [vp, vp, vp]
     L.dg_apply_jacobian.argtypes = [vp, vp, vp, vp]
     L.dg_apply_jacobian_planes.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int]
@@ -113,27 +121,64 @@ def dg_setup(N, k: int, quad: int, *, plane_begin: int = 0, nplanes: int | None 
              jac: np.ndarray | None = None, coeff_kind: int = 0, penalty_scale: float = 10.0, device: int = 0,
              stream: int | None = None, problem: int = 0) -> int:
     """Returns an opaque context handle (int). jac: host float64 array [(L+2) N1 N2, 9] for affine."""
-    L = load()
+    m, _keep = _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem)
+    h = ctypes.c_void_p()
+    _check(load().dg_setup(ctypes.byref(m), k, quad, ctypes.byref(h)))
+    return h.value
+
+
+def _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem):
+    """dg_mesh for the C-ABI (+ the contiguous jac array it points to, kept alive by the caller)."""
     m = dg_mesh()
     m.N[0], m.N[1], m.N[2] = int(N[0]), int(N[1]), int(N[2])
     m.plane_begin = plane_begin
     m.nplanes = int(N[0]) if nplanes is None else nplanes
     m.geom_kind = geom_kind
+    keep = None
     if jac is not None:
-        jac = np.ascontiguousarray(jac, dtype=np.float64)
-        L_ = m.nplanes
-        need = 9 * (L_ + 2) * int(N[1]) * int(N[2])  # J of the L+2 planes plane_begin-1 .. plane_begin+L
-        if jac.size != need:
-            raise DgError(DG_ERR_INVALID, f"jac has {jac.size} doubles, the slab needs {need} (9 per cell of L+2 planes)")
-        m.jac = jac.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        keep = np.ascontiguousarray(jac, dtype=np.float64)
+        need = 9 * (m.nplanes + 2) * int(N[1]) * int(N[2])
+        if keep.size != need:
+            raise DgError(DG_ERR_INVALID, f"jac has {keep.size} doubles, the slab needs {need} (9 per cell of L+2 planes)")
+        m.jac = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     m.coeff_kind = coeff_kind
     m.penalty_scale = float(penalty_scale)
     m.device = device
     m.stream = stream
     m.problem = problem
+    return m, keep
+
+
+def dg_slab_range(N0: int, rank: int, nranks: int):
+    """(plane_begin, nplanes) of a rank in the collective form's x0-slab split."""
+    b, n = ctypes.c_int32(), ctypes.c_int32()
+    _check(load().dg_slab_range(int(N0), rank, nranks, ctypes.byref(b), ctypes.byref(n)))
+    return b.value, n.value
+
+
+def dg_get_unique_id() -> bytes:
+    """A 128-byte ncclUniqueId for dg_setup_dist (create on one rank, broadcast)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().dg_get_unique_id(buf))
+    return buf.raw
+
+
+def dg_setup_dist(N, k: int, quad: int, rank: int, nranks: int, nccl_id: bytes, *, geom_kind: int = 0,
+                  jac: np.ndarray | None = None, coeff_kind: int = 0, penalty_scale: float = 10.0, device: int = 0,
+                  stream: int | None = None, problem: int = 0) -> int:
+    """Collective context for rank `rank` of `nranks` (include/dg.h): jac covers the rank's L+2 planes."""
+    pb, npl = dg_slab_range(int(N[0]), rank, nranks)
+    m, _keep = _mesh(N, pb, npl, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem)
+    if len(nccl_id) != 128:
+        raise DgError(DG_ERR_INVALID, "nccl_id must be 128 bytes")
+    idbuf = ctypes.create_string_buffer(nccl_id, 128)
     h = ctypes.c_void_p()
-    _check(L.dg_setup(ctypes.byref(m), k, quad, ctypes.byref(h)))
+    _check(load().dg_setup_dist(ctypes.byref(m), k, quad, rank, nranks, idbuf, ctypes.byref(h)))
     return h.value
+
+
+def dg_apply_dist(ctx: int, x, r):
+    _check(load().dg_apply_dist(ctx, _ptr(x), _ptr(r)))
 
 
 def dg_apply(ctx: int, x, r):
@@ -351,3 +396,37 @@ class Operator:
             self.close()
         except Exception:
             pass
+
+
+class DistOperator(Operator):
+    """The collective form (dg_setup_dist / dg_apply_dist): this rank's x0-slab, the halo exchange done by libdg's own
+    NCCL communicator. Every rank constructs it with the same nccl_id and calls apply in the same order."""
+
+    def __init__(self, N, k: int, rank: int, nranks: int, nccl_id: bytes, *, geom_kind: int = 0, coeff_kind: int = 0,
+                 penalty_scale: float = 10.0, jac: np.ndarray | None = None, device: int = 0, stream=None,
+                 quad: int | None = None, problem: int = 0):
+        import torch
+        self.N = tuple(int(v) for v in N)
+        self.k = k
+        self.n = k + 1
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self._stream = stream
+        self.rank, self.nranks = rank, nranks
+        self.ctx = dg_setup_dist(self.N, k, k + 1 if quad is None else quad, rank, nranks, nccl_id,
+                                 geom_kind=geom_kind, jac=jac, coeff_kind=coeff_kind, penalty_scale=penalty_scale,
+                                 device=device, stream=stream.cuda_stream, problem=problem)
+        self.ndofs = dg_local_ndofs(self.ctx)
+        self.offset = dg_local_offset(self.ctx)
+        self.plane_ndofs = dg_plane_ndofs(self.ctx)
+        self.halo_ndofs = dg_halo_ndofs(self.ctx)
+        self.nplanes = self.ndofs // self.plane_ndofs
+
+    def apply(self, x, r=None):
+        import torch
+        self._chk(x)
+        if r is None:
+            r = torch.empty_like(x)
+        self._chk(r)
+        dg_apply_dist(self.ctx, x, r)
+        return r

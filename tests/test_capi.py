@@ -52,7 +52,7 @@ def test_errors_without_device_or_bad_args(lib):
     m.penalty_scale = 10.0
     h = ctypes.c_void_p()
     assert lib.dg_setup(ctypes.byref(m), 9, 10, ctypes.byref(h)) == dg.DG_ERR_INVALID
-    assert lib.dg_setup(ctypes.byref(m), 2, 5, ctypes.byref(h)) == dg.DG_ERR_UNSUPPORTED
+    assert lib.dg_setup(ctypes.byref(m), 2, 6, ctypes.byref(h)) == dg.DG_ERR_UNSUPPORTED  # k+4 points
     m.N[1] = 1
     assert lib.dg_setup(ctypes.byref(m), 2, 3, ctypes.byref(h)) == dg.DG_ERR_INVALID
     m.N[1] = 4
@@ -91,3 +91,32 @@ def test_problem_validation(lib):
     assert "Stokes" in dg.dg_last_error()
     assert lib.dg_apply_jacobian(None, None, None, None) == dg.DG_ERR_INVALID
     assert lib.dg_apply_jacobian_planes(None, None, None, None, None, None, 0, 0) == dg.DG_ERR_INVALID
+
+
+def test_slab_range_matches_slab_plan(lib):
+    """dg_slab_range (the collective form's partition, host-only) == slab.plan (the torch.distributed form)."""
+    from paper_1812_08075_b200 import dg, slab
+    for N0 in (2, 5, 96, 256):
+        for P in (1, 2, 3, 4, 8):
+            if N0 < P:
+                with pytest.raises(dg.DgError):
+                    dg.dg_slab_range(N0, 0, P)
+                continue
+            for q in range(P):
+                p = slab.plan(N0, q, P)
+                assert dg.dg_slab_range(N0, q, P) == (p.plane_begin, p.nplanes)
+
+
+def test_setup_dist_rejects_bad_args(lib):
+    from paper_1812_08075_b200 import dg
+    m = dg.dg_mesh()
+    m.N[0] = m.N[1] = m.N[2] = 4
+    m.nplanes = 4
+    m.penalty_scale = 10.0
+    h = ctypes.c_void_p()
+    idb = ctypes.create_string_buffer(128)
+    assert lib.dg_setup_dist(ctypes.byref(m), 2, 3, 0, 2, None, ctypes.byref(h)) == dg.DG_ERR_INVALID  # no id
+    assert lib.dg_setup_dist(ctypes.byref(m), 2, 3, 2, 2, idb, ctypes.byref(h)) == dg.DG_ERR_INVALID    # rank
+    assert lib.dg_setup_dist(ctypes.byref(m), 2, 3, 0, 2, idb, ctypes.byref(h)) == dg.DG_ERR_INVALID    # slab != rank 0's
+    assert "slab" in dg.dg_last_error()
+    assert lib.dg_apply_dist(None, None, None) == dg.DG_ERR_INVALID

@@ -25,18 +25,18 @@ done
 ncu --set full --clock-control none --import-source on -k regex:k_axis8 -s 3 -c 1 -o $O/prof_axis8_cfg3 python bench.py --config 3 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg2 python bench.py --config 2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg4 python bench.py --config 4 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu4.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_gen -s 3 -c 1 -o $O/prof_gen_cfg1 python bench.py --config 1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_line -s 3 -c 1 -o $O/prof_line_cfg1 python bench.py --config 1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu1.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_quad -s 3 -c 1 -o $O/prof_quad_dr3 python bench.py --problem diffreac --k 3 --N 64 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu5.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_stokes -s 3 -c 1 -o $O/prof_stokes_k3 python bench.py --problem stokes --k 3 --N 48 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu7.log 2>&1
-python tools/ncu_counters.py $O/ncu_counters.json cfg3_poisson_q7_96:k_axis8:$O/prof_axis8_cfg3.ncu-rep cfg2_diffusion_q5_64_affine:k_gen:$O/prof_gen_cfg2.ncu-rep cfg4_diffusion_q4_256_affine:k_gen:$O/prof_gen_cfg4.ncu-rep cfg1_poisson_q3_32:k_gen:$O/prof_gen_cfg1.ncu-rep > $O/counters.log 2>&1
-for R2 in axis8_cfg3 gen_cfg2 gen_cfg4 gen_cfg1 quad_dr3 stokes_k3; do
+python tools/ncu_counters.py $O/ncu_counters.json cfg3_poisson_q7_96:k_axis8:$O/prof_axis8_cfg3.ncu-rep cfg2_diffusion_q5_64_affine:k_gen:$O/prof_gen_cfg2.ncu-rep cfg4_diffusion_q4_256_affine:k_gen:$O/prof_gen_cfg4.ncu-rep cfg1_poisson_q3_32:k_line:$O/prof_line_cfg1.ncu-rep > $O/counters.log 2>&1
+for R2 in axis8_cfg3 gen_cfg2 gen_cfg4 line_cfg1 quad_dr3 stokes_k3; do
   python tools/ncu_stalls.py $O/prof_$R2.ncu-rep > $O/stalls_$R2.txt 2>&1
   python tools/ncu_stalls.py $O/prof_$R2.ncu-rep --lines >> $O/stalls_$R2.txt 2>&1
 done
 python tools/ncu_summary.py --launches $O/launches_cfg3.csv --rep $O/prof_axis8_cfg3.ncu-rep --out $O/ncu_axis8_cfg3 --title "k_axis8 on cfg3 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --launches $O/launches_cfg2.csv --rep $O/prof_gen_cfg2.ncu-rep --out $O/ncu_gen_cfg2 --title "k_gen on cfg2 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --launches $O/launches_cfg4.csv --rep $O/prof_gen_cfg4.ncu-rep --out $O/ncu_gen_cfg4 --title "k_gen on cfg4 (N=1)" > /dev/null 2>&1
-python tools/ncu_summary.py --launches $O/launches_cfg1.csv --rep $O/prof_gen_cfg1.ncu-rep --out $O/ncu_gen_cfg1 --title "k_gen on cfg1 (N=1)" > /dev/null 2>&1
+python tools/ncu_summary.py --launches $O/launches_cfg1.csv --rep $O/prof_line_cfg1.ncu-rep --out $O/ncu_line_cfg1 --title "k_line on cfg1 (N=1)" > /dev/null 2>&1
 python tools/ncu_summary.py --rep $O/prof_quad_dr3.ncu-rep --out $O/ncu_quad_dr3 --title "k_quad_diffreac, k=3 on 64^3 (SURVEY 8(f1))" > /dev/null 2>&1
 python tools/ncu_summary.py --rep $O/prof_stokes_k3.ncu-rep --out $O/ncu_stokes_k3 --title "k_stokes, k=3 on 48^3 (SURVEY 8(f4))" > /dev/null 2>&1
 mkdir -p $O/reps && mv $O/prof_gen_cfg4.ncu-rep $O/reps/ 2>/dev/null
