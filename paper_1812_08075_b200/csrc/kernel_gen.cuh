@@ -177,6 +177,23 @@ struct TRView {
     __device__ __forceinline__ TRRef operator[](int p) const { return TRRef{u[p], g[p]}; }
 };
 
+// lane -> task (fo N + l) of the warp-local face pass B (t2-lines); -1: idle lane. Tables from an offline search
+// (tools/passb_perm.py) for the face-slot strides FSD = FB = TSEL mod 16 of Lay; identity for other n
+__constant__ signed char c_passb3[32] = {26, 16, 11, 10, 23, 5, 29, 20, 28, 17, 13, 0, 19, 12, 14, 3,
+                                        1, 7, 9, 22, 6, 21, 15, 8, 2, 24, 25, 27, 18, 4, -1, -1};
+__constant__ signed char c_passb4[32] = {26, 17, 11, 10, 28, 1, 4, 7, 16, 9, 19, 13, 0, 23, 14, 18,
+                                        5, 30, 22, 21, 29, 6, 12, 20, 15, 3, 31, 2, 24, 25, 27, 8};
+__constant__ signed char c_passb5[32] = {26, 16, 11, 10, 23, 1, 5, 7, 20, 9, 28, 13, 19, 22, 6, 24,
+                                        29, 17, 0, 12, 21, 14, 15, 3, 8, 2, 25, 27, 18, 4, -1, -1};
+template <int N>
+__device__ __forceinline__ int passb_task(int lane)
+{
+    if (N == 3) return c_passb3[lane];
+    if (N == 4) return c_passb4[lane];
+    if (N == 5) return c_passb5[lane];
+    return lane < (32 / N) * N ? lane : -1;
+}
+
 // shared-memory layout (in doubles) of k_gen<N, AFFINE, COEFF, T1, T2>
 template <int N, bool AFFINE, bool COEFF, int T1, int T2>
 struct Lay {
@@ -218,7 +235,7 @@ struct Lay {
     static constexpr int S0 = NC * N2 + P0, S1 = NC * N2 + P1;
     static constexpr int G01 = GE + (AFFINE ? 2 * NCG * GREC : 0);      // G0 [N][S0], G1 [N][S1]: grad0/1 -> Q0/1 -> R0/1
     static constexpr int TRB = (G01 + N * (S0 + S1) + 1) / 2 * 2;                       // [NF][u|V, gn|G][side][N2] (+ pad)
-    static constexpr int CX = TRB + NF * FSD;                           // [2][NC][CXSZ] c(x) factor tables (volume)
+    static constexpr int CX = (TRB + NF * FSD + 1) / 2 * 2;             // [2][NC][CXSZ] c(x) factor tables (volume; 16-B pairs)
     static constexpr int CF = CX + (COEFF ? 2 * NC * CXSZ : 0);         // [2][NCG][CFSZ] c(x) at upper-face points
     static constexpr int END = CF + (COEFF ? 2 * NCG * CFSZ : 0);
     static constexpr int BYTES = END * 8 + 64; // + 2 mbarriers
@@ -365,6 +382,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     __shared__ double sXi[N + 1], sD[N * N], sW[N];
 
     const int tid = threadIdx.x;
+    const int passb_t = gn::passb_task<N>(tid & 31); // warp-local face pass B lane order
     const int ntile2 = M.N2 / T2;
     const int ntiles = (M.N1 / T1) * ntile2;
     const int chunk = blockIdx.x / ntiles, tile = blockIdx.x % ntiles;
@@ -706,20 +724,31 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         const int fo = HALF ? (lane >> 4) * FPH + hl / N : lane / N;
         const int l = hl - (hl / N) * N;
         const bool lane_on = HALF ? hl < FPH * N : lane < FPW * N;
+        // pass B (t2-lines, lane offsets FSD fo + l) under the lane order of passes A / C is 2-way bank conflicted;
+        // its own lane -> (face, line) order (searched offline: one half-warp with distinct FSD fo + l mod 16, the
+        // other with at most two 2-way pairs) serves the same warp-local tasks: 3 wavefronts instead of 4
+        const int tb = passb_t;
+        const int foB = HALF ? fo : (tb >= 0 ? tb / N : 0), lB = HALF ? l : (tb >= 0 ? tb - (tb / N) * N : 0);
+        const bool onB_lane = HALF ? lane_on : tb >= 0;
+        auto face_of = [&](int o, int& f, int& d) {
+            if (o < NC) { f = 3 * o; d = 0; }
+            else if (o < 2 * NC) { f = 3 * (o - NC) + 1; d = 1; }
+            else if (o < 3 * NC) { f = 3 * (o - 2 * NC) + 2; d = 2; }
+            else { f = o; d = (o < 3 * NC + T2) ? 1 : 2; }
+        };
         for (int base = 0; base < NF; base += FPW * NWARP) {
             const int o = base + warp * FPW + fo;
             const bool on = lane_on && o < NF;
             int f = 0, d = 0;
-            if (on) {
-                if (o < NC) { f = 3 * o; d = 0; }
-                else if (o < 2 * NC) { f = 3 * (o - NC) + 1; d = 1; }
-                else if (o < 3 * NC) { f = 3 * (o - 2 * NC) + 2; d = 2; }
-                else { f = o; d = (o < 3 * NC + T2) ? 1 : 2; }
-            }
+            if (on) face_of(o, f, d);
             const gn::RunD DC{d};
+            const int oB = base + warp * FPW + foB;
+            const bool onB = onB_lane && oB < NF;
+            int fB = 0, dB = 0;
+            if (onB) face_of(oB, fB, dB);
             if (on) lineA(DC, gb, f, l);
             __syncwarp();
-            if (on) lineB(DC, gb, f, l);
+            if (onB) lineB(gn::RunD{dB}, gb, fB, lB);
             __syncwarp();
             if (on) lineC(DC, gb, f, l);
             __syncwarp();
@@ -997,16 +1026,24 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
         // ---------------- P2: stage 2 at the thread's d=2 line points (a, b, q); face pass A ----------------
         double q2[N];
         if (act) {
+            // geometry (G~, 16-B pairs) and c(x) factors ((cos, sin) pairs) as 16-B loads: one shared-memory
+            // wavefront per warp instruction for these cell-uniform / row-uniform values
             double gt[6];
+            if (AFFINE) {
+                const double2* g2p = reinterpret_cast<const double2*>(gb + mc * GREC);
+                const double2 ga = g2p[0], gbb = g2p[1], gc = g2p[2];
+                gt[0] = ga.x; gt[1] = ga.y; gt[2] = gbb.x; gt[3] = gbb.y; gt[4] = gc.x; gt[5] = gc.y;
+            } else {
 #pragma unroll
-            for (int i = 0; i < 6; ++i) gt[i] = AFFINE ? gb[mc * GREC + i] : 0.0;
+                for (int i = 0; i < 6; ++i) gt[i] = 0.0;
+            }
             double z0r = 0, z0i = 0, z1r = 0, z1i = 0;
+            const double2* cx2 = reinterpret_cast<const double2*>(cxcur + mc * CXSZ); // [k][b][q] (cos, sin)
             if (COEFF) {
-                const double* cx = cxcur + mc * CXSZ;
-                gn::cmul(cx[((0 * 3 + 0) * (N + 1) + ma) * 2], cx[((0 * 3 + 0) * (N + 1) + ma) * 2 + 1],
-                         cx[((0 * 3 + 1) * (N + 1) + mb) * 2], cx[((0 * 3 + 1) * (N + 1) + mb) * 2 + 1], z0r, z0i);
-                gn::cmul(cx[((1 * 3 + 0) * (N + 1) + ma) * 2], cx[((1 * 3 + 0) * (N + 1) + ma) * 2 + 1],
-                         cx[((1 * 3 + 1) * (N + 1) + mb) * 2], cx[((1 * 3 + 1) * (N + 1) + mb) * 2 + 1], z1r, z1i);
+                const double2 a0 = cx2[(0 * 3 + 0) * (N + 1) + ma], b0 = cx2[(0 * 3 + 1) * (N + 1) + mb];
+                const double2 a1 = cx2[(1 * 3 + 0) * (N + 1) + ma], b1 = cx2[(1 * 3 + 1) * (N + 1) + mb];
+                gn::cmul(a0.x, a0.y, b0.x, b0.y, z0r, z0i);
+                gn::cmul(a1.x, a1.y, b1.x, b1.y, z1r, z1i);
             }
             const double wab = sW[ma] * sW[mb];
 #pragma unroll
@@ -1014,11 +1051,10 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
                 const int P = gix0(2, q), P1 = gix1(2, q);
                 double cW = wab * E.w[q];
                 if (COEFF) {
-                    const double* cx = cxcur + mc * CXSZ;
-                    const double* e0 = cx + ((0 * 3 + 2) * (N + 1) + q) * 2;
-                    const double* e1 = cx + ((1 * 3 + 2) * (N + 1) + q) * 2;
-                    const double s0 = fma(z0r, e0[1], z0i * e0[0]);  // Im(z0 e0) = sin(2 pi x0)
-                    const double c1 = fma(z1r, e1[0], -z1i * e1[1]); // Re(z1 e1) = cos(2 pi x1)
+                    const double2 e0 = cx2[(0 * 3 + 2) * (N + 1) + q];
+                    const double2 e1 = cx2[(1 * 3 + 2) * (N + 1) + q];
+                    const double s0 = fma(z0r, e0.y, z0i * e0.x);  // Im(z0 e0) = sin(2 pi x0)
+                    const double c1 = fma(z1r, e1.x, -z1i * e1.y); // Re(z1 e1) = cos(2 pi x1)
                     cW *= fma(0.5 * s0, c1, 1.0);
                 }
                 const double a0 = G0[P], a1 = G1[P1], a2 = g2[q];
