@@ -277,6 +277,10 @@ def main():
     ap.add_argument("--comm", default="libdg", choices=["libdg", "torch"],
                     help="N > 1: the halo exchange of libdg's collective C-ABI (dg_apply_dist, its own NCCL "
                          "communicator; default) or of slab.py over torch.distributed")
+    ap.add_argument("--dist-loopback", action="store_true",
+                    help="N = 1: run the collective multi-GPU step (dg_setup_dist / dg_apply_dist with one rank: trace "
+                         "packing, interior planes, NCCL send/recv of the wrap halos to itself, boundary planes) instead "
+                         "of the single dg_apply launch; measures the cost of the slab-step structure on one GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -337,10 +341,11 @@ def main():
     def jac_fn(pb, npl):
         return synth.jac_planes_torch(w, pb, npl, device=dev).cpu().numpy()
 
-    if world > 1 and args.comm == "libdg" and not args.jacobian:
+    if (world > 1 or args.dist_loopback) and args.comm == "libdg" and not args.jacobian:
         # the collective C-ABI (dg_setup_dist / dg_apply_dist): libdg's own NCCL communicator and halo step
         uid = [dg.dg_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         pb, npl = dg.dg_slab_range(w.N[0], rank, world)
         jac = jac_fn(pb - 1, npl + 2) if w.geom_kind else None
         sop = _DistSlab(dg.DistOperator(w.N, w.k, rank, world, uid[0], geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
@@ -553,18 +558,21 @@ def main():
     # ---- sanity of the timed result (not a parity claim: tests/ do that): finite, nonzero
     ok = bool(torch.isfinite(r).all().item()) and r.abs().max().item() > 0
     halo = None
-    if world > 1:
+    if world > 1 or (args.dist_loopback and isinstance(sop, _DistSlab)):
         ap = sop if isinstance(sop, _DistSlab) else sop._apply
         halo = {"payload": "face traces (u, d_0 u at the n^2 face points, dg_pack_halo)" if ap.traces else "boundary planes",
                 "bytes_per_message": 8 * ap.payload_doubles, "messages_per_rank": 4,
-                "exchange": "libdg dg_apply_dist (own NCCL communicator)" if isinstance(sop, _DistSlab)
-                else "slab.py over torch.distributed (NCCL)",
+                "exchange": ("libdg dg_apply_dist (own NCCL communicator)" if isinstance(sop, _DistSlab)
+                             else "slab.py over torch.distributed (NCCL)")
+                            + (": one rank, the wrap halos sent / received to itself (--dist-loopback)" if world == 1 else ""),
                 "overlap": "interior planes on the compute stream while the exchange runs on a high-priority stream; "
                            "NVTX ranges slab:pack / slab:interior / slab:halo / slab:boundary"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": _config(w, world), "roofline": roof,
+        "dtype": "f64", "data": "synthetic",
+        "config": dict(_config(w, world), **({"mode": "dist-loopback: the collective slab step on one rank"}
+                                             if args.dist_loopback and world == 1 else {})), "roofline": roof,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": K * sop.launches_per_apply,
         "clocks": clk.summary(), "result_finite": ok,
         "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
