@@ -38,6 +38,14 @@ def lib():
         i64p = ctypes.POINTER(ctypes.c_int64)
         L.oracle_gauss_legendre.argtypes = [ctypes.c_int, dp, dp]
         L.oracle_basis_1d.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, dp]
+        L.oracle_basis_1d_b.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp]
+        L.oracle_gauss_lobatto.argtypes = [ctypes.c_int, dp]
+        L.oracle_apply_b.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, ctypes.c_int, dp, dp, i64p,
+                                     ctypes.c_int64]
+        L.oracle_apply_cells_local_b.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                                 ctypes.c_int, i64p, ctypes.c_int64, dp, dp, dp]
         L.oracle_apply.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, dp, ctypes.c_int, ctypes.c_double, dp, dp, i64p, ctypes.c_int64]
         L.oracle_apply_cells_local.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
@@ -81,14 +89,22 @@ def gauss_legendre(m: int):
     return xi, w
 
 
-def basis_1d(n: int, pts):
-    """Values and derivatives of the n Lagrange polynomials on the n GL nodes at `pts`:
-    arrays [len(pts), n]."""
+def gauss_lobatto(n: int):
+    """n Gauss-Lobatto nodes on [0,1] (oracle's own Newton iteration on P_{n-1}')."""
+    xi = np.zeros(n)
+    if lib().oracle_gauss_lobatto(n, _dp(xi)) != 0:
+        raise ValueError(f"invalid n={n}")
+    return xi
+
+
+def basis_1d(n: int, pts, basis: int = 0):
+    """Values and derivatives of the n Lagrange polynomials on the n GL nodes (basis 0) or the n Gauss-Lobatto
+    nodes (basis 1) at `pts`: arrays [len(pts), n]."""
     pts = np.ascontiguousarray(pts, dtype=np.float64)
     val = np.zeros((len(pts), n))
     der = np.zeros((len(pts), n))
-    if lib().oracle_basis_1d(n, len(pts), _dp(pts), _dp(val), _dp(der)) != 0:
-        raise ValueError("invalid n")
+    if lib().oracle_basis_1d_b(n, int(basis), len(pts), _dp(pts), _dp(val), _dp(der)) != 0:
+        raise ValueError("invalid n / basis")
     return val, der
 
 
@@ -108,8 +124,8 @@ def apply(w, x: np.ndarray, jac: np.ndarray | None = None, cells=None) -> np.nda
     else:
         cells = np.ascontiguousarray(cells, dtype=np.int64)
         cp, nc = _i64p(cells), len(cells)
-    rc = lib().oracle_apply(w.N[0], w.N[1], w.N[2], w.k, w.m, w.geom_kind, jp, w.coeff_kind,
-                            float(w.penalty_scale), _dp(x), _dp(r), cp, nc)
+    rc = lib().oracle_apply_b(w.N[0], w.N[1], w.N[2], w.k, w.m, w.geom_kind, jp, w.coeff_kind,
+                              float(w.penalty_scale), int(getattr(w, "basis", 0)), _dp(x), _dp(r), cp, nc)
     if rc != 0:
         raise ValueError("oracle_apply: invalid arguments")
     return r
@@ -202,9 +218,9 @@ def apply_cells_local(w, cells, x7: np.ndarray, j7: np.ndarray | None) -> np.nda
         j7 = np.zeros((len(cells), 7, 9))
     j7 = np.ascontiguousarray(j7, dtype=np.float64).reshape(len(cells), 7, 9)
     r = np.zeros((len(cells), n3))
-    rc = lib().oracle_apply_cells_local(w.N[0], w.N[1], w.N[2], w.k, w.m, w.geom_kind, w.coeff_kind,
-                                        float(w.penalty_scale), _i64p(cells), len(cells), _dp(x7),
-                                        _dp(j7), _dp(r))
+    rc = lib().oracle_apply_cells_local_b(w.N[0], w.N[1], w.N[2], w.k, w.m, w.geom_kind, w.coeff_kind,
+                                          float(w.penalty_scale), int(getattr(w, "basis", 0)), _i64p(cells),
+                                          len(cells), _dp(x7), _dp(j7), _dp(r))
     if rc != 0:
         raise ValueError("oracle_apply_cells_local: invalid arguments")
     return r

@@ -18,7 +18,9 @@
  *
  * Notation follows PAPER.md §2.1 and §5.2:
  *   n = k+1 basis functions per direction, Lagrange on the n Gauss-Legendre nodes of [0,1]
- *   (BASELINE.json cfg0; reading R8); m quadrature points per direction.
+ *   (BASELINE.json cfg0; reading R8), or on the n Gauss-Lobatto nodes (the *_b entry points, basis 1:
+ *   the non-Gauss basis of SURVEY §8(f2), A^(i) != I at the Gauss points); m quadrature
+ *   points per direction.
  *   Cell T = (i0,i1,i2), canonical id c = (i0 N1 + i1) N2 + i2; local DOF J = j0 + n j1 + n^2 j2
  *   (vec convention, j0 fastest); global DOF g = c n^3 + J (reading R10).
  *   mu_T(xi) = o_T + J_T xi, o_T = (i0/N0, i1/N1, i2/N2) (reading R11).
@@ -30,6 +32,9 @@
  * exactness; Q1 table closed forms; independent Kronecker-sum SIPG matrix (oracle/brute.py,
  * exact polynomial integration) on tiny meshes; symmetry, A.1 = 0, PSD; linear and quadratic
  * consistency (exact special cases); c(x) reduction u = x2; uniform-shear affine consistency.
+ * Gauss-Lobatto basis (tests/test_oracle_lobatto.py): node closed forms + numpy roots of P_{n-1}';
+ * the change of basis r^L(x) = T^T r^G(T x), T_ij = l^L_j(xi^G_i) built with numpy, for every geometry
+ * and coefficient with m = n and m = n + 1.
  */
 #include <math.h>
 #include <stdint.h>
@@ -86,6 +91,47 @@ int oracle_gauss_legendre(int m, double* xi, double* w)
     return 0;
 }
 
+/* -------------------------------------------------------------------------------------- */
+/* n-point Gauss-Lobatto nodes on [0,1] (the non-Gauss basis of SURVEY §8(f2): Lagrange     */
+/* polynomials on these nodes, A = [l_j(xi_q)] != I at the Gauss points):       */
+/* t = -1, the n-2 roots of P_{n-1}'(t), +1; Newton on P_{n-1}' with                         */
+/* (1 - t^2) P_{n-1}'' = 2 t P_{n-1}' - (n-1) n P_{n-1} (Legendre's equation), P_{n-1} and   */
+/* P_{n-1}' from the three-term recurrence and P' = m (t P_m - P_{m-1}) / (t^2 - 1).         */
+/* -------------------------------------------------------------------------------------- */
+static void legendre_pd(int m, double t, double* p, double* dp)
+{
+    double pm1 = 1.0, pm = t;
+    if (m == 0) { *p = 1.0; *dp = 0.0; return; }
+    for (int k = 1; k < m; ++k) {
+        double pn = ((2.0 * k + 1.0) * t * pm - k * pm1) / (k + 1.0);
+        pm1 = pm; pm = pn;
+    }
+    *p = pm;
+    *dp = m * (t * pm - pm1) / (t * t - 1.0);
+}
+
+int oracle_gauss_lobatto(int n, double* xi)
+{
+    if (n < 2 || n > OMAX) return -1;
+    const int m = n - 1; /* interior nodes: roots of P_m' */
+    xi[0] = 0.0;
+    xi[n - 1] = 1.0;
+    for (int i = 1; i < n - 1; ++i) {
+        /* initial guess: Chebyshev-Gauss-Lobatto point, descending in t */
+        double t = cos(PI * i / m);
+        for (int it = 0; it < 100; ++it) {
+            double p, dp;
+            legendre_pd(m, t, &p, &dp);
+            const double d2p = (2.0 * t * dp - m * (m + 1.0) * p) / (1.0 - t * t);
+            const double dt = dp / d2p;
+            t -= dt;
+            if (fabs(dt) < 1e-17) break;
+        }
+        xi[n - 1 - i] = 0.5 * (1.0 + t);
+    }
+    return 0;
+}
+
 /* Lagrange polynomial l_j on nodes[0..n-1] at s (product formula) and its derivative     */
 /* (product rule: l_j'(s) = sum_{a != j} 1/(x_j - x_a) prod_{b != j, a} (s - x_b)/(x_j - x_b)). */
 static void lagrange_1d(int n, const double* nodes, int j, double s, double* val, double* der)
@@ -103,6 +149,26 @@ static void lagrange_1d(int n, const double* nodes, int j, double s, double* val
     }
     *val = v;
     *der = d;
+}
+
+/* Basis nodes: basis 0 the n Gauss-Legendre nodes (reading R8), 1 the n Gauss-Lobatto nodes. */
+static int basis_nodes(int basis, int n, double* xi)
+{
+    double w[OMAX];
+    if (basis == 0) return oracle_gauss_legendre(n, xi, w);
+    if (basis == 1) return oracle_gauss_lobatto(n, xi);
+    return -1;
+}
+
+/* Exported for pins: 1D tables of the basis (n nodes of the given kind) evaluated at arbitrary points. */
+int oracle_basis_1d_b(int n, int basis, int npts, const double* pts, double* val, double* der)
+{
+    double xi[OMAX];
+    if (basis_nodes(basis, n, xi)) return -1;
+    for (int q = 0; q < npts; ++q)
+        for (int j = 0; j < n; ++j)
+            lagrange_1d(n, xi, j, pts[q], &val[q * n + j], &der[q * n + j]);
+    return 0;
 }
 
 /* Exported for pins: 1D tables of the basis (n GL nodes) evaluated at arbitrary points.    */
@@ -154,7 +220,7 @@ typedef struct {
     int N[3];
     int coeff_kind;
     double penalty_scale;
-    double bnodes[OMAX];           /* basis nodes: n-point GL nodes */
+    double bnodes[OMAX];           /* basis nodes: n-point GL nodes (basis 0) or GLL nodes (basis 1) */
     double qx[OMAX], qw[OMAX];     /* quadrature rule, m points */
     /* volume tables at all M = m^3 points for all n^3 basis functions: phi, dphi/dxi_0..2 */
     double* vphi;                  /* [M][n^3][4] */
@@ -190,7 +256,7 @@ static void tangential(int d, int* t1, int* t2)
     else { *t1 = 0; *t2 = 1; }
 }
 
-static int otab_init(otab* T, int N0, int N1, int N2, int k, int m, int coeff_kind, double penalty_scale)
+static int otab_init_b(otab* T, int N0, int N1, int N2, int k, int m, int coeff_kind, double penalty_scale, int basis)
 {
     memset(T, 0, sizeof(*T));
     T->k = k; T->n = k + 1; T->m = m;
@@ -198,8 +264,7 @@ static int otab_init(otab* T, int N0, int N1, int N2, int k, int m, int coeff_ki
     T->coeff_kind = coeff_kind;
     T->penalty_scale = penalty_scale;
     if (T->n > OMAX || m > OMAX || k < 1 || m < 1) return -1;
-    double w[OMAX];
-    if (oracle_gauss_legendre(T->n, T->bnodes, w)) return -1;
+    if (basis_nodes(basis, T->n, T->bnodes)) return -1;
     if (oracle_gauss_legendre(m, T->qx, T->qw)) return -1;
     const int n3 = T->n * T->n * T->n, M = m * m * m;
     T->vphi = (double*)malloc(sizeof(double) * (size_t)M * n3 * 4);
@@ -227,6 +292,11 @@ static int otab_init(otab* T, int N0, int N1, int N2, int k, int m, int coeff_ki
         }
     }
     return 0;
+}
+
+static int otab_init(otab* T, int N0, int N1, int N2, int k, int m, int coeff_kind, double penalty_scale)
+{
+    return otab_init_b(T, N0, N1, N2, k, m, coeff_kind, penalty_scale, 0);
 }
 
 static void otab_free(otab* T)
@@ -555,12 +625,12 @@ static void cell_jac(int geom_kind, const int N[3], const double* jac, int64_t c
  *   cells: list of canonical cell ids to compute (NULL => all cells)
  * Returns 0, or -1 on invalid arguments.
  */
-int oracle_apply(int N0, int N1, int N2, int k, int m, int geom_kind, const double* jac, int coeff_kind,
-                 double penalty_scale, const double* x, double* r, const int64_t* cells, int64_t ncells)
+int oracle_apply_b(int N0, int N1, int N2, int k, int m, int geom_kind, const double* jac, int coeff_kind,
+                   double penalty_scale, int basis, const double* x, double* r, const int64_t* cells, int64_t ncells)
 {
     otab T;
     if (N0 < 1 || N1 < 1 || N2 < 1 || (geom_kind == 1 && !jac)) return -1;
-    if (otab_init(&T, N0, N1, N2, k, m, coeff_kind, penalty_scale)) { otab_free(&T); return -1; }
+    if (otab_init_b(&T, N0, N1, N2, k, m, coeff_kind, penalty_scale, basis)) { otab_free(&T); return -1; }
     const int n = k + 1;
     const int64_t n3 = (int64_t)n * n * n;
     const int64_t total = (int64_t)N0 * N1 * N2;
@@ -592,6 +662,12 @@ int oracle_apply(int N0, int N1, int N2, int k, int m, int geom_kind, const doub
     return 0;
 }
 
+int oracle_apply(int N0, int N1, int N2, int k, int m, int geom_kind, const double* jac, int coeff_kind,
+                 double penalty_scale, const double* x, double* r, const int64_t* cells, int64_t ncells)
+{
+    return oracle_apply_b(N0, N1, N2, k, m, geom_kind, jac, coeff_kind, penalty_scale, 0, x, r, cells, ncells);
+}
+
 /*
  * Cell-local form used for sampled verification of meshes too large to hold on the host:
  *   cells[s]       canonical id of target cell s
@@ -599,12 +675,12 @@ int oracle_apply(int N0, int N1, int N2, int k, int m, int geom_kind, const doub
  *   j7[s][7][9]    matching Jacobians (ignored for geom_kind 0)
  *   r[s][n^3]      output rows
  */
-int oracle_apply_cells_local(int N0, int N1, int N2, int k, int m, int geom_kind, int coeff_kind,
-                             double penalty_scale, const int64_t* cells, int64_t ncells, const double* x7,
-                             const double* j7, double* r)
+int oracle_apply_cells_local_b(int N0, int N1, int N2, int k, int m, int geom_kind, int coeff_kind,
+                               double penalty_scale, int basis, const int64_t* cells, int64_t ncells, const double* x7,
+                               const double* j7, double* r)
 {
     otab T;
-    if (otab_init(&T, N0, N1, N2, k, m, coeff_kind, penalty_scale)) { otab_free(&T); return -1; }
+    if (otab_init_b(&T, N0, N1, N2, k, m, coeff_kind, penalty_scale, basis)) { otab_free(&T); return -1; }
     const int n = k + 1;
     const int64_t n3 = (int64_t)n * n * n;
 #pragma omp parallel for schedule(dynamic, 4)
@@ -624,6 +700,13 @@ int oracle_apply_cells_local(int N0, int N1, int N2, int k, int m, int geom_kind
     }
     otab_free(&T);
     return 0;
+}
+
+int oracle_apply_cells_local(int N0, int N1, int N2, int k, int m, int geom_kind, int coeff_kind,
+                             double penalty_scale, const int64_t* cells, int64_t ncells, const double* x7,
+                             const double* j7, double* r)
+{
+    return oracle_apply_cells_local_b(N0, N1, N2, k, m, geom_kind, coeff_kind, penalty_scale, 0, cells, ncells, x7, j7, r);
 }
 
 int oracle_num_threads(void)

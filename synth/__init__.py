@@ -96,6 +96,8 @@ class Workload:
                                 #    (non-periodic cube, Dirichlet g = |x|^2, K = xx^T + I, c = 10,
                                 #    f = -6; penalty_scale = alpha = 3, gamma = alpha k(k+2) |F|/|T|)
     text: str = ""
+    basis: int = 0              # 0: Lagrange on the n Gauss-Legendre nodes (reading R8); 1: on the n Gauss-Lobatto nodes
+                                #    (the non-Gauss basis of SURVEY §8(f2): A != I even at m = n)
 
     @property
     def n(self) -> int:
@@ -163,12 +165,12 @@ def stokes(k: int, N, seed: int = 17, alpha: float = 3.0) -> Workload:
                     problem=3)
 
 
-def small(k: int, N, geom_kind: int = 0, coeff_kind: int = 0, seed: int = 7, quad: int = -1) -> Workload:
+def small(k: int, N, geom_kind: int = 0, coeff_kind: int = 0, seed: int = 7, quad: int = -1, basis: int = 0) -> Workload:
     """A small ad-hoc workload for tests."""
     if isinstance(N, int):
         N = (N, N, N)
-    return Workload(f"small_k{k}_N{N[0]}x{N[1]}x{N[2]}_g{geom_kind}c{coeff_kind}", k, tuple(N),
-                    geom_kind, coeff_kind, seed=seed, quad=quad)
+    return Workload(f"small_k{k}_N{N[0]}x{N[1]}x{N[2]}_g{geom_kind}c{coeff_kind}" + ("_gll" if basis else ""), k, tuple(N),
+                    geom_kind, coeff_kind, seed=seed, quad=quad, basis=basis)
 
 
 # --------------------------------------------------------------------------- draws
