@@ -295,6 +295,9 @@ def main():
                     help="nlreac: time the Jacobian action J(u0) z (dg_apply_jacobian) instead of the residual")
     ap.add_argument("--k", type=int, default=3)
     ap.add_argument("--N", type=int, default=64)
+    ap.add_argument("--basis", default="gauss", choices=["gauss", "lobatto", "equidistant"],
+                    help="Lagrange basis nodes: gauss (the configs, reading R8) or lobatto (the non-Gauss basis of SURVEY "
+                         "§8(f2): A != I at every rule, k_quad)")
     ap.add_argument("--quad", type=int, default=-1,
                     help="Gauss points per direction (default k+1; k+2 = overintegration, SURVEY §8(f2))")
     args = ap.parse_args()
@@ -314,6 +317,10 @@ def main():
     if args.quad > 0 and args.quad != w.k + 1:
         import dataclasses
         w = dataclasses.replace(w, quad=args.quad, name=f"{w.name}_quad{args.quad}")
+    if args.basis != "gauss":
+        import dataclasses
+        w = dataclasses.replace(w, basis=1 if args.basis == "lobatto" else 2,
+                                name=f"{w.name}_{'gll' if args.basis == 'lobatto' else 'equi'}")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -350,11 +357,11 @@ def main():
         jac = jac_fn(pb - 1, npl + 2) if w.geom_kind else None
         sop = _DistSlab(dg.DistOperator(w.N, w.k, rank, world, uid[0], geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
                                         penalty_scale=w.penalty_scale, jac=jac, device=local_rank, quad=w.m,
-                                        problem=w.problem))
+                                        problem=w.problem, basis=w.basis))
     else:
         sop = slab.SlabOperator(w.N, w.k, rank, world, geom_kind=w.geom_kind, coeff_kind=w.coeff_kind,
                                 penalty_scale=w.penalty_scale, jac_fn=jac_fn, device=local_rank, quad=w.m,
-                                problem=w.problem)
+                                problem=w.problem, basis=w.basis)
     op = sop.op
     x = synth.x_torch(w, start=sop.offset, count=sop.ndofs, device=dev)
     r = torch.empty_like(x)

@@ -67,6 +67,16 @@ extern "C" {
                                  K, g, penalty, restrictions as DG_PROBLEM_DIFFREAC; dg_apply returns the
                                  nonlinear residual R(x), dg_apply_jacobian* the action J(u0) z of its Jacobian */
 
+#define DG_BASIS_GAUSS 0   /* Lagrange basis on the n = k+1 Gauss-Legendre nodes (reading R8; the configs): collocated
+                              with the k+1-point rule, A = I */
+#define DG_BASIS_LOBATTO 1 /* Lagrange basis on the n Gauss-Lobatto nodes (the non-Gauss basis):
+                              A^(i) = [l_j(xi_q)] != I at every Gauss rule, so stage 1 / 3 need the full sum
+                              factorisation (Eq. lowcomplex); DG_PROBLEM_PERIODIC only, any
+                              geometry / coefficient, quad = k+1 .. k+3 (k_quad); DOF j of a line is the value at the
+                              j-th Gauss-Lobatto node */
+#define DG_BASIS_EQUIDISTANT 2 /* Lagrange basis on the n equidistant nodes j / k (SPEC.md's CPU program); as
+                              DG_BASIS_LOBATTO otherwise */
+
 typedef struct dg_ctx dg_ctx;
 
 typedef struct dg_mesh {
@@ -84,6 +94,7 @@ typedef struct dg_mesh {
     int32_t device;        /* CUDA device ordinal */
     void* stream;          /* cudaStream_t on which dg_apply* enqueue work (NULL: legacy default stream) */
     int32_t problem;       /* DG_PROBLEM_PERIODIC (default, 0), _DIFFREAC, _NLREAC or _STOKES */
+    int32_t basis;         /* DG_BASIS_GAUSS (default, 0), DG_BASIS_LOBATTO or DG_BASIS_EQUIDISTANT */
 } dg_mesh;
 
 /* Create a context: 1D tables (Gauss-Legendre nodes/weights, Lagrange derivative matrix D,

@@ -18,8 +18,8 @@
  *
  * Notation follows PAPER.md §2.1 and §5.2:
  *   n = k+1 basis functions per direction, Lagrange on the n Gauss-Legendre nodes of [0,1]
- *   (BASELINE.json cfg0; reading R8), or on the n Gauss-Lobatto nodes (the *_b entry points, basis 1:
- *   the non-Gauss basis of SURVEY §8(f2), A^(i) != I at the Gauss points); m quadrature
+ *   (BASELINE.json cfg0; reading R8), or on the n Gauss-Lobatto nodes / the n equidistant nodes (the *_b entry
+ *   points, basis 1 / 2: the non-Gauss bases of SURVEY §8(f2), A^(i) != I at the Gauss points); m quadrature
  *   points per direction.
  *   Cell T = (i0,i1,i2), canonical id c = (i0 N1 + i1) N2 + i2; local DOF J = j0 + n j1 + n^2 j2
  *   (vec convention, j0 fastest); global DOF g = c n^3 + J (reading R10).
@@ -151,12 +151,18 @@ static void lagrange_1d(int n, const double* nodes, int j, double s, double* val
     *der = d;
 }
 
-/* Basis nodes: basis 0 the n Gauss-Legendre nodes (reading R8), 1 the n Gauss-Lobatto nodes. */
+/* Basis nodes: basis 0 the n Gauss-Legendre nodes (reading R8), 1 the n Gauss-Lobatto nodes, 2 the n equidistant
+ * nodes j / (n - 1) (SPEC.md's CPU program's choice). */
 static int basis_nodes(int basis, int n, double* xi)
 {
     double w[OMAX];
     if (basis == 0) return oracle_gauss_legendre(n, xi, w);
     if (basis == 1) return oracle_gauss_lobatto(n, xi);
+    if (basis == 2) {
+        if (n < 2 || n > OMAX) return -1;
+        for (int j = 0; j < n; ++j) xi[j] = (double)j / (n - 1);
+        return 0;
+    }
     return -1;
 }
 

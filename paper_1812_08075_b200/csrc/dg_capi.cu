@@ -262,7 +262,8 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
     E->Sc[2] = h[0] * h[1] / h[2];
 }
 
-// ---- general quadrature (M = n + MQ Gauss points per direction, MQ = 1 or 2): k_quad
+// ---- general quadrature (M = n + MQ Gauss points per direction, MQ = 1 or 2; MQ = 0 with the Gauss-Lobatto basis;
+//      SURVEY §8(f2)): k_quad
 template <int N, bool AFF, bool COEF, int PR = 0, int MQ = 1>
 cudaError_t launch_quad(const void* qt, const dg::MeshArgs& M, const double* x, const double* xb, const double* xa,
                         double* r, long long c0, long long c1, cudaStream_t st, const double* u0)
@@ -289,6 +290,14 @@ LaunchFn pick_quad_n(bool aff, bool coef, cudaError_t* err, int pr = 0, int mq =
     if (pr == 1) { *err = attr_quad<N, false, false, 1>(); return launch_quad<N, false, false, 1>; }
     if (pr == 2) { *err = attr_quad<N, false, false, 2>(); return launch_quad<N, false, false, 2>; }
     if (pr == 3) { *err = attr_quad<N, false, false, 3>(); return launch_quad<N, false, false, 3>; }
+    if (mq == 0) { // the Gauss-Lobatto basis with m = n Gauss points (A != I)
+        if (aff) {
+            *err = coef ? attr_quad<N, true, true, 0, 0>() : attr_quad<N, true, false, 0, 0>();
+            return coef ? launch_quad<N, true, true, 0, 0> : launch_quad<N, true, false, 0, 0>;
+        }
+        *err = coef ? attr_quad<N, false, true, 0, 0>() : attr_quad<N, false, false, 0, 0>();
+        return coef ? launch_quad<N, false, true, 0, 0> : launch_quad<N, false, false, 0, 0>;
+    }
     if constexpr (N <= 7) {
         if (mq == 2) {
             if (aff) {
@@ -712,6 +721,10 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     if (mesh->problem != DG_PROBLEM_PERIODIC && mesh->problem != DG_PROBLEM_DIFFREAC && mesh->problem != DG_PROBLEM_NLREAC &&
         mesh->problem != DG_PROBLEM_STOKES)
         return fail(DG_ERR_INVALID, "dg_setup: problem=%d", mesh->problem);
+    if (mesh->basis != DG_BASIS_GAUSS && mesh->basis != DG_BASIS_LOBATTO && mesh->basis != DG_BASIS_EQUIDISTANT)
+        return fail(DG_ERR_INVALID, "dg_setup: basis=%d", mesh->basis);
+    if (mesh->basis != DG_BASIS_GAUSS && mesh->problem != DG_PROBLEM_PERIODIC)
+        return fail(DG_ERR_UNSUPPORTED, "dg_setup: the non-Gauss bases are built for DG_PROBLEM_PERIODIC only");
     if (mesh->problem == DG_PROBLEM_STOKES &&
         (mesh->geom_kind != DG_GEOM_AXIS || mesh->coeff_kind != DG_COEFF_ONE || quad != k + 1))
         return fail(DG_ERR_UNSUPPORTED, "dg_setup: the Stokes problem needs DG_GEOM_AXIS, DG_COEFF_ONE and quad = k+1");
@@ -776,7 +789,7 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
     c->launch = pick(n, mesh->geom_kind == DG_GEOM_AFFINE, mesh->coeff_kind == DG_COEFF_SINCOS);
     c->kname = "k_cell_general";
     c->m = quad;
-    c->quad = quad >= k + 2;
+    c->quad = quad >= k + 2 || mesh->basis != DG_BASIS_GAUSS;
     if (c->quad) {
         // overintegration: m = n + 1 or n + 2 Gauss points, interpolation A != I -> k_quad
         dg::HostTables Hm;
@@ -784,11 +797,21 @@ int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out)
             return setup_fail(c, DG_ERR_INVALID, "tables m=%d", quad);
         }
         const int mq = quad - k - 1;
+        // the basis: Gauss-Legendre (collocated only at m = n, which does not come here) or Gauss-Lobatto nodes
+        dg::HostTables Hb;
+        if (mesh->basis == DG_BASIS_LOBATTO) {
+            if (dg::build_tables_lobatto(n, &Hb)) return setup_fail(c, DG_ERR_INVALID, "Gauss-Lobatto tables n=%d", n);
+        } else if (mesh->basis == DG_BASIS_EQUIDISTANT) {
+            if (dg::build_tables_equidistant(n, &Hb)) return setup_fail(c, DG_ERR_INVALID, "equidistant tables n=%d", n);
+        } else {
+            Hb = H;
+        }
         switch (n) {
 #define QTAB_CASE(NN)                                                                                                  \
     case NN:                                                                                                           \
-        if (mq == 2) fill_qtab<NN, (NN <= 7 ? 2 : 1)>(H, Hm, c->qtab);                                                 \
-        else fill_qtab<NN>(H, Hm, c->qtab);                                                                            \
+        if (mq == 2) fill_qtab<NN, (NN <= 7 ? 2 : 1)>(Hb, Hm, c->qtab);                                                \
+        else if (mq == 0) fill_qtab<NN, 0>(Hb, Hm, c->qtab);                                                           \
+        else fill_qtab<NN>(Hb, Hm, c->qtab);                                                                           \
         break;
             QTAB_CASE(2) QTAB_CASE(3) QTAB_CASE(4) QTAB_CASE(5) QTAB_CASE(6) QTAB_CASE(7) QTAB_CASE(8)
 #undef QTAB_CASE

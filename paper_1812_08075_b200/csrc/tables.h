@@ -20,4 +20,11 @@ struct HostTables {
 // Returns 0 on success, -1 if n is out of range.
 int build_tables(int n, HostTables* t);
 
+// The non-Gauss basis of SURVEY §8(f2): Lagrange polynomials on the n Gauss-Lobatto nodes (t = -1, the roots of
+// P_{n-1}', +1 mapped to [0,1]); D at those nodes, e0 / e1 the unit vectors of the end nodes, d0 / d1 rows of D.
+// Interpolated to Gauss points by fill_qtab: A = [l_j(xi_q)] != I even at m = n. n >= 2.
+int build_tables_lobatto(int n, HostTables* t);
+// The same for the n equidistant nodes j / (n - 1) (SPEC.md's CPU program's basis).
+int build_tables_equidistant(int n, HostTables* t);
+
 } // namespace dg

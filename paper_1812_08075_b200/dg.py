@@ -28,6 +28,7 @@ DG_PROBLEM_PERIODIC = 0
 DG_PROBLEM_DIFFREAC = 1
 DG_PROBLEM_NLREAC = 2
 DG_PROBLEM_STOKES = 3
+DG_BASIS_GAUSS, DG_BASIS_LOBATTO, DG_BASIS_EQUIDISTANT = 0, 1, 2
 
 _ERRNAMES = {-1: "DG_ERR_INVALID", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_CUDA", -4: "DG_ERR_NCCL", -5: "DG_ERR_OOM"}
 
@@ -50,6 +51,7 @@ class dg_mesh(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("problem", ctypes.c_int32),
+        ("basis", ctypes.c_int32),
     ]
 
 
@@ -119,15 +121,16 @@ def _ptr(t) -> int:
 # ------------------------------------------------------------------ C-ABI with the same names
 def dg_setup(N, k: int, quad: int, *, plane_begin: int = 0, nplanes: int | None = None, geom_kind: int = 0,
              jac: np.ndarray | None = None, coeff_kind: int = 0, penalty_scale: float = 10.0, device: int = 0,
-             stream: int | None = None, problem: int = 0) -> int:
-    """Returns an opaque context handle (int). jac: host float64 array [(L+2) N1 N2, 9] for affine."""
-    m, _keep = _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem)
+             stream: int | None = None, problem: int = 0, basis: int = 0) -> int:
+    """Returns an opaque context handle (int). jac: host float64 array [(L+2) N1 N2, 9] for affine; basis:
+    DG_BASIS_GAUSS (0) or DG_BASIS_LOBATTO (1)."""
+    m, _keep = _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem, basis)
     h = ctypes.c_void_p()
     _check(load().dg_setup(ctypes.byref(m), k, quad, ctypes.byref(h)))
     return h.value
 
 
-def _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem):
+def _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem, basis=0):
     """dg_mesh for the C-ABI (+ the contiguous jac array it points to, kept alive by the caller)."""
     m = dg_mesh()
     m.N[0], m.N[1], m.N[2] = int(N[0]), int(N[1]), int(N[2])
@@ -146,6 +149,7 @@ def _mesh(N, plane_begin, nplanes, geom_kind, jac, coeff_kind, penalty_scale, de
     m.device = device
     m.stream = stream
     m.problem = problem
+    m.basis = basis
     return m, keep
 
 
@@ -165,10 +169,10 @@ def dg_get_unique_id() -> bytes:
 
 def dg_setup_dist(N, k: int, quad: int, rank: int, nranks: int, nccl_id: bytes, *, geom_kind: int = 0,
                   jac: np.ndarray | None = None, coeff_kind: int = 0, penalty_scale: float = 10.0, device: int = 0,
-                  stream: int | None = None, problem: int = 0) -> int:
+                  stream: int | None = None, problem: int = 0, basis: int = 0) -> int:
     """Collective context for rank `rank` of `nranks` (include/dg.h): jac covers the rank's L+2 planes."""
     pb, npl = dg_slab_range(int(N[0]), rank, nranks)
-    m, _keep = _mesh(N, pb, npl, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem)
+    m, _keep = _mesh(N, pb, npl, geom_kind, jac, coeff_kind, penalty_scale, device, stream, problem, basis)
     if len(nccl_id) != 128:
         raise DgError(DG_ERR_INVALID, "nccl_id must be 128 bytes")
     idbuf = ctypes.create_string_buffer(nccl_id, 128)
@@ -279,7 +283,7 @@ class Operator:
 
     def __init__(self, N, k: int, *, geom_kind: int = 0, coeff_kind: int = 0, penalty_scale: float = 10.0,
                  jac: np.ndarray | None = None, plane_begin: int = 0, nplanes: int | None = None, device: int = 0,
-                 stream=None, quad: int | None = None, problem: int = 0):
+                 stream=None, quad: int | None = None, problem: int = 0, basis: int = 0):
         import torch
         self.N = tuple(int(v) for v in N)
         self.k = k
@@ -289,7 +293,7 @@ class Operator:
         self._stream = stream
         self.ctx = dg_setup(self.N, k, k + 1 if quad is None else quad, plane_begin=plane_begin, nplanes=nplanes,
                             geom_kind=geom_kind, jac=jac, coeff_kind=coeff_kind, penalty_scale=penalty_scale,
-                            device=device, stream=stream.cuda_stream, problem=problem)
+                            device=device, stream=stream.cuda_stream, problem=problem, basis=basis)
         self.ndofs = dg_local_ndofs(self.ctx)
         self.offset = dg_local_offset(self.ctx)
         self.plane_ndofs = dg_plane_ndofs(self.ctx)
@@ -404,7 +408,7 @@ class DistOperator(Operator):
 
     def __init__(self, N, k: int, rank: int, nranks: int, nccl_id: bytes, *, geom_kind: int = 0, coeff_kind: int = 0,
                  penalty_scale: float = 10.0, jac: np.ndarray | None = None, device: int = 0, stream=None,
-                 quad: int | None = None, problem: int = 0):
+                 quad: int | None = None, problem: int = 0, basis: int = 0):
         import torch
         self.N = tuple(int(v) for v in N)
         self.k = k
@@ -415,7 +419,7 @@ class DistOperator(Operator):
         self.rank, self.nranks = rank, nranks
         self.ctx = dg_setup_dist(self.N, k, k + 1 if quad is None else quad, rank, nranks, nccl_id,
                                  geom_kind=geom_kind, jac=jac, coeff_kind=coeff_kind, penalty_scale=penalty_scale,
-                                 device=device, stream=stream.cuda_stream, problem=problem)
+                                 device=device, stream=stream.cuda_stream, problem=problem, basis=basis)
         self.ndofs = dg_local_ndofs(self.ctx)
         self.offset = dg_local_offset(self.ctx)
         self.plane_ndofs = dg_plane_ndofs(self.ctx)

@@ -208,7 +208,8 @@ class SlabOperator:
     """libdg context for one rank's slab + the overlapped halo exchange (GPU, NCCL)."""
 
     def __init__(self, N, k: int, rank: int, world: int, *, geom_kind=0, coeff_kind=0, penalty_scale=10.0,
-                 jac_fn=None, group=None, device=0, quad=None, problem=0, traces: bool = True, staged: bool = False):
+                 jac_fn=None, group=None, device=0, quad=None, problem=0, traces: bool = True, staged: bool = False,
+                 basis: int = 0):
         """jac_fn(plane_begin, nplanes) -> host float64 [(nplanes) N1 N2, 9] (affine only); called for the
         L+2 planes plane_begin-1 .. plane_begin+L."""
         from .dg import Operator
@@ -218,7 +219,7 @@ class SlabOperator:
             jac = jac_fn(self.plan.plane_begin - 1, self.plan.nplanes + 2)
         self.op = Operator(N, k, geom_kind=geom_kind, coeff_kind=coeff_kind, penalty_scale=penalty_scale, jac=jac,
                            plane_begin=self.plan.plane_begin, nplanes=self.plan.nplanes, device=device, quad=quad,
-                           problem=problem)
+                           problem=problem, basis=basis)
         self.ndofs = self.op.ndofs
         self.offset = self.op.offset
         self.plane_ndofs = self.op.plane_ndofs

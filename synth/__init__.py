@@ -96,8 +96,8 @@ class Workload:
                                 #    (non-periodic cube, Dirichlet g = |x|^2, K = xx^T + I, c = 10,
                                 #    f = -6; penalty_scale = alpha = 3, gamma = alpha k(k+2) |F|/|T|)
     text: str = ""
-    basis: int = 0              # 0: Lagrange on the n Gauss-Legendre nodes (reading R8); 1: on the n Gauss-Lobatto nodes
-                                #    (the non-Gauss basis of SURVEY §8(f2): A != I even at m = n)
+    basis: int = 0              # 0: Lagrange on the n Gauss-Legendre nodes (reading R8); 1: on the n Gauss-Lobatto nodes;
+                                #    2: on the n equidistant nodes (the non-Gauss bases of SURVEY §8(f2): A != I at m = n)
 
     @property
     def n(self) -> int:
@@ -169,7 +169,7 @@ def small(k: int, N, geom_kind: int = 0, coeff_kind: int = 0, seed: int = 7, qua
     """A small ad-hoc workload for tests."""
     if isinstance(N, int):
         N = (N, N, N)
-    return Workload(f"small_k{k}_N{N[0]}x{N[1]}x{N[2]}_g{geom_kind}c{coeff_kind}" + ("_gll" if basis else ""), k, tuple(N),
+    return Workload(f"small_k{k}_N{N[0]}x{N[1]}x{N[2]}_g{geom_kind}c{coeff_kind}" + ("", "_gll", "_equi")[basis], k, tuple(N),
                     geom_kind, coeff_kind, seed=seed, quad=quad, basis=basis)
 
 

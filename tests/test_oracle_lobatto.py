@@ -1,4 +1,5 @@
-"""Pins of the oracle's non-Gauss basis (Lagrange polynomials on the n Gauss-Lobatto nodes, so the
+"""Pins of the oracle's non-Gauss bases (Lagrange polynomials on the n Gauss-Lobatto nodes or on the n
+equidistant nodes of SPEC.md's CPU program, so the
 interpolation matrix A^(i) = [l_j(xi_q)] != I even with m = n Gauss points).
 
 * nodes: closed forms (tests/golden/gauss_lobatto.txt) and, for larger n, numpy's roots of P_{n-1}';
@@ -78,16 +79,21 @@ def kron3(T):
     return np.kron(T, np.kron(T, T))
 
 
+def basis_nodes_np(basis, n):
+    return numpy_lobatto(n) if basis == 1 else np.linspace(0.0, 1.0, n)
+
+
 @pytest.mark.parametrize("k", [1, 2, 3, 4])
 @pytest.mark.parametrize("geom,coeff", [(0, 0), (0, 1), (1, 1)])
 @pytest.mark.parametrize("mq", [0, 1])
-def test_change_of_basis(k, geom, coeff, mq):
+@pytest.mark.parametrize("basis", [1, 2])
+def test_change_of_basis(k, geom, coeff, mq, basis):
     n = k + 1
     N = (3, 2, 3)
-    wl = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=70 + k, quad=n + mq, basis=1)
+    wl = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=70 + k, quad=n + mq, basis=basis)
     wg = synth.small(k, N, geom_kind=geom, coeff_kind=coeff, seed=70 + k, quad=n + mq, basis=0)
     gx, _ = np.polynomial.legendre.leggauss(n)
-    T = lagrange_at(numpy_lobatto(n), 0.5 * (gx + 1.0))  # T[i, j] = l^L_j(xi^G_i)
+    T = lagrange_at(basis_nodes_np(basis, n), 0.5 * (gx + 1.0))  # T[i, j] = l^L_j(xi^G_i)
     T3 = kron3(T)
     # kron(T, kron(T, T)) acts on the index j2 n^2 + j1 n + j0 with the FIRST factor on j2: the vec order of a block
     jac = synth.jac_cells_np(wl, np.arange(wl.ncells)) if geom else None
