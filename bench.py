@@ -303,6 +303,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if args.dist_loopback:
+        args.no_e2e = True  # the loopback mode measures the device-side slab step only
 
     import synth
     w = synth.CONFIGS[args.config]
