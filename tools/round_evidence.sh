@@ -18,6 +18,8 @@ timeout 900 python bench.py --config 2 --quad 7 --steps 5 --warmup 3 --no-e2e --
 timeout 900 python bench.py --problem diffreac --k 3 --N 64 --solve --steps 10 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_diffreac_k3_64.json 2> $O/bench_diffreac.err
 timeout 900 python bench.py --problem nlreac --k 3 --N 64 --jacobian --steps 10 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_nljac_k3_64.json 2> $O/bench_nlreac.err
 timeout 900 python bench.py --problem stokes --k 3 --N 48 --steps 10 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_stokes_k3_48.json 2> $O/bench_stokes.err
+timeout 900 python bench.py --config 2 --basis lobatto --steps 10 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_cfg2_gll.json 2> $O/bench_cfg2_gll.err
+for C in 3 4; do timeout 900 python bench.py --config $C --steps 10 --warmup 3 --dist-loopback --no-cpu-baseline > $O/bench_cfg${C}_distloop.json 2> $O/bench_cfg${C}_distloop.err; done
 for C in 3 2 4 1; do
   B="python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
   ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg$C.csv $B > /dev/null 2>&1
