@@ -109,7 +109,8 @@ typedef struct dg_mesh {
  * the caller, release with dg_destroy. Synchronous. Kernel selection is deterministic: k_axis8 for
  * axis-aligned Q7 with c = 1 and N1 % 2 == N2 % 4 == 0; k_line for other axis-aligned c = 1 slabs whose x
  * is at most 32 MB (L2-resident); k_gen when its (i1, i2) tile divides the mesh;
- * k_cell_general otherwise; k_quad / k_stokes for the other problems. A failing kernel attribute
+ * k_cell_general otherwise; k_quad / k_stokes for the other problems, and k_quad for the non-Gauss bases
+ * (DG_BASIS_LOBATTO / DG_BASIS_EQUIDISTANT: A != I at every rule, quad = k+1 .. k+3). A failing kernel attribute
  * call or allocation returns DG_ERR_CUDA / DG_ERR_OOM (no silent switch to another kernel) and
  * releases everything allocated so far. */
 int dg_setup(const dg_mesh* mesh, int k, int quad, dg_ctx** out);
