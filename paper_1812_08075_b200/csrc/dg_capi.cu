@@ -434,43 +434,31 @@ void fill_tab(const dg::HostTables& H, void* out)
 // B^ = D^T W D + 1/2 (e0 d0^T + d0 e0^T - e1 d1^T - d1 e1^T) + P (e0 e0^T + e1 e1^T)  (see kernel_axis8.cuh)
 void build_axis8(const dg::HostTables& H, double P, const double h[3], dg::AxisTab8* A)
 {
+    // K = D^T W D (the volume stiffness of one line) in even/odd halves, symmetrised (the kernel reads the upper
+    // triangle); the face terms of B^ and the neighbour couplings are formed in the kernel from the trace vectors
     const int n = 8, m = 4;
-    double B[8][8];
+    double K[8][8];
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             double s = 0.0;
             for (int q = 0; q < n; ++q) s += H.D[q * n + i] * H.w[q] * H.D[q * n + j];
-            s += 0.5 * (H.e0[i] * H.d0[j] + H.d0[i] * H.e0[j] - H.e1[i] * H.d1[j] - H.d1[i] * H.e1[j]);
-            s += P * (H.e0[i] * H.e0[j] + H.e1[i] * H.e1[j]);
-            B[i][j] = s;
+            K[i][j] = s;
         }
     for (int i = 0; i < m; ++i)
         for (int j = 0; j < m; ++j) {
-            A->Ee[i][j] = 0.5 * (B[i][j] + B[i][n - 1 - j]);
-            A->Oo[i][j] = 0.5 * (B[i][j] - B[i][n - 1 - j]);
+            const double ke = 0.5 * (K[i][j] + K[i][n - 1 - j]), ke_t = 0.5 * (K[j][i] + K[j][n - 1 - i]);
+            const double ko = 0.5 * (K[i][j] - K[i][n - 1 - j]), ko_t = 0.5 * (K[j][i] - K[j][n - 1 - i]);
+            A->Ke[i][j] = 0.5 * (ke + ke_t);
+            A->Ko[i][j] = 0.5 * (ko + ko_t);
         }
-    double aL[8], bL[8], aR[8], bR[8];
-    for (int i = 0; i < n; ++i) {
-        aL[i] = -0.5 * H.d0[i] - P * H.e0[i];
-        bL[i] = 0.5 * H.e0[i];
-        aR[i] = 0.5 * H.d1[i] - P * H.e1[i];
-        bR[i] = -0.5 * H.e1[i];
-    }
     for (int i = 0; i < m; ++i) {
         A->te[i] = 0.5 * (H.e0[i] + H.e0[n - 1 - i]);
         A->to[i] = 0.5 * (H.e0[i] - H.e0[n - 1 - i]);
         A->qe[i] = 0.5 * (H.d0[i] + H.d0[n - 1 - i]);
         A->qo[i] = 0.5 * (H.d0[i] - H.d0[n - 1 - i]);
-        A->aue[i] = 0.5 * (aL[i] + aR[i]);
-        A->age[i] = 0.5 * (bL[i] - bR[i]);
-        A->auo[i] = 0.5 * (aL[i] - aR[i]);
-        A->ago[i] = 0.5 * (bL[i] + bR[i]);
     }
-    for (int i = 0; i < n; ++i) {
-        A->e0[i] = H.e0[i];
-        A->d0[i] = H.d0[i];
-        A->w[i] = H.w[i];
-    }
+    A->P = P;
+    for (int i = 0; i < n; ++i) A->w[i] = H.w[i];
     A->c[0] = h[1] * h[2] / h[0];
     A->c[1] = h[0] * h[2] / h[1];
     A->c[2] = h[0] * h[1] / h[2];

@@ -37,10 +37,13 @@
 namespace dg {
 
 struct AxisTab8 {
-    double Ee[4][4], Oo[4][4];           // even/odd halves of B^ (with the 1/2)
-    double te[4], to[4], qe[4], qo[4];   // e0 and d0 in even/odd form
-    double aue[4], age[4], auo[4], ago[4]; // neighbour-trace coefficients in even/odd form
-    double e0[8], d0[8];
+    // Even/odd halves of the volume stiffness K = D^T W D (symmetric: the kernels read [min(i,j)][max(i,j)]).
+    // The face part of B^ and the neighbour couplings are rank-2 per parity in the trace vectors, so the line
+    // operator needs only K, the trace vectors and P (37 distinct doubles in the hot loop instead of 80: sm_100a
+    // DFMA takes table operands from uniform registers, and 31 doubles fit there; see line_eo):
+    double Ke[4][4], Ko[4][4];
+    double te[4], to[4], qe[4], qo[4];   // e0 and d0 in even/odd form: e0.x = TE + TO, e1.x = TE - TO, ...
+    double P;                            // penalty_scale k (k+1)
     double w[8];
     double c[3];                         // h_t1 h_t2 / h_d
 };
@@ -114,44 +117,56 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-// Even/odd line kernel: given xe, xo (4 each) and neighbour traces, return ye, yo.
-__device__ __forceinline__ void line_eo(const AxisTab8& A, const double xe[4], const double xo[4], double uL, double gL,
-                                        double uR, double gR, double ye[4], double yo[4])
+// Trace sums of a line in even/odd form: TE = te.xe, TO = to.xo, QE = qe.xe, QO = qo.xo, so that
+// e0.x = TE + TO, e1.x = TE - TO, d0.x = QE + QO, d1.x = QO - QE (1-point tables).
+struct Sums {
+    double TE, TO, QE, QO;
+};
+__device__ __forceinline__ Sums sums_eo(const AxisTab8& A, const double xe[4], const double xo[4])
+{
+    Sums t{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        t.TE = fma(A.te[j], xe[j], t.TE);
+        t.TO = fma(A.to[j], xo[j], t.TO);
+        t.QE = fma(A.qe[j], xe[j], t.QE);
+        t.QO = fma(A.qo[j], xo[j], t.QO);
+    }
+    return t;
+}
+__device__ __forceinline__ void split8(const double v[8], double xe[4], double xo[4])
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
+}
+
+// Even/odd line kernel: y = B^ x + a^_L uL + b^_L gL + a^_R uR + b^_R gR in the halves ye (y_i + y_{7-i} parts), yo.
+// With B^ = K + 1/2 (e0 d0^T + d0 e0^T - e1 d1^T - d1 e1^T) + P (e0 e0^T + e1 e1^T) (header) and the couplings
+// a^_L = -d0/2 - P e0, b^_L = e0/2, a^_R = d1/2 - P e1, b^_R = -e1/2, the even half is
+//   ye_i = (Ke xe)_i + te_i (2P TE + QE + dg/2 - P su) + qe_i (TE - su/2)
+// and the odd half
+//   yo_i = (Ko xo)_i + to_i (2P TO + QO + sg/2 - P du) + qo_i (TO - du/2)
+// (su = uL + uR, du = uL - uR, sg = gL + gR, dg = gL - gR): the same FMAs per output as a full B^ table, from
+// the trace sums the caller forms anyway.
+__device__ __forceinline__ void line_eo(const AxisTab8& A, const double xe[4], const double xo[4], const Sums& t,
+                                        double uL, double gL, double uR, double gR, double ye[4], double yo[4])
 {
     const double su = uL + uR, du = uL - uR, sg = gL + gR, dg = gL - gR;
+    const double ae = fma(A.P, fma(2.0, t.TE, -su), fma(0.5, dg, t.QE)), be = fma(-0.5, su, t.TE);
+    const double ao = fma(A.P, fma(2.0, t.TO, -du), fma(0.5, sg, t.QO)), bo = fma(-0.5, du, t.TO);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        double e = fma(A.aue[i], su, A.age[i] * dg);
-        double o = fma(A.auo[i], du, A.ago[i] * sg);
+        double e = fma(A.te[i], ae, A.qe[i] * be);
+        double o = fma(A.to[i], ao, A.qo[i] * bo);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            e = fma(A.Ee[i][j], xe[j], e);
-            o = fma(A.Oo[i][j], xo[j], o);
+            e = fma(A.Ke[i < j ? i : j][i < j ? j : i], xe[j], e);
+            o = fma(A.Ko[i < j ? i : j][i < j ? j : i], xo[j], o);
         }
         ye[i] = e;
         yo[i] = o;
     }
 }
-
-// traces of a line in even/odd form: u0 = e0.x, u1 = e1.x, g0 = d0.x, g1 = d1.x
-__device__ __forceinline__ void traces_eo(const AxisTab8& A, const double xe[4], const double xo[4], double& u0,
-                                          double& u1, double& g0, double& g1)
-{
-    double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        a = fma(A.te[j], xe[j], a);
-        b = fma(A.to[j], xo[j], b);
-        c = fma(A.qe[j], xe[j], c);
-        d = fma(A.qo[j], xo[j], d);
-    }
-    u0 = a + b;
-    u1 = a - b;
-    g0 = c + d;
-    g1 = d - c;
-}
-
-
 
 // In-plane pass (pd = 1: lines along j1 / neighbours along i1; pd = 2: along j2 / i2).
 // TL = tile cells along the pass direction, TW = across. G = threads per tile row (1 or 2).
@@ -202,27 +217,30 @@ __device__ __forceinline__ void inplane_pass(const AxisTab8& A, const MeshArgs& 
         for (int j = 0; j < 8; ++j) rv[k][j] = __ldg(g + eoff(j));
     }
     double xe[CPT][4], xo[CPT][4], u0[CPT], u1[CPT], g0[CPT], g1[CPT];
+    Sums ts[CPT];
 #pragma unroll
     for (int cc = 0; cc < CPT; ++cc) {
         const uint32_t cb = X + bcell(cc) * CELL_BYTES;
         double v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = lds(cb + swz(8 * eoff(j)));
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { xe[cc][j] = v[j] + v[7 - j]; xo[cc][j] = v[j] - v[7 - j]; }
-        traces_eo(A, xe[cc], xo[cc], u0[cc], u1[cc], g0[cc], g1[cc]);
+        split8(v, xe[cc], xo[cc]);
+        ts[cc] = sums_eo(A, xe[cc], xo[cc]);
+        u0[cc] = ts[cc].TE + ts[cc].TO;
+        u1[cc] = ts[cc].TE - ts[cc].TO;
+        g0[cc] = ts[cc].QE + ts[cc].QO;
+        g1[cc] = ts[cc].QO - ts[cc].QE;
     }
-    // ring traces: lower ring cell -> (e1.x, d1.x); upper -> (e0.x, d0.x)
+    // ring traces: lower ring cell -> (e1.x, d1.x); upper -> (e0.x, d0.x) (the same even/odd sums)
     double loU = 0, loG = 0, hiU = 0, hiG = 0;
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
         const bool up = (G == 1) ? (k == 1) : (half == 1);
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            a = fma(up ? A.e0[j] : A.e0[7 - j], rv[k][j], a);
-            b = fma(up ? A.d0[j] : -A.d0[7 - j], rv[k][j], b);
-        }
+        double re[4], ro[4];
+        split8(rv[k], re, ro);
+        const Sums t = sums_eo(A, re, ro);
+        const double a = up ? t.TE + t.TO : t.TE - t.TO;
+        const double b = up ? t.QE + t.QO : t.QO - t.QE;
         if (G == 1) { if (k) { hiU = a; hiG = b; } else { loU = a; loG = b; } }
         else { loU = hiU = a; loG = hiG = b; }
     }
@@ -243,7 +261,7 @@ __device__ __forceinline__ void inplane_pass(const AxisTab8& A, const MeshArgs& 
         else if (G == 2 && !half) { uR = recvU; gR = recvG; }
         else { uR = hiU; gR = hiG; }
         double ye[4], yo[4];
-        line_eo(A, xe[cc], xo[cc], uL, gL, uR, gR, ye, yo);
+        line_eo(A, xe[cc], xo[cc], ts[cc], uL, gL, uR, gR, ye, yo);
         const uint32_t rb = R + bcell(cc) * CELL_BYTES;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -295,23 +313,15 @@ __global__ void k_pack_traces8(const double* __restrict__ x, double* __restrict_
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = __ldg(src + j);
     double* o = (side ? hi : lo) + c * 128;
-    if (side) { // upper end: pass d = 0 carries these from the even/odd traces of the plane's own lines
-        double xe[4], xo[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
-        double u0, u1, g0, g1;
-        ax8::traces_eo(A, xe, xo, u0, u1, g0, g1);
-        o[l] = u1;
-        o[64 + l] = g1;
-    } else {    // lower end: pass d = 0 sums e0.x, d0.x of the next plane's line directly
-        double u = 0.0, g = 0.0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            u = fma(A.e0[j], v[j], u);
-            g = fma(A.d0[j], v[j], g);
-        }
-        o[l] = u;
-        o[64 + l] = g;
+    double xe[4], xo[4];
+    ax8::split8(v, xe, xo);
+    const ax8::Sums ts = ax8::sums_eo(A, xe, xo);
+    if (side) { // upper end (e1.x, d1.x)
+        o[l] = ts.TE - ts.TO;
+        o[64 + l] = ts.QO - ts.QE;
+    } else {    // lower end (e0.x, d0.x)
+        o[l] = ts.TE + ts.TO;
+        o[64 + l] = ts.QE + ts.QO;
     }
 }
 
@@ -421,12 +431,10 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
                 v[2 * k + 1] = t.y;
             }
             double xe[4], xo[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
-            double u0, u1, g0, g1;
-            ax8::traces_eo(A, xe, xo, u0, u1, g0, g1);
-            prevU[q] = u1;
-            prevG[q] = g1;
+            ax8::split8(v, xe, xo);
+            const ax8::Sums ts = ax8::sums_eo(A, xe, xo);
+            prevU[q] = ts.TE - ts.TO;
+            prevG[q] = ts.QO - ts.QE;
         }
     }
 
@@ -485,25 +493,23 @@ k_axis8(const __grid_constant__ CUtensorMap tmx, const double* __restrict__ x, c
                             v[2 * k + 1] = t.y;
                         }
                     }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        uR = fma(A.e0[j], v[j], uR);
-                        gR = fma(A.d0[j], v[j], gR);
-                    }
+                    double ne[4], no[4];
+                    ax8::split8(v, ne, no);
+                    const ax8::Sums tn = ax8::sums_eo(A, ne, no);
+                    uR = tn.TE + tn.TO;
+                    gR = tn.QE + tn.QO;
                 }
                 double v[8];
                 const uint32_t xcb = X + cb * CELL_BYTES;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) lds2(xcb + swz(8 * (8 * L + 2 * k)), v[2 * k], v[2 * k + 1]);
                 double xe[4], xo[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
-                double u0, u1, g0, g1;
-                ax8::traces_eo(A, xe, xo, u0, u1, g0, g1);
+                ax8::split8(v, xe, xo);
+                const ax8::Sums ts = ax8::sums_eo(A, xe, xo);
                 double ye[4], yo[4];
-                ax8::line_eo(A, xe, xo, prevU[q], prevG[q], uR, gR, ye, yo);
-                prevU[q] = u1;
-                prevG[q] = g1;
+                ax8::line_eo(A, xe, xo, ts, prevU[q], prevG[q], uR, gR, ye, yo);
+                prevU[q] = ts.TE - ts.TO;
+                prevG[q] = ts.QO - ts.QE;
                 const uint32_t rb = bufR + cb * CELL_BYTES;
                 double o[8];
 #pragma unroll
