@@ -196,19 +196,12 @@ void fill_eotab(const dg::HostTables& Ht, double P, const double h[3], void* out
         for (int j = 0; j < H; ++j) {
             E->Fm[q][j] = 0.5 * (D(q, j) - D(q, N - 1 - j));
             E->Fp[q][j] = 0.5 * (D(q, j) + D(q, N - 1 - j));
-            E->Tm[q][j] = 0.5 * (D(j, q) - D(N - 1 - j, q));
-            E->Tp[q][j] = 0.5 * (D(j, q) + D(N - 1 - j, q));
         }
         if (N & 1) {
             E->Fp[q][H] = D(q, H);
-            E->Tp[q][H] = D(H, q);
-        }
-        if (N & 1) {
             E->Fmid[q] = D(H, q);
-            E->Tmid[q] = D(q, H);
         } else {
             E->Fmid[q] = 0.0;
-            E->Tmid[q] = 0.0;
         }
     }
     for (int j = 0; j < H; ++j) {

@@ -35,7 +35,7 @@ namespace dg {
 // With xe_j = x_j + x_{n-1-j}, xo_j = x_j - x_{n-1-j} (j < H), xe_H = x_H (odd n):
 //   y = D x      : S_q = sum_{j<H} Fm[q][j] xo_j, A_q = sum_{j<HE} Fp[q][j] xe_j, y_q = S_q + A_q,
 //                  y_{n-1-q} = S_q - A_q (q < H); odd n: y_H = sum_{j<H} Fmid[j] xo_j
-//   y = D^T x    : the same with Tm, Tp, Tmid
+//   y = D^T x    : the same with the transposed halves (tm / tp below)
 //   traces       : u_lo = TE + TO, u_hi = TE - TO, gn_lo = QE + QO, gn_hi = QO - QE with
 //                  TE = sum Es xe, TO = sum Ea xo, QE = sum Ds xe, QO = sum Da xo
 //   face terms of stage 3: S_i += Es_i (Vl + Vh) + Ds_i (Gl - Gh), A_i += Ea_i (Vl - Vh) + Da_i (Gl + Gh)
@@ -43,7 +43,6 @@ template <int N>
 struct EOTab {
     static constexpr int H = N / 2, ODD = N & 1, HE = H + ODD;
     double Fm[H][H], Fp[H][HE], Fmid[H];
-    double Tm[H][H], Tp[H][HE], Tmid[H];
     double Es[HE], Ea[H], Ds[HE], Da[H];
     double D[N * N];   // plain D[q*N + j] (tangential face derivatives)
     double w[N], xi[N];
@@ -82,6 +81,17 @@ __host__ __device__ __forceinline__ void split(const double v[N], double xe[EOTa
     if (N & 1) xe[H] = v[H];
 }
 
+// The halves of D^T are those of D transposed (D centro-antisymmetric: D(n-1-j, q) = -D(j, n-1-q)): Tm[q][j] =
+// Fp[j][q], Tp[q][j] = Fm[j][q] (j < H), Tp[q][H] = Fmid[q], Tmid[j] = Fp[j][H]. The sweeps read D's halves only, so a
+// kernel keeps half the distinct table doubles live (sm_100a DFMA takes table operands from the 63 uniform registers).
+template <int N>
+__host__ __device__ __forceinline__ double tm(const EOTab<N>& E, int q, int j) { return E.Fp[j][q]; }
+template <int N>
+__host__ __device__ __forceinline__ double tp(const EOTab<N>& E, int q, int j)
+{
+    return j < EOTab<N>::H ? E.Fm[j][q] : E.Fmid[q];
+}
+
 // y = D x (TR = false) or y = D^T x (TR = true), plus optional stage-3 face terms at both ends
 template <int N, bool TR, bool FACE>
 __host__ __device__ __forceinline__ void sweep(const EOTab<N>& E, const double xe[EOTab<N>::HE], const double xo[EOTab<N>::H],
@@ -94,16 +104,16 @@ __host__ __device__ __forceinline__ void sweep(const EOTab<N>& E, const double x
         double S = FACE ? fma(E.Es[q], sV, E.Ds[q] * dG) : 0.0;
         double A = FACE ? fma(E.Ea[q], dV, E.Da[q] * sG) : 0.0;
 #pragma unroll
-        for (int j = 0; j < H; ++j) S = fma(TR ? E.Tm[q][j] : E.Fm[q][j], xo[j], S);
+        for (int j = 0; j < H; ++j) S = fma(TR ? tm(E, q, j) : E.Fm[q][j], xo[j], S);
 #pragma unroll
-        for (int j = 0; j < HE; ++j) A = fma(TR ? E.Tp[q][j] : E.Fp[q][j], xe[j], A);
+        for (int j = 0; j < HE; ++j) A = fma(TR ? tp(E, q, j) : E.Fp[q][j], xe[j], A);
         y[q] = S + A;
         y[N - 1 - q] = S - A;
     }
     if (N & 1) {
         double m = FACE ? fma(E.Es[H], sV, E.Ds[H] * dG) : 0.0;
 #pragma unroll
-        for (int j = 0; j < H; ++j) m = fma(TR ? E.Tmid[j] : E.Fmid[j], xo[j], m);
+        for (int j = 0; j < H; ++j) m = fma(TR ? E.Fp[j][H] : E.Fmid[j], xo[j], m);
         y[H] = m;
     }
 }
