@@ -507,7 +507,7 @@ struct dg_ctx {
     double* hx_d;
     double* hr_d;
     cudaStream_t s_h2d, s_d2h, s_cmp;
-    cudaEvent_t ev_in[8], ev_cmp[8]; // created with the streams, destroyed by dg_destroy (no per-call events)
+    cudaEvent_t ev_in[32], ev_cmp[32]; // created with the streams, destroyed by dg_destroy (no per-call events)
     // collective form (dg_setup_dist / dg_apply_dist): library-owned NCCL communicator and halo state
     ncclComm_t comm;
     int rank, nranks;
@@ -996,7 +996,7 @@ int dg_destroy(dg_ctx* c)
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 32; ++i) {
         if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
         if (c->ev_cmp[i]) cudaEventDestroy(c->ev_cmp[i]);
     }
@@ -1213,7 +1213,7 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
     if (!c->s_h2d) CU(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
     if (!c->s_d2h) CU(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
     if (!c->s_cmp) CU(cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking));
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 32; ++i) {
         if (!c->ev_in[i]) CU(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
         if (!c->ev_cmp[i]) CU(cudaEventCreateWithFlags(&c->ev_cmp[i], cudaEventDisableTiming));
     }
@@ -1221,8 +1221,14 @@ int dg_apply_host(dg_ctx* c, const double* xh, double* rh)
     const int64_t pd = c->plane_dofs;
     const size_t pbytes = sizeof(double) * (size_t)pd;
     // chunks of planes; chunk i computes planes [b_i, e_i) once planes [b_i-1, e_i] are resident
-    const int nch = L >= 8 ? 8 : L;
-    int bnd[9];
+    // up to 32 chunks: the transfers of the last chunk (compute of chunk i waits for chunk i+1's first plane, so
+    // about two chunks of D2H trail the last H2D) are 1/16 of the step instead of 1/4 with 8 chunks
+    int nch = L >= 32 ? 32 : L;
+    if (const char* hc = getenv("DG_HOST_CHUNKS")) { // experiments only
+        const int v = atoi(hc);
+        if (v >= 1 && v <= 32) nch = v < L ? v : L;
+    }
+    int bnd[33];
     for (int i = 0; i <= nch; ++i) bnd[i] = (int)((int64_t)L * i / nch);
     cudaEvent_t* ev_in = c->ev_in;
     cudaEvent_t* ev_cmp = c->ev_cmp;
