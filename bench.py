@@ -215,7 +215,7 @@ def run_reference(args, w, rank):
                          **_host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
     return 0
 
 
@@ -267,7 +267,26 @@ def _config(w, ngpu):
 
 
 # ----------------------------------------------------------------------------- main
+_OUT = None  # the original stdout: exactly one JSON line goes there
+
+
+def _emit(line):
+    out = _OUT if _OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _stdout_for_json_only():
+    """Point fd 1 at stderr for the rest of the run (NCCL writes its version / INFO lines to stdout from native
+    code), keeping the original stdout for the one JSON line."""
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
+    _stdout_for_json_only()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -341,8 +360,8 @@ def main():
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        # NCCL's own init lines (transport, rings / channels over NVLink) on stderr: the communicator the halo
-        # exchange uses is visible in the run log
+        # NCCL's own init lines (transport, rings / channels over NVLink) in the run log (stderr: fd 1 points there,
+        # see _stdout_for_json_only): the communicator the halo exchange uses is visible
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,P2P")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
@@ -612,7 +631,7 @@ def main():
     if world > 1:
         dist.barrier()
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        _emit(line)
     sop.close()
     if world > 1:
         dist.destroy_process_group()
