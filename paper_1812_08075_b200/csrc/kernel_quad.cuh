@@ -182,6 +182,11 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         if constexpr (GT == NT) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(GT) : "memory");
     };
+    // first task of this thread in a loop that follows `before` tasks of the same phase (dealt round-robin from
+    // thread 0): the loop starts where the previous one ended, so the threads that got a task more there get one
+    // less here (the phases end at a group barrier: its wait is the phase's most loaded thread). Measured: n = 6
+    // (128-thread groups) 2-6 % faster; n = 4 (64-thread groups, neighbour traces prefetched) 9 % slower: n >= 6 only
+    auto rot = [&](int before) { return N >= 6 ? (gtid - before % GT + GT) % GT : gtid; };
     auto ftp = [&](int c, int f) { return cellp(c) + L::FT + f * 4 * N2; };  // face traces / FB2
     auto f1p = [&](int c, int f) { return cellp(c) + L::F1 + f * 6 * NM; };  // t1 contractions / FB1
     auto cfp = [&](int c, int f) { return cellp(c) + L::C + f * 4 * M2; };   // flux coefficients
@@ -311,6 +316,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // the neighbour values of this thread's trace tasks are loaded before the stage-1a sweeps and consumed
         // after them (L2 latency behind the sweeps; n <= 5, where the registers allow it)
         constexpr bool PREF = N <= 5;
+        // the face-trace tasks follow the stage-1a sweeps (and the Jacobian's u0 sweeps)
+        const int P1_BEFORE = ncell * qd::Sw3<N, N, N, 2, M, false, false>::NL * (PR == 3 ? 2 : 1);
         constexpr int NFT = PREF ? (6 * N2 + GT - 1) / GT : 1;
         double vnb[NFT][N];
         auto nb_of = [&](int c, int f) -> const double* {
@@ -325,7 +332,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         if constexpr (PREF) {
 #pragma unroll
             for (int k = 0; k < NFT; ++k) {
-                const int t = gtid + k * GT;
+                const int t = rot(P1_BEFORE) + k * GT;
                 if (t < ncell * 6 * N2) {
                     const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
                     const bool bnd = DR && cellp(c)[L::GEO + 14 + 16 * f + 15] != 0.0;
@@ -342,11 +349,11 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             S::line2(b + L::X, b + L::Y2, T.A, b + L::Y2d, T.Dq, l); // A2 X and D2 X from one load of the line
         }
         if (PR == 3)
-            for (int t = gtid; t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.A, t % S::NL);
+            for (int t = rot(ncell * S::NL); t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.A, t % S::NL);
         constexpr int NFL = PREF ? NFT : (6 * N2 + GT - 1) / GT;
 #pragma unroll
         for (int k = 0; k < NFL; ++k) {
-            const int t = gtid + k * GT;
+            const int t = rot(P1_BEFORE) + k * GT;
             if (t >= ncell * 6 * N2) break;
             const int c = t / (6 * N2), f = (t / N2) % 6, p = t % N2, a = p % N, bq = p / N;
             const int d = f >> 1, side = f & 1;
@@ -381,9 +388,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             else SA::line(b + L::Y2d, b + L::Zd2, T.A, l);
         }
         if (PR == 3)
-            for (int t = gtid; t < ncell * SA::NL; t += GT) SA::line(u0_T1(t / SA::NL), cellp(t / SA::NL) + L::T2U, T.A, t % SA::NL);
+            for (int t = rot(ncell * 2 * SA::NL); t < ncell * SA::NL; t += GT) SA::line(u0_T1(t / SA::NL), cellp(t / SA::NL) + L::T2U, T.A, t % SA::NL);
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
-        for (int t = gtid; t < ncell * 6 * 6 * F::NL; t += GT) {
+        for (int t = rot(ncell * SA::NL * (PR == 3 ? 3 : 2)); t < ncell * 6 * 6 * F::NL; t += GT) {
             const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
             double* FT = ftp(c, f);
             double* F1 = f1p(c, f);
@@ -410,7 +417,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             }
         }
         if (PR == 3)
-            for (int t = gtid; t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.A, t % SB::NL);
+            for (int t = rot(ncell * 3 * SB::NL); t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.A, t % SB::NL);
         // (the face values at the M^2 points are formed pointwise in P4 from F1: no stored [8][M^2] array)
     }
     gsync();
@@ -454,7 +461,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         b[L::G1 + P] = cW * fma(g[3], a0, fma(g[1], a1, g[5] * a2));
         b[L::G2 + P] = cW * fma(g[4], a0, fma(g[5], a1, g[2] * a2));
     }
-    for (int t = gtid; t < ncell * 6 * M2; t += GT) {
+    for (int t = rot(ncell * M3); t < ncell * 6 * M2; t += GT) {
         const int c = t / (6 * M2), f = (t / M2) % 6, p = t % M2, a = p % M, bq = p / M;
         const int d = f >> 1, side = f & 1;
         const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
@@ -563,7 +570,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // Pv = A^T_t2 Cv + D^T_t2 Ct2, Pt = A^T_t2 Ct1, Pn = A^T_t2 Cn   ([t1 = M][t2 = N])
         using F = qd::Sw2<M, M, 1, N, true, false>;
         using FA = qd::Sw2<M, M, 1, N, true, true>;
-        for (int t = gtid; t < ncell * 6 * 3 * F::NL; t += GT) {
+        for (int t = rot(ncell * 3 * SB::NL); t < ncell * 6 * 3 * F::NL; t += GT) {
             const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
             double* F1 = f1p(c, f);
             const double* C = cfp(c, f);
@@ -586,7 +593,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // V2 = A^T_t1 Pv + D^T_t1 Pt, G2 = A^T_t1 Pn   ([t1 = N][t2 = N], into FT)
         using F = qd::Sw2<M, N, 0, N, true, false>;
         using FA = qd::Sw2<M, N, 0, N, true, true>;
-        for (int t = gtid; t < ncell * 6 * 2 * F::NL; t += GT) {
+        for (int t = rot(ncell * 2 * SA::NL); t < ncell * 6 * 2 * F::NL; t += GT) {
             const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
             double* FT = ftp(c, f);
             const double* P = f1p(c, f);
