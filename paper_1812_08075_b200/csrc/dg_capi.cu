@@ -378,6 +378,25 @@ void fill_stab(const dg::HostTables& H, const dg::HostTables& Hp, void* out)
     }
 }
 
+// even/odd form of an LO x LIN row-major table (kernel_quad.cuh, EOMat); tr: read the table transposed (T[j][q])
+template <int LO, int LIN, int S>
+void fill_eomat(const double* T, bool tr, dg::EOMat<LO, LIN, S>* E)
+{
+    constexpr int HO = LO / 2, HI = LIN / 2;
+    auto t = [&](int q, int j) { return tr ? T[j * LO + q] : T[q * LIN + j]; };
+    for (int q = 0; q < HO; ++q) {
+        for (int j = 0; j < HI; ++j) {
+            E->Pe[q][j] = 0.5 * (t(q, j) + t(q, LIN - 1 - j));
+            E->Po[q][j] = 0.5 * (t(q, j) - t(q, LIN - 1 - j));
+        }
+        if (LIN & 1) E->Pe[q][HI] = t(q, HI);
+    }
+    if (LO & 1) {
+        for (int j = 0; j < HI; ++j) E->Pm[j] = t(HO, j);
+        if (LIN & 1) E->Pm[HI] = S > 0 ? t(HO, HI) : 0.0;
+    }
+}
+
 // interpolation / derivative of the n-node Lagrange basis at the m = n + MQ Gauss points (long double
 // product formulas, no division by (s - x_a): robust when a quadrature point is close to a node)
 template <int N, int MQ = 1>
@@ -407,6 +426,10 @@ void fill_qtab(const dg::HostTables& Hn, const dg::HostTables& Hm, void* out)
         Q->d0[j] = Hn.d0[j];
         Q->d1[j] = Hn.d1[j];
     }
+    fill_eomat(Q->A, false, &Q->eA);
+    fill_eomat(Q->Dq, false, &Q->eD);
+    fill_eomat(Q->A, true, &Q->eAt);
+    fill_eomat(Q->Dq, true, &Q->eDt);
 }
 
 template <int N>

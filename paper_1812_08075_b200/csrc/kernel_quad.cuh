@@ -21,13 +21,66 @@
 
 namespace dg {
 
+// Even/odd form of an LO x LIN table T with T[LO-1-q][LIN-1-j] = S T[q][j] (S = +1: the interpolation A, S = -1:
+// the derivative D; both on symmetric nodes and symmetric Gauss points, and their transposes): with
+// xe_j = x_j + x_{LIN-1-j}, xo_j = x_j - x_{LIN-1-j} (j < LIN/2; xe holds the middle entry of an odd line),
+//   E_q = Pe[q] . xe, O_q = Po[q] . xo, y_q = E_q + O_q, y_{LO-1-q} = S (E_q - O_q)   (q < LO/2),
+//   y_mid = Pm . xe (S = +1) or Pm . xo (S = -1)                                       (odd LO).
+// Half the FMAs of the plain product and half the distinct table doubles (sm_100a DFMA takes table operands from
+// the uniform registers, 31 doubles).
+template <int LO, int LIN, int S>
+struct EOMat {
+    static constexpr int HO = LO / 2, HI = LIN / 2, HEI = HI + (LIN & 1);
+    double Pe[HO][HEI];
+    double Po[HO][HI];
+    double Pm[HEI];
+};
+
 template <int N, int M>
 struct QTab {
     double A[M * N];  // A[q*N + j] = l_j(xi_q) at the M Gauss points (basis: Lagrange on the N Gauss nodes)
     double Dq[M * N]; // l_j'(xi_q)
     double wq[M], xq[M];
     double e0[N], e1[N], d0[N], d1[N];
+    EOMat<M, N, 1> eA;   // A, D and their transposes in even/odd form (the sweeps)
+    EOMat<M, N, -1> eD;
+    EOMat<N, M, 1> eAt;
+    EOMat<N, M, -1> eDt;
 };
+
+template <int LO, int LIN, int S>
+__host__ __device__ __forceinline__ void eo_apply(const EOMat<LO, LIN, S>& T, const double v[LIN], double y[LO])
+{
+    constexpr int HO = LO / 2, HI = LIN / 2, HEI = HI + (LIN & 1);
+    double xe[HEI], xo[HI];
+#pragma unroll
+    for (int j = 0; j < HI; ++j) {
+        xe[j] = v[j] + v[LIN - 1 - j];
+        xo[j] = v[j] - v[LIN - 1 - j];
+    }
+    if (LIN & 1) xe[HI] = v[HI];
+#pragma unroll
+    for (int q = 0; q < HO; ++q) {
+        double e = 0.0, o = 0.0;
+#pragma unroll
+        for (int j = 0; j < HEI; ++j) e = fma(T.Pe[q][j], xe[j], e);
+#pragma unroll
+        for (int j = 0; j < HI; ++j) o = fma(T.Po[q][j], xo[j], o);
+        y[q] = e + o;
+        y[LO - 1 - q] = S > 0 ? e - o : o - e;
+    }
+    if (LO & 1) {
+        double m = 0.0;
+        if (S > 0) {
+#pragma unroll
+            for (int j = 0; j < HEI; ++j) m = fma(T.Pm[j], xe[j], m);
+        } else {
+#pragma unroll
+            for (int j = 0; j < HI; ++j) m = fma(T.Pm[j], xo[j], m);
+        }
+        y[HO] = m;
+    }
+}
 
 namespace qd {
 
@@ -79,6 +132,41 @@ struct Sw3 {
             out2[ob + ost * q] = ACC ? out2[ob + ost * q] + b : b;
         }
     }
+    // the same with tables in even/odd form (EOMat)
+    template <int S>
+    __device__ static void line(const double* in, double* out, const EOMat<LO, LIN, S>& T, int l)
+    {
+        int ib, ist, ob, ost;
+        idx(l, ib, ist, ob, ost);
+        double v[LIN], y[LO];
+#pragma unroll
+        for (int j = 0; j < LIN; ++j) v[j] = in[ib + ist * j];
+        eo_apply(T, v, y);
+#pragma unroll
+        for (int q = 0; q < LO; ++q) out[ob + ost * q] = ACC ? out[ob + ost * q] + y[q] : y[q];
+    }
+    template <int S1, int S2>
+    __device__ static void line2(const double* in, double* out1, const EOMat<LO, LIN, S1>& T1, double* out2,
+                                 const EOMat<LO, LIN, S2>& T2, int l)
+    {
+        int ib, ist, ob, ost;
+        idx(l, ib, ist, ob, ost);
+        double v[LIN], y[LO];
+#pragma unroll
+        for (int j = 0; j < LIN; ++j) v[j] = in[ib + ist * j];
+        eo_apply(T1, v, y);
+#pragma unroll
+        for (int q = 0; q < LO; ++q) out1[ob + ost * q] = ACC ? out1[ob + ost * q] + y[q] : y[q];
+        eo_apply(T2, v, y);
+#pragma unroll
+        for (int q = 0; q < LO; ++q) out2[ob + ost * q] = ACC ? out2[ob + ost * q] + y[q] : y[q];
+    }
+    __device__ static void idx(int l, int& ib, int& ist, int& ob, int& ost)
+    {
+        if (DIM == 0) { ib = E0 * l; ist = 1; ob = O0 * l; ost = 1; }
+        else if (DIM == 1) { const int i0 = l % E0, i2 = l / E0; ib = i0 + E0 * E1 * i2; ist = E0; ob = i0 + O0 * O1 * i2; ost = O0; }
+        else { ib = l; ist = E0 * E1; ob = l; ost = O0 * O1; }
+    }
 };
 
 // the same for a 2D array with extents (E0, E1)
@@ -101,6 +189,18 @@ struct Sw2 {
             for (int j = 0; j < LIN; ++j) a = fma(TRN ? T[j * LO + q] : T[q * LIN + j], v[j], a);
             out[ob + ost * q] = ACC ? out[ob + ost * q] + a : a;
         }
+    }
+    template <int S>
+    __device__ static void line(const double* in, double* out, const EOMat<LO, LIN, S>& T, int l)
+    {
+        const int ib = DIM == 0 ? E0 * l : l, ist = DIM == 0 ? 1 : E0;
+        const int ob = DIM == 0 ? O0 * l : l, ost = DIM == 0 ? 1 : O0;
+        double v[LIN], y[LO];
+#pragma unroll
+        for (int j = 0; j < LIN; ++j) v[j] = in[ib + ist * j];
+        eo_apply(T, v, y);
+#pragma unroll
+        for (int q = 0; q < LO; ++q) out[ob + ost * q] = ACC ? out[ob + ost * q] + y[q] : y[q];
     }
 };
 
@@ -346,10 +446,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = gtid; t < ncell * S::NL; t += GT) {
             const int c = t / S::NL, l = t % S::NL;
             double* b = cellp(c);
-            S::line2(b + L::X, b + L::Y2, T.A, b + L::Y2d, T.Dq, l); // A2 X and D2 X from one load of the line
+            S::line2(b + L::X, b + L::Y2, T.eA, b + L::Y2d, T.eD, l); // A2 X and D2 X from one load of the line
         }
         if (PR == 3)
-            for (int t = rot(ncell * S::NL); t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.A, t % S::NL);
+            for (int t = rot(ncell * S::NL); t < ncell * S::NL; t += GT) S::line(cellp(t / S::NL) + L::R, u0_T1(t / S::NL), T.eA, t % S::NL);
         constexpr int NFL = PREF ? NFT : (6 * N2 + GT - 1) / GT;
 #pragma unroll
         for (int k = 0; k < NFL; ++k) {
@@ -384,11 +484,11 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = gtid; t < ncell * 2 * SA::NL; t += GT) {
             const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
             double* b = cellp(c);
-            if (k == 0) SA::line2(b + L::Y2, b + L::Z, T.A, b + L::Zd1, T.Dq, l); // A1 (A2 X), D1 (A2 X)
-            else SA::line(b + L::Y2d, b + L::Zd2, T.A, l);
+            if (k == 0) SA::line2(b + L::Y2, b + L::Z, T.eA, b + L::Zd1, T.eD, l); // A1 (A2 X), D1 (A2 X)
+            else SA::line(b + L::Y2d, b + L::Zd2, T.eA, l);
         }
         if (PR == 3)
-            for (int t = rot(ncell * 2 * SA::NL); t < ncell * SA::NL; t += GT) SA::line(u0_T1(t / SA::NL), cellp(t / SA::NL) + L::T2U, T.A, t % SA::NL);
+            for (int t = rot(ncell * 2 * SA::NL); t < ncell * SA::NL; t += GT) SA::line(u0_T1(t / SA::NL), cellp(t / SA::NL) + L::T2U, T.eA, t % SA::NL);
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
         for (int t = rot(ncell * SA::NL * (PR == 3 ? 3 : 2)); t < ncell * 6 * 6 * F::NL; t += GT) {
             const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
@@ -396,8 +496,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             double* F1 = f1p(c, f);
             // k: 0 own Ua1 = A u, 1 own Ud1 = D u, 2 own Ga1 = A g, 3..5 the same for the neighbour
             const double* src = FT + ((k < 3) ? (k == 2 ? N2 : 0) : (k == 5 ? 3 * N2 : 2 * N2));
-            if (k % 3 == 1) F::line(src, F1 + k * NM, T.Dq, l);
-            else F::line(src, F1 + k * NM, T.A, l);
+            if (k % 3 == 1) F::line(src, F1 + k * NM, T.eD, l);
+            else F::line(src, F1 + k * NM, T.eA, l);
         }
     }
     gsync();
@@ -410,14 +510,14 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
             if (k == 0) {
-                if (DR) SB::line2(b + L::Z, b + L::G0, T.Dq, b + L::GU, T.A, l);
-                else SB::line(b + L::Z, b + L::G0, T.Dq, l);
+                if (DR) SB::line2(b + L::Z, b + L::G0, T.eD, b + L::GU, T.eA, l);
+                else SB::line(b + L::Z, b + L::G0, T.eD, l);
             } else {
-                SB::line(b + (k == 1 ? L::Zd1 : L::Zd2), b + (k == 1 ? L::G1 : L::G2), T.A, l);
+                SB::line(b + (k == 1 ? L::Zd1 : L::Zd2), b + (k == 1 ? L::G1 : L::G2), T.eA, l);
             }
         }
         if (PR == 3)
-            for (int t = rot(ncell * 3 * SB::NL); t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.A, t % SB::NL);
+            for (int t = rot(ncell * 3 * SB::NL); t < ncell * SB::NL; t += GT) SB::line(cellp(t / SB::NL) + L::T2U, cellp(t / SB::NL) + L::U0Q, T.eA, t % SB::NL);
         // (the face values at the M^2 points are formed pointwise in P4 from F1: no stored [8][M^2] array)
     }
     gsync();
@@ -561,11 +661,11 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
             double* b = cellp(c);
             if (k == 0) {
-                SB::line(b + L::G0, b + L::Z, T.Dq, l); // V
-                if (DR) qd::Sw3<M, M, M, 0, N, true, true>::line(b + L::GU, b + L::Z, T.A, l); // + A0^T (c u - f)
+                SB::line(b + L::G0, b + L::Z, T.eDt, l); // V
+                if (DR) qd::Sw3<M, M, M, 0, N, true, true>::line(b + L::GU, b + L::Z, T.eAt, l); // + A0^T (c u - f)
             }
-            else if (k == 1) SB::line(b + L::G1, b + L::Zd1, T.A, l); // W1
-            else SB::line(b + L::G2, b + L::Zd2, T.A, l);             // W2
+            else if (k == 1) SB::line(b + L::G1, b + L::Zd1, T.eAt, l); // W1
+            else SB::line(b + L::G2, b + L::Zd2, T.eAt, l);             // W2
         }
         // Pv = A^T_t2 Cv + D^T_t2 Ct2, Pt = A^T_t2 Ct1, Pn = A^T_t2 Cn   ([t1 = M][t2 = N])
         using F = qd::Sw2<M, M, 1, N, true, false>;
@@ -574,9 +674,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
             double* F1 = f1p(c, f);
             const double* C = cfp(c, f);
-            if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, T.A, l); FA::line(C + 2 * M2, F1 + 0 * NM, T.Dq, l); }
-            else if (k == 1) F::line(C + 1 * M2, F1 + 1 * NM, T.A, l);
-            else F::line(C + 3 * M2, F1 + 2 * NM, T.A, l);
+            if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, T.eAt, l); FA::line(C + 2 * M2, F1 + 0 * NM, T.eDt, l); }
+            else if (k == 1) F::line(C + 1 * M2, F1 + 1 * NM, T.eAt, l);
+            else F::line(C + 3 * M2, F1 + 2 * NM, T.eAt, l);
         }
     }
     gsync();
@@ -587,8 +687,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = gtid; t < ncell * 2 * SA::NL; t += GT) {
             const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
             double* b = cellp(c);
-            if (k == 0) { SA::line(b + L::Z, b + L::Y2, T.A, l); SAa::line(b + L::Zd1, b + L::Y2, T.Dq, l); } // Ya
-            else SA::line(b + L::Zd2, b + L::Y2d, T.A, l);                                                   // Yb
+            if (k == 0) { SA::line(b + L::Z, b + L::Y2, T.eAt, l); SAa::line(b + L::Zd1, b + L::Y2, T.eDt, l); } // Ya
+            else SA::line(b + L::Zd2, b + L::Y2d, T.eAt, l);                                                   // Yb
         }
         // V2 = A^T_t1 Pv + D^T_t1 Pt, G2 = A^T_t1 Pn   ([t1 = N][t2 = N], into FT)
         using F = qd::Sw2<M, N, 0, N, true, false>;
@@ -597,8 +697,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
             double* FT = ftp(c, f);
             const double* P = f1p(c, f);
-            if (k == 0) { F::line(P + 0 * NM, FT, T.A, l); FA::line(P + 1 * NM, FT, T.Dq, l); }
-            else F::line(P + 2 * NM, FT + N2, T.A, l);
+            if (k == 0) { F::line(P + 0 * NM, FT, T.eAt, l); FA::line(P + 1 * NM, FT, T.eDt, l); }
+            else F::line(P + 2 * NM, FT + N2, T.eAt, l);
         }
     }
     gsync();
@@ -609,8 +709,8 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         for (int t = gtid; t < ncell * S::NL; t += GT) {
             const int c = t / S::NL, l = t % S::NL;
             double* b = cellp(c);
-            S::line(b + L::Y2, b + L::R, T.A, l);
-            Sa::line(b + L::Y2d, b + L::R, T.Dq, l);
+            S::line(b + L::Y2, b + L::R, T.eAt, l);
+            Sa::line(b + L::Y2d, b + L::R, T.eDt, l);
         }
     }
     gsync();
