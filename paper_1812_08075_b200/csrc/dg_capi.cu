@@ -351,6 +351,25 @@ LaunchFn pick_stokes(int n, cudaError_t* err)
 }
 // velocity tables (collocated: D at the n Gauss points) and the pressure basis (n-1 Gauss nodes) at the
 // velocity nodes (long double product formulas, as fill_qtab)
+// even/odd form of an LO x LIN row-major table (kernel_quad.cuh, EOMat); tr: read the table transposed (T[j][q])
+template <int LO, int LIN, int S>
+void fill_eomat(const double* T, bool tr, dg::EOMat<LO, LIN, S>* E)
+{
+    constexpr int HO = LO / 2, HI = LIN / 2;
+    auto t = [&](int q, int j) { return tr ? T[j * LO + q] : T[q * LIN + j]; };
+    for (int q = 0; q < HO; ++q) {
+        for (int j = 0; j < HI; ++j) {
+            E->Pe[q][j] = 0.5 * (t(q, j) + t(q, LIN - 1 - j));
+            E->Po[q][j] = 0.5 * (t(q, j) - t(q, LIN - 1 - j));
+        }
+        if (LIN & 1) E->Pe[q][HI] = t(q, HI);
+    }
+    if (LO & 1) {
+        for (int j = 0; j < HI; ++j) E->Pm[j] = t(HO, j);
+        if (LIN & 1) E->Pm[HI] = S > 0 ? t(HO, HI) : 0.0;
+    }
+}
+
 template <int N>
 void fill_stab(const dg::HostTables& H, const dg::HostTables& Hp, void* out)
 {
@@ -376,25 +395,10 @@ void fill_stab(const dg::HostTables& H, const dg::HostTables& Hp, void* out)
         S->ep0[j] = Hp.e0[j];
         S->ep1[j] = Hp.e1[j];
     }
-}
-
-// even/odd form of an LO x LIN row-major table (kernel_quad.cuh, EOMat); tr: read the table transposed (T[j][q])
-template <int LO, int LIN, int S>
-void fill_eomat(const double* T, bool tr, dg::EOMat<LO, LIN, S>* E)
-{
-    constexpr int HO = LO / 2, HI = LIN / 2;
-    auto t = [&](int q, int j) { return tr ? T[j * LO + q] : T[q * LIN + j]; };
-    for (int q = 0; q < HO; ++q) {
-        for (int j = 0; j < HI; ++j) {
-            E->Pe[q][j] = 0.5 * (t(q, j) + t(q, LIN - 1 - j));
-            E->Po[q][j] = 0.5 * (t(q, j) - t(q, LIN - 1 - j));
-        }
-        if (LIN & 1) E->Pe[q][HI] = t(q, HI);
-    }
-    if (LO & 1) {
-        for (int j = 0; j < HI; ++j) E->Pm[j] = t(HO, j);
-        if (LIN & 1) E->Pm[HI] = S > 0 ? t(HO, HI) : 0.0;
-    }
+    fill_eomat(S->D, false, &S->eD);
+    fill_eomat(S->D, true, &S->eDt);
+    fill_eomat(S->AP, false, &S->eAP);
+    fill_eomat(S->AP, true, &S->eAPt);
 }
 
 // interpolation / derivative of the n-node Lagrange basis at the m = n + MQ Gauss points (long double

@@ -18,6 +18,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernel_quad.cuh" // qd::Sw3 / Sw2, EOMat
 #include "kernel_quad.cuh"
 
 namespace dg {
@@ -30,6 +31,10 @@ struct STab {
     double w[N], xi[N];
     double e0[N], e1[N], d0[N], d1[N];
     double ep0[NP], ep1[NP];
+    EOMat<N, N, -1> eD;    // D, D^T, AP, AP^T in even/odd form (kernel_quad.cuh, EOMat): the sweeps
+    EOMat<N, N, -1> eDt;
+    EOMat<N, NP, 1> eAP;
+    EOMat<NP, N, 1> eAPt;
 };
 
 namespace sk {
@@ -135,21 +140,21 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
             const int c = ce / 3, e = ce % 3;
             const double* in = U + c * N3;
             double* out = G + ce * N3;
-            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.D, l);
-            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.D, l);
-            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.D, l);
+            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.eD, l);
+            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.eD, l);
+            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.eD, l);
         }
     } else {
         for (int t = tid; t < 9 * N2; t += NT) {
             const int ce = t / N2, l = t % N2, c = ce / 3, e = ce % 3;
             const double* in = U + c * N3;
             double* out = G + ce * N3;
-            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.D, l);
-            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.D, l);
-            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.D, l);
+            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.eD, l);
+            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.eD, l);
+            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.eD, l);
         }
     }
-    for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, NP, 2, N, false, false>::line(PR, TA, T.AP, t);
+    for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, NP, 2, N, false, false>::line(PR, TA, T.eAP, t);
     constexpr int NFL = PREF ? NFT : (18 * N2 + NT - 1) / NT;
 #pragma unroll
     for (int k = 0; k < NFL; ++k) {
@@ -197,19 +202,19 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     }
     __syncthreads();
     // ---------------- P2: pressure A_p along j1; face pressure A_p along t1 ----------------
-    for (int t = tid; t < NP * N; t += NT) qd::Sw3<NP, NP, N, 1, N, false, false>::line(TA, TB, T.AP, t);
+    for (int t = tid; t < NP * N; t += NT) qd::Sw3<NP, NP, N, 1, N, false, false>::line(TA, TB, T.eAP, t);
     for (int t = tid; t < 12 * NP; t += NT) {
         const int f = t / (2 * NP), s = (t / NP) % 2, l = t % NP;
         double* Fb = face(f);
-        qd::Sw2<NP, NP, 0, N, false, false>::line(Fb + L::PT + s * NP2, Fb + L::PF1 + s * N * NP, T.AP, l);
+        qd::Sw2<NP, NP, 0, N, false, false>::line(Fb + L::PT + s * NP2, Fb + L::PF1 + s * N * NP, T.eAP, l);
     }
     __syncthreads();
     // ---------------- P3: pressure A_p along j0 (p at the N^3 points); face pressure along t2 ----------------
-    for (int t = tid; t < N2; t += NT) qd::Sw3<NP, N, N, 0, N, false, false>::line(TB, PQ, T.AP, t);
+    for (int t = tid; t < N2; t += NT) qd::Sw3<NP, N, N, 0, N, false, false>::line(TB, PQ, T.eAP, t);
     for (int t = tid; t < 12 * N; t += NT) {
         const int f = t / (2 * N), s = (t / N) % 2, l = t % N;
         double* Fb = face(f);
-        qd::Sw2<N, NP, 1, N, false, false>::line(Fb + L::PF1 + s * N * NP, Fb + L::PF2 + s * N2, T.AP, l);
+        qd::Sw2<N, NP, 1, N, false, false>::line(Fb + L::PF1 + s * N * NP, Fb + L::PF2 + s * N2, T.eAP, l);
     }
     __syncthreads();
     // ---------------- P4: pointwise volume terms; face fluxes ----------------
@@ -293,31 +298,31 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     // ---------------- P5: stage 3 (D^T per direction into RU, A_p^T for the pressure), face A_p^T ----------------
     for (int t = tid; t < 3 * N2; t += NT) {
         const int c = t / N2, l = t % N2;
-        qd::Sw3<N, N, N, 0, N, true, false>::line(G + (3 * c) * N3, U + c * N3, T.D, l);
+        qd::Sw3<N, N, N, 0, N, true, false>::line(G + (3 * c) * N3, U + c * N3, T.eDt, l);
     }
-    for (int t = tid; t < N2; t += NT) qd::Sw3<N, N, N, 0, NP, true, false>::line(PQ, TB, T.AP, t);
+    for (int t = tid; t < N2; t += NT) qd::Sw3<N, N, N, 0, NP, true, false>::line(PQ, TB, T.eAPt, t);
     for (int t = tid; t < 6 * N; t += NT) {
         const int f = t / N, l = t % N;
         double* Fb = face(f);
-        qd::Sw2<N, N, 1, NP, true, false>::line(Fb + L::PF2, Fb + L::PF1, T.AP, l);
+        qd::Sw2<N, N, 1, NP, true, false>::line(Fb + L::PF2, Fb + L::PF1, T.eAPt, l);
     }
     __syncthreads();
     for (int t = tid; t < 3 * N2; t += NT) {
         const int c = t / N2, l = t % N2;
-        qd::Sw3<N, N, N, 1, N, true, true>::line(G + (3 * c + 1) * N3, U + c * N3, T.D, l);
+        qd::Sw3<N, N, N, 1, N, true, true>::line(G + (3 * c + 1) * N3, U + c * N3, T.eDt, l);
     }
-    for (int t = tid; t < NP * N; t += NT) qd::Sw3<NP, N, N, 1, NP, true, false>::line(TB, TA, T.AP, t);
+    for (int t = tid; t < NP * N; t += NT) qd::Sw3<NP, N, N, 1, NP, true, false>::line(TB, TA, T.eAPt, t);
     for (int t = tid; t < 6 * NP; t += NT) {
         const int f = t / NP, l = t % NP;
         double* Fb = face(f);
-        qd::Sw2<N, NP, 0, NP, true, false>::line(Fb + L::PF1, Fb + L::PT, T.AP, l);
+        qd::Sw2<N, NP, 0, NP, true, false>::line(Fb + L::PF1, Fb + L::PT, T.eAPt, l);
     }
     __syncthreads();
     for (int t = tid; t < 3 * N2; t += NT) {
         const int c = t / N2, l = t % N2;
-        qd::Sw3<N, N, N, 2, N, true, true>::line(G + (3 * c + 2) * N3, U + c * N3, T.D, l);
+        qd::Sw3<N, N, N, 2, N, true, true>::line(G + (3 * c + 2) * N3, U + c * N3, T.eDt, l);
     }
-    for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, N, 2, NP, true, false>::line(TA, PR, T.AP, t);
+    for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, N, 2, NP, true, false>::line(TA, PR, T.eAPt, t);
     __syncthreads();
     // ---------------- P6: add the face back-projections along the normals, write the block once ----------------
     for (int i = tid; i < B; i += NT) {
