@@ -31,8 +31,8 @@ namespace dg {
 template <int LO, int LIN, int S>
 struct EOMat {
     static constexpr int HO = LO / 2, HI = LIN / 2, HEI = HI + (LIN & 1);
-    double Pe[HO][HEI];
-    double Po[HO][HI];
+    double Pe[HO > 0 ? HO : 1][HEI];
+    double Po[HO > 0 ? HO : 1][HI > 0 ? HI : 1];
     double Pm[HEI];
 };
 
@@ -52,7 +52,7 @@ template <int LO, int LIN, int S>
 __host__ __device__ __forceinline__ void eo_apply(const EOMat<LO, LIN, S>& T, const double v[LIN], double y[LO])
 {
     constexpr int HO = LO / 2, HI = LIN / 2, HEI = HI + (LIN & 1);
-    double xe[HEI], xo[HI];
+    double xe[HEI], xo[HI > 0 ? HI : 1];
 #pragma unroll
     for (int j = 0; j < HI; ++j) {
         xe[j] = v[j] + v[LIN - 1 - j];
