@@ -231,6 +231,14 @@ int dg_bench_fp64(int device, int iters, double* tflops, double* ms);
  * computed in the even/odd (centro-(anti)symmetric) form the kernels use. k in [1,7]. */
 int dg_line_ops(int k, double penalty_scale, const double* x, const double* nb, double* out);
 
+/* The same for k_axis8's line operator (k = 7, n = 8; host build of kernel_axis8.cuh's algebra with the tables
+ * dg_setup gives that kernel): B^ applied from the volume stiffness K = D^T W D and rank-2 trace
+ * terms. For one line x[8] and nb = (a, b, c, d) writes out[12]:
+ *   out[0, 8)   B^ x + aL a + bL b + aR c + bR d   (same B^, aL, bL, aR, bR as dg_line_ops, P = penalty_scale 56)
+ *   out[8, 12)  e0.x, d0.x, e1.x, d1.x
+ * Host pointers, caller-owned; returns DG_ERR_INVALID for NULL arguments. */
+int dg_line_ops_axis8(double penalty_scale, const double* x, const double* nb, double* out);
+
 /* Thread-local description of the last error ("" if none). */
 const char* dg_last_error(void);
 

@@ -1070,6 +1070,30 @@ int dg_line_ops(int k, double penalty_scale, const double* x, const double* nb, 
     }
 }
 
+int dg_line_ops_axis8(double penalty_scale, const double* x, const double* nb, double* out)
+{
+    if (!x || !nb || !out) return fail(DG_ERR_INVALID, "dg_line_ops_axis8: NULL argument");
+    dg::HostTables H;
+    if (dg::build_tables(8, &H)) return fail(DG_ERR_INVALID, "tables n=8");
+    const double h[3] = {1.0, 1.0, 1.0};
+    dg::AxisTab8 A;
+    build_axis8(H, penalty_scale * 7 * 8, h, &A);
+    double v[8], xe[4], xo[4], ye[4], yo[4];
+    for (int j = 0; j < 8; ++j) v[j] = x[j];
+    dg::ax8::split8(v, xe, xo);
+    const dg::ax8::Sums t = dg::ax8::sums_eo(A, xe, xo);
+    dg::ax8::line_eo(A, xe, xo, t, nb[0], nb[1], nb[2], nb[3], ye, yo);
+    for (int i = 0; i < 4; ++i) {
+        out[i] = ye[i] + yo[i];
+        out[7 - i] = ye[i] - yo[i];
+    }
+    out[8] = t.TE + t.TO;
+    out[9] = t.QE + t.QO;
+    out[10] = t.TE - t.TO;
+    out[11] = t.QO - t.QE;
+    return DG_OK;
+}
+
 double dg_alg_flops(const dg_ctx* c)
 {
     // collocated sum factorisation, each face once, multiply-add = 2 flops.

@@ -122,7 +122,7 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
 struct Sums {
     double TE, TO, QE, QO;
 };
-__device__ __forceinline__ Sums sums_eo(const AxisTab8& A, const double xe[4], const double xo[4])
+__host__ __device__ __forceinline__ Sums sums_eo(const AxisTab8& A, const double xe[4], const double xo[4])
 {
     Sums t{0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -134,7 +134,7 @@ __device__ __forceinline__ Sums sums_eo(const AxisTab8& A, const double xe[4], c
     }
     return t;
 }
-__device__ __forceinline__ void split8(const double v[8], double xe[4], double xo[4])
+__host__ __device__ __forceinline__ void split8(const double v[8], double xe[4], double xo[4])
 {
 #pragma unroll
     for (int j = 0; j < 4; ++j) { xe[j] = v[j] + v[7 - j]; xo[j] = v[j] - v[7 - j]; }
@@ -148,7 +148,7 @@ __device__ __forceinline__ void split8(const double v[8], double xe[4], double x
 //   yo_i = (Ko xo)_i + to_i (2P TO + QO + sg/2 - P du) + qo_i (TO - du/2)
 // (su = uL + uR, du = uL - uR, sg = gL + gR, dg = gL - gR): the same FMAs per output as a full B^ table, from
 // the trace sums the caller forms anyway.
-__device__ __forceinline__ void line_eo(const AxisTab8& A, const double xe[4], const double xo[4], const Sums& t,
+__host__ __device__ __forceinline__ void line_eo(const AxisTab8& A, const double xe[4], const double xo[4], const Sums& t,
                                         double uL, double gL, double uR, double gR, double ye[4], double yo[4])
 {
     const double su = uL + uR, du = uL - uR, sg = gL + gR, dg = gL - gR;

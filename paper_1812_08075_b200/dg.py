@@ -57,7 +57,7 @@ class dg_mesh(ctypes.Structure):
 
 EXPORTS = ["dg_setup", "dg_apply", "dg_apply_planes", "dg_apply_host", "dg_destroy", "dg_set_stream",
            "dg_local_ndofs", "dg_local_offset", "dg_plane_ndofs", "dg_alg_flops", "dg_alg_bytes",
-           "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops",
+           "dg_launches_per_apply", "dg_kernel_name", "dg_last_error", "dg_bench_fp64", "dg_line_ops", "dg_line_ops_axis8",
            "dg_apply_jacobian", "dg_apply_jacobian_planes", "dg_halo_ndofs", "dg_pack_halo", "dg_apply_planes_tr", "dg_slab_range", "dg_get_unique_id",
            "dg_setup_dist", "dg_apply_dist"]
 
@@ -102,6 +102,7 @@ def load(path: str = LIB_PATH):
     L.dg_last_error.restype = ctypes.c_char_p
     L.dg_bench_fp64.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp]
     L.dg_line_ops.argtypes = [ctypes.c_int, ctypes.c_double, vp, vp, vp]
+    L.dg_line_ops_axis8.argtypes = [ctypes.c_double, vp, vp, vp]
     _lib = L
     return L
 
@@ -270,6 +271,17 @@ def dg_line_ops(k: int, penalty_scale: float, x, nb) -> np.ndarray:
     assert x.shape == (n,) and nb.shape == (4,)
     out = np.empty(3 * n + 4)
     _check(load().dg_line_ops(k, float(penalty_scale), x.ctypes.data, nb.ctypes.data, out.ctypes.data))
+    return out
+
+
+def dg_line_ops_axis8(penalty_scale: float, x, nb) -> np.ndarray:
+    """k_axis8's line operator on the host (include/dg.h): [B^ x + neighbour terms | e0.x, d0.x, e1.x, d1.x] for
+    one line x of 8 values (k = 7) and nb = 4 values."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    nb = np.ascontiguousarray(nb, dtype=np.float64)
+    assert x.shape == (8,) and nb.shape == (4,)
+    out = np.empty(12)
+    _check(load().dg_line_ops_axis8(float(penalty_scale), x.ctypes.data, nb.ctypes.data, out.ctypes.data))
     return out
 
 

@@ -67,3 +67,25 @@ def test_line_ops_exact_on_polynomials(k):
     one = dg.dg_line_ops(k, 10.0, np.ones(n), np.zeros(4))[2 * n:3 * n]
     xi_, w, D, e0, e1, d0, d1 = ref_tables(n)
     np.testing.assert_allclose(one, 10.0 * k * (k + 1) * (e0 + e1) + 0.5 * (d0 - d1), rtol=1e-10, atol=1e-10)
+
+
+@pytest.mark.parametrize("penalty", [10.0, 3.0, 0.0])
+def test_axis8_line_operator_matches_plain_tables(penalty):
+    """k_axis8's line operator (built from the volume stiffness K = D^T W D and rank-2 trace terms)
+    equals the full B^ and neighbour couplings assembled here from the numpy tables."""
+    from paper_1812_08075_b200 import dg
+    k, n = 7, 8
+    xi, w, D, e0, e1, d0, d1 = ref_tables(n)
+    Pn = penalty * k * (k + 1)
+    B = D.T @ np.diag(w) @ D + 0.5 * (np.outer(e0, d0) + np.outer(d0, e0) - np.outer(e1, d1) - np.outer(d1, e1)) \
+        + Pn * (np.outer(e0, e0) + np.outer(e1, e1))
+    aL, bL, aR, bR = -0.5 * d0 - Pn * e0, 0.5 * e0, 0.5 * d1 - Pn * e1, -0.5 * e1
+    rng = np.random.default_rng(77)
+    for _ in range(8):
+        x = rng.uniform(-1, 1, n)
+        nb = rng.uniform(-1, 1, 4)
+        out = dg.dg_line_ops_axis8(penalty, x, nb)
+        ref = B @ x + aL * nb[0] + bL * nb[1] + aR * nb[2] + bR * nb[3]
+        np.testing.assert_allclose(out[:n], ref, rtol=0, atol=1e-12 * np.abs(B).max() * n)
+        scale = np.abs(D).max() * n
+        np.testing.assert_allclose(out[n:], [e0 @ x, d0 @ x, e1 @ x, d1 @ x], rtol=0, atol=1e-12 * scale)
