@@ -491,7 +491,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             for (int t = rot(ncell * 2 * SA::NL); t < ncell * SA::NL; t += GT) SA::line(u0_T1(t / SA::NL), cellp(t / SA::NL) + L::T2U, T.eA, t % SA::NL);
         using F = qd::Sw2<N, N, 0, M, false, false>; // [t1][t2]: N x N -> M x N
         for (int t = rot(ncell * SA::NL * (PR == 3 ? 3 : 2)); t < ncell * 6 * 6 * F::NL; t += GT) {
-            const int c = t / (36 * F::NL), f = (t / (6 * F::NL)) % 6, k = (t / F::NL) % 6, l = t % F::NL;
+            // kind-major task order (the A-table kinds 0, 2, 3, 5, then the D-table kinds 1, 4): the lanes of a warp
+            // run one sweep body instead of interleaving the kinds every F::NL lanes
+            const int c = t / (36 * F::NL), kk = (t / (6 * F::NL)) % 6, f = (t / F::NL) % 6, l = t % F::NL;
+            const int k = kk == 0 ? 0 : (kk == 1 ? 2 : (kk == 2 ? 3 : (kk == 3 ? 5 : (kk == 4 ? 1 : 4))));
             double* FT = ftp(c, f);
             double* F1 = f1p(c, f);
             // k: 0 own Ua1 = A u, 1 own Ud1 = D u, 2 own Ga1 = A g, 3..5 the same for the neighbour
@@ -671,7 +674,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         using F = qd::Sw2<M, M, 1, N, true, false>;
         using FA = qd::Sw2<M, M, 1, N, true, true>;
         for (int t = rot(ncell * 3 * SB::NL); t < ncell * 6 * 3 * F::NL; t += GT) {
-            const int c = t / (18 * F::NL), f = (t / (3 * F::NL)) % 6, k = (t / F::NL) % 3, l = t % F::NL;
+            const int c = t / (18 * F::NL), k = (t / (6 * F::NL)) % 3, f = (t / F::NL) % 6, l = t % F::NL; // kind-major
             double* F1 = f1p(c, f);
             const double* C = cfp(c, f);
             if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, T.eAt, l); FA::line(C + 2 * M2, F1 + 0 * NM, T.eDt, l); }
@@ -694,7 +697,7 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         using F = qd::Sw2<M, N, 0, N, true, false>;
         using FA = qd::Sw2<M, N, 0, N, true, true>;
         for (int t = rot(ncell * 2 * SA::NL); t < ncell * 6 * 2 * F::NL; t += GT) {
-            const int c = t / (12 * F::NL), f = (t / (2 * F::NL)) % 6, k = (t / F::NL) % 2, l = t % F::NL;
+            const int c = t / (12 * F::NL), k = (t / (6 * F::NL)) % 2, f = (t / F::NL) % 6, l = t % F::NL; // kind-major
             double* FT = ftp(c, f);
             const double* P = f1p(c, f);
             if (k == 0) { F::line(P + 0 * NM, FT, T.eAt, l); FA::line(P + 1 * NM, FT, T.eDt, l); }
