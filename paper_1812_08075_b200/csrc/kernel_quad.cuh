@@ -287,6 +287,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     // less here (the phases end at a group barrier: its wait is the phase's most loaded thread). Measured: n = 6
     // (128-thread groups) 2-6 % faster; n = 4 (64-thread groups, neighbour traces prefetched) 9 % slower: n >= 6 only
     auto rot = [&](int before) { return N >= 6 ? (gtid - before % GT + GT) % GT : gtid; };
+    // n < 6 (64-thread groups): the task kinds of a stage loop start on warp boundaries (each kind's range padded to
+    // a multiple of 32), so a warp runs one sweep body; n >= 6 keeps the dense ranges the rot() balance assumes
+    constexpr auto kpad = [](int nl) { return N < 6 ? (nl + 31) / 32 * 32 : nl; };
     auto ftp = [&](int c, int f) { return cellp(c) + L::FT + f * 4 * N2; };  // face traces / FB2
     auto f1p = [&](int c, int f) { return cellp(c) + L::F1 + f * 6 * NM; };  // t1 contractions / FB1
     auto cfp = [&](int c, int f) { return cellp(c) + L::C + f * 4 * M2; };   // flux coefficients
@@ -481,8 +484,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     // ---------------- P2: stage 1b (along j1); face contraction along t1 ----------------
     {
         using SA = qd::Sw3<N, N, M, 1, M, false, false>;
-        for (int t = gtid; t < ncell * 2 * SA::NL; t += GT) {
-            const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
+        constexpr int NLp = kpad(SA::NL);
+        for (int t = gtid; t < ncell * 2 * NLp; t += GT) {
+            const int c = t / (2 * NLp), k = (t / NLp) % 2, l = t % NLp;
+            if (l >= SA::NL) continue;
             double* b = cellp(c);
             if (k == 0) SA::line2(b + L::Y2, b + L::Z, T.eA, b + L::Zd1, T.eD, l); // A1 (A2 X), D1 (A2 X)
             else SA::line(b + L::Y2d, b + L::Zd2, T.eA, l);
@@ -509,8 +514,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         using SB = qd::Sw3<N, M, M, 0, M, false, false>;
         // (k = 0: Z -> G0 with D0 and, for the diffusion-reaction problems, Z -> GU = u with A0 from the same
         // line; k = 1, 2: the A0 sweeps of Zd1, Zd2 — one sweep body per task kind)
-        for (int t = gtid; t < ncell * 3 * SB::NL; t += GT) {
-            const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
+        constexpr int NLp = kpad(SB::NL);
+        for (int t = gtid; t < ncell * 3 * NLp; t += GT) {
+            const int c = t / (3 * NLp), k = (t / NLp) % 3, l = t % NLp;
+            if (l >= SB::NL) continue;
             double* b = cellp(c);
             if (k == 0) {
                 if (DR) SB::line2(b + L::Z, b + L::G0, T.eD, b + L::GU, T.eA, l);
@@ -660,8 +667,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     // ---------------- P5: stage 3a (D0^T / A0^T along j0); face back-projection along t2 ----------------
     {
         using SB = qd::Sw3<M, M, M, 0, N, true, false>; // M^3 -> N x M x M
-        for (int t = gtid; t < ncell * 3 * SB::NL; t += GT) {
-            const int c = t / (3 * SB::NL), k = (t / SB::NL) % 3, l = t % SB::NL;
+        constexpr int NLp = kpad(SB::NL);
+        for (int t = gtid; t < ncell * 3 * NLp; t += GT) {
+            const int c = t / (3 * NLp), k = (t / NLp) % 3, l = t % NLp;
+            if (l >= SB::NL) continue;
             double* b = cellp(c);
             if (k == 0) {
                 SB::line(b + L::G0, b + L::Z, T.eDt, l); // V
@@ -687,8 +696,10 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
     {
         using SA = qd::Sw3<N, M, M, 1, N, true, false>;  // N x M x M -> N x N x M
         using SAa = qd::Sw3<N, M, M, 1, N, true, true>;
-        for (int t = gtid; t < ncell * 2 * SA::NL; t += GT) {
-            const int c = t / (2 * SA::NL), k = (t / SA::NL) % 2, l = t % SA::NL;
+        constexpr int NLp = kpad(SA::NL);
+        for (int t = gtid; t < ncell * 2 * NLp; t += GT) {
+            const int c = t / (2 * NLp), k = (t / NLp) % 2, l = t % NLp;
+            if (l >= SA::NL) continue;
             double* b = cellp(c);
             if (k == 0) { SA::line(b + L::Z, b + L::Y2, T.eAt, l); SAa::line(b + L::Zd1, b + L::Y2, T.eDt, l); } // Ya
             else SA::line(b + L::Zd2, b + L::Y2d, T.eAt, l);                                                   // Yb
