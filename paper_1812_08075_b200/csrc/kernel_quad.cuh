@@ -682,8 +682,13 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // Pv = A^T_t2 Cv + D^T_t2 Ct2, Pt = A^T_t2 Ct1, Pn = A^T_t2 Cn   ([t1 = M][t2 = N])
         using F = qd::Sw2<M, M, 1, N, true, false>;
         using FA = qd::Sw2<M, M, 1, N, true, true>;
-        for (int t = rot(ncell * 3 * SB::NL); t < ncell * 6 * 3 * F::NL; t += GT) {
-            const int c = t / (18 * F::NL), k = (t / (6 * F::NL)) % 3, f = (t / F::NL) % 6, l = t % F::NL; // kind-major
+        // kind-major (the two-sweep kind 0 first, padded to a warp boundary for n < 6; a group holds one cell)
+        constexpr int K0 = 6 * F::NL, K0p = kpad(K0);
+        for (int t = rot(ncell * 3 * SB::NL); t < ncell * (K0p + 2 * K0); t += GT) {
+            int k, q;
+            if (t < K0p) { if (t >= K0) continue; k = 0; q = t; }
+            else { k = 1 + (t - K0p) / K0; q = (t - K0p) % K0; }
+            const int c = 0, f = q / F::NL, l = q % F::NL;
             double* F1 = f1p(c, f);
             const double* C = cfp(c, f);
             if (k == 0) { F::line(C + 0 * M2, F1 + 0 * NM, T.eAt, l); FA::line(C + 2 * M2, F1 + 0 * NM, T.eDt, l); }
@@ -707,8 +712,12 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
         // V2 = A^T_t1 Pv + D^T_t1 Pt, G2 = A^T_t1 Pn   ([t1 = N][t2 = N], into FT)
         using F = qd::Sw2<M, N, 0, N, true, false>;
         using FA = qd::Sw2<M, N, 0, N, true, true>;
-        for (int t = rot(ncell * 2 * SA::NL); t < ncell * 6 * 2 * F::NL; t += GT) {
-            const int c = t / (12 * F::NL), k = (t / (6 * F::NL)) % 2, f = (t / F::NL) % 6, l = t % F::NL; // kind-major
+        constexpr int K0 = 6 * F::NL, K0p = kpad(K0);
+        for (int t = rot(ncell * 2 * SA::NL); t < ncell * (K0p + K0); t += GT) {
+            int k, q;
+            if (t < K0p) { if (t >= K0) continue; k = 0; q = t; }
+            else { k = 1; q = t - K0p; }
+            const int c = 0, f = q / F::NL, l = q % F::NL;
             double* FT = ftp(c, f);
             const double* P = f1p(c, f);
             if (k == 0) { F::line(P + 0 * NM, FT, T.eAt, l); FA::line(P + 1 * NM, FT, T.eDt, l); }
