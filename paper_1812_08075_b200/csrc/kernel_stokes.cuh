@@ -93,6 +93,29 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     double* const TA = sm + L::TA;
     double* const TB = sm + L::TB;
     auto face = [&](int f) { return sm + L::F + f * L::FACE; };
+    // the small tables indexed by run-time point indices, in shared memory: a constant-bank load with lane-varying
+    // addresses is serialised over the distinct addresses of a warp
+    __shared__ double sTab[6 * N + 2 * NP];
+    double* const sE0 = sTab;
+    double* const sE1 = sTab + N;
+    double* const sD0 = sTab + 2 * N;
+    double* const sD1 = sTab + 3 * N;
+    double* const sW = sTab + 4 * N;
+    double* const sXi = sTab + 5 * N;
+    double* const sEp0 = sTab + 6 * N;
+    double* const sEp1 = sTab + 6 * N + NP;
+    for (int i = tid; i < N; i += NT) {
+        sE0[i] = T.e0[i];
+        sE1[i] = T.e1[i];
+        sD0[i] = T.d0[i];
+        sD1[i] = T.d1[i];
+        sW[i] = T.w[i];
+        sXi[i] = T.xi[i];
+        if (i < NP) {
+            sEp0[i] = T.ep0[i];
+            sEp1[i] = T.ep1[i];
+        }
+    }
     // neighbour block across face f = 2d + side, or nullptr on the boundary of the cube
     auto nbp = [&](int f) -> const double* {
         const int d = f >> 1, side = f & 1;
@@ -222,7 +245,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     auto hsel = [&](int e) { return e == 0 ? h0 : (e == 1 ? h1 : h2); };
     for (int P = tid; P < N3; P += NT) {
         const int q0 = P % N, q1 = (P / N) % N, q2 = P / N2;
-        const double W = T.w[q0] * T.w[q1] * T.w[q2] * h0 * h1 * h2;
+        const double W = sW[q0] * sW[q1] * sW[q2] * h0 * h1 * h2;
         const double p = PQ[P];
         double div = 0.0;
 #pragma unroll
@@ -247,7 +270,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         double* Fb = face(f);
         double* TR = Fb + L::TR;
         const bool bnd = on_bnd(d, side);
-        const double W = T.w[a] * T.w[bq] * hsel(t1) * hsel(t2);
+        const double W = sW[a] * sW[bq] * hsel(t1) * hsel(t2);
         const double hd = hsel(d);
         const double gam = d == 0 ? Ms.gamma[0] : (d == 1 ? Ms.gamma[1] : Ms.gamma[2]);
         double Cv[3], Cn[3], Cq;
@@ -257,7 +280,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         } else if (bnd) {
             // Dirichlet face: [u] -> u - g, one-sided flux, outer normal sn e_d
             const double sn = side ? 1.0 : -1.0;
-            const double xi1 = d == 1 ? (double)side : (t1 == 1 ? T.xi[a] : T.xi[bq]);
+            const double xi1 = d == 1 ? (double)side : (t1 == 1 ? sXi[a] : sXi[bq]);
             const double X1 = (ig1 + xi1) * h1;
             const double po = Fb[L::PF2 + p];
             double jd = 0.0;
@@ -337,7 +360,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
                     const double* TR = face(2 * d + side) + L::TR + c * 4 * N2;
-                    const double e = side ? T.e1[j[d]] : T.e0[j[d]], dd = side ? T.d1[j[d]] : T.d0[j[d]];
+                    const double e = side ? sE1[j[d]] : sE0[j[d]], dd = side ? sD1[j[d]] : sD0[j[d]];
                     v = fma(e, TR[p], fma(dd, TR[N2 + p], v));
                 }
             }
@@ -350,7 +373,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
                 const int p = j[t1] + NP * j[t2];
 #pragma unroll
                 for (int side = 0; side < 2; ++side) {
-                    const double e = side ? T.ep1[j[d]] : T.ep0[j[d]];
+                    const double e = side ? sEp1[j[d]] : sEp0[j[d]];
                     v = fma(e, face(2 * d + side)[L::PT + p], v);
                 }
             }
