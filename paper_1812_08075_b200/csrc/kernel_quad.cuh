@@ -549,11 +549,13 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             int lp_, rem_, ig_[3];
             coords(c, lp_, rem_, ig_);
             const double x0 = (ig_[0] + sxq[q0]) * h0, x1 = (ig_[1] + sxq[q1]) * h1, x2 = (ig_[2] + sxq[q2]) * h2;
-            const double p0 = a0 / h0, p1 = a1 / h1, p2 = a2 / h2; // physical gradient
+            // (1/h by multiplication: a double division is a ~20-instruction sequence with a slow-path branch)
+            const double ih0 = 1.0 / h0, ih1 = 1.0 / h1, ih2 = 1.0 / h2; // (loop-invariant: hoisted)
+            const double p0 = a0 * ih0, p1 = a1 * ih1, p2 = a2 * ih2; // physical gradient
             const double xg = x0 * p0 + x1 * p1 + x2 * p2;        // K grad u = x (x . grad u) + grad u
-            b[L::G0 + P] = W * fma(x0, xg, p0) / h0;
-            b[L::G1 + P] = W * fma(x1, xg, p1) / h1;
-            b[L::G2 + P] = W * fma(x2, xg, p2) / h2;
+            b[L::G0 + P] = W * fma(x0, xg, p0) * ih0;
+            b[L::G1 + P] = W * fma(x1, xg, p1) * ih1;
+            b[L::G2 + P] = W * fma(x2, xg, p2) * ih2;
             const double uq = b[L::GU + P];
             double react;
             if (PR == 1) {
@@ -616,7 +618,9 @@ k_quad(const double* __restrict__ x, const double* __restrict__ xb, const double
             const double Xt1 = d == 0 ? X1 : X0, Xt2 = d == 2 ? X1 : X2;
             const double hd = Ms.h[d], ht1 = Ms.h[t1], ht2 = Ms.h[t2];
             // (K e)_d for e = d, t1, t2 (K symmetric), scaled to reference derivatives (1/h_e)
-            const double kd = (Xd * Xd + 1.0) / hd, kt1 = Xd * Xt1 / ht1, kt2 = Xd * Xt2 / ht2;
+            const double ih0 = 1.0 / Ms.h[0], ih1 = 1.0 / Ms.h[1], ih2 = 1.0 / Ms.h[2]; // (loop-invariant: hoisted)
+            const double ihd = d == 0 ? ih0 : (d == 1 ? ih1 : ih2), iht1 = t1 == 0 ? ih0 : ih1, iht2 = t2 == 1 ? ih1 : ih2;
+            const double kd = (Xd * Xd + 1.0) * ihd, kt1 = Xd * Xt1 * iht1, kt2 = Xd * Xt2 * iht2;
             const double W = sw[a] * sw[bq] * ht1 * ht2;
             const double gam = Ms.gamma[d];
             const double Kgo = kd * Gno + kt1 * T1o + kt2 * T2o; // (K grad u)_d of the own side

@@ -243,6 +243,9 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     // ---------------- P4: pointwise volume terms; face fluxes ----------------
     const double h0 = Ms.h[0], h1 = Ms.h[1], h2 = Ms.h[2];
     auto hsel = [&](int e) { return e == 0 ? h0 : (e == 1 ? h1 : h2); };
+    // 1/h by multiplication (a double division is a ~20-instruction sequence with a slow-path branch)
+    const double ih0 = 1.0 / h0, ih1 = 1.0 / h1, ih2 = 1.0 / h2;
+    auto ihsel = [&](int e) { return e == 0 ? ih0 : (e == 1 ? ih1 : ih2); };
     for (int P = tid; P < N3; P += NT) {
         const int q0 = P % N, q1 = (P / N) % N, q2 = P / N2;
         const double W = sW[q0] * sW[q1] * sW[q2] * h0 * h1 * h2;
@@ -253,12 +256,12 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
 #pragma unroll
             for (int e = 0; e < 3; ++e) {
                 double* g = G + (3 * c + e) * N3 + P;
-                const double he = e == 0 ? h0 : (e == 1 ? h1 : h2);
-                const double ge = *g / he;             // physical d u_c / d x_e
+                const double ihe = e == 0 ? ih0 : (e == 1 ? ih1 : ih2);
+                const double ge = *g * ihe;            // physical d u_c / d x_e
                 if (c == e) div += ge;
                 double q = W * ge;                     // (grad u_c, grad v): . d v / d x_e
                 if (c == e) q -= W * p;                // -(p, div v)
-                *g = q / he;                           // coefficient of the reference derivative
+                *g = q * ihe;                          // coefficient of the reference derivative
             }
         }
         PQ[P] = -W * div;                              // -(div u, q)
@@ -271,7 +274,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         double* TR = Fb + L::TR;
         const bool bnd = on_bnd(d, side);
         const double W = sW[a] * sW[bq] * hsel(t1) * hsel(t2);
-        const double hd = hsel(d);
+        const double ihd = ihsel(d);
         const double gam = d == 0 ? Ms.gamma[0] : (d == 1 ? Ms.gamma[1] : Ms.gamma[2]);
         double Cv[3], Cn[3], Cq;
         if (bnd && d == 0 && side == 1) {
@@ -288,9 +291,9 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
             for (int c = 0; c < 3; ++c) {
                 const double g = c == 0 ? 4.0 * X1 * (1.0 - X1) : 0.0;
                 const double jmp = TR[c * 4 * N2 + p] - g;
-                const double dun = sn * TR[c * 4 * N2 + N2 + p] / hd;
+                const double dun = sn * TR[c * 4 * N2 + N2 + p] * ihd;
                 Cv[c] = W * (-dun + gam * jmp + (c == d ? sn * po : 0.0));
-                Cn[c] = -W * jmp * sn / hd;            // theta (u - g, grad v . n), theta = -1
+                Cn[c] = -W * jmp * sn * ihd;           // theta (u - g, grad v . n), theta = -1
                 if (c == d) jd = jmp;
             }
             Cq = W * sn * jd;                          // ((u - g) . n, q)
@@ -303,9 +306,9 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
                 const double uo = TR[c * 4 * N2 + p], go = TR[c * 4 * N2 + N2 + p];
                 const double un = TR[c * 4 * N2 + 2 * N2 + p], gn = TR[c * 4 * N2 + 3 * N2 + p];
                 const double jump = side ? uo - un : un - uo;
-                const double avg = 0.5 * (go + gn) / hd;
+                const double avg = 0.5 * (go + gn) * ihd;
                 Cv[c] = sv * W * (-avg + gam * jump + (c == d ? pavg : 0.0));
-                Cn[c] = -0.5 * W * jump / hd;          // theta ([u], {grad v} n)
+                Cn[c] = -0.5 * W * jump * ihd;         // theta ([u], {grad v} n)
                 if (c == d) jd = jump;
             }
             Cq = 0.5 * W * jd;                         // ([u] . n, {q})
