@@ -514,6 +514,8 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
     // ---------------- face passes (face f with normal DC, point p = (a, b)) ----------------
     // the T- record slot of face f: own upper faces 3c + d -> c, tile-boundary faces 3 NC + r -> NC + r
     auto face_rec = [&](int f) { return f < 3 * NC ? f / 3 : NC + (f - 3 * NC); };
+    // 1/h_d once (axis-aligned faces: no double division per face point)
+    const double ihx0 = 1.0 / M.h[0], ihx1 = 1.0 / M.h[1], ihx2 = 1.0 / M.h[2];
     // a-, a+ components (normal d, tangential t1, t2) and dS of face f from its T- record (16-B pairs)
     struct FaceA {
         double mdn, mt1, mt2, pdn, pt1, pt2, dS;
@@ -534,7 +536,7 @@ k_gen(const double* __restrict__ x, const double* __restrict__ xb, const double*
             A.pdn = r2.y;
             A.dS = r3.x;
         } else {
-            A.mdn = A.pdn = 1.0 / M.h[d];
+            A.mdn = A.pdn = d == 0 ? ihx0 : (d == 1 ? ihx1 : ihx2);
             A.mt1 = A.mt2 = A.pt1 = A.pt2 = 0.0;
             A.dS = M.h[(d + 1) % 3] * M.h[(d + 2) % 3];
         }
