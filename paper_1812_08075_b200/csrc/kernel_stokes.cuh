@@ -46,11 +46,16 @@ struct SLay {
     // n <= 3: one round of the 9 n^2 gradient lines (measured: k = 2 1.52 -> 1.26 ms); n = 4, 5: 128 (k = 4:
     // 1.24 -> 1.11 ms on 40^3); else 256
     static constexpr int NT = N <= 3 ? (9 * N * N + 31) / 32 * 32 : (N <= 5 ? 128 : 256);
+    // velocity / gradient blocks: point (j0, j1, j2) at j0 + N j1 + PS j2. n = 4: PS = 20, so that the 16 lines of a
+    // j1-sweep (lanes (j0, j2), stride 4 along the line) fall on 16 distinct banks (dense: 4-way conflicts); the
+    // j2-sweeps stay conflict-free
+    static constexpr int PS = N == 4 ? 20 : N2;
+    static constexpr int NB = N * PS;
     // per-cell shared buffers (doubles)
-    static constexpr int U = 0;            // velocity (3 N3), later the velocity residual RU
-    static constexpr int PR = U + 3 * N3;  // pressure (NP3), later the pressure residual RP
-    static constexpr int G = PR + NP3;     // 9 reference gradients [c][e] (N3 each), later the fluxes Q[c][e]
-    static constexpr int PQ = G + 9 * N3;  // p at the points, later -W div u
+    static constexpr int U = 0;            // velocity (3 blocks of NB), later the velocity residual RU
+    static constexpr int PR = U + 3 * NB;  // pressure (NP3), later the pressure residual RP
+    static constexpr int G = PR + NP3;     // 9 reference gradients [c][e] (NB each), later the fluxes Q[c][e]
+    static constexpr int PQ = G + 9 * NB;  // p at the points (dense N3), later -W div u
     static constexpr int TA = PQ + N3;     // [NP][NP][N]
     static constexpr int TB = TA + NP2 * N; // [NP][N][N]
     // per face: TR [3][4][N2] (own u, own du/dn_hat, nb u, nb du/dn_hat) -> coefficients Cv = TR[c][0],
@@ -62,6 +67,28 @@ struct SLay {
     static constexpr int END = F + 6 * FACE;
     static constexpr int BYTES = END * 8;
 };
+// 1D sweep along DIM of a velocity / gradient block with plane stride PS (the line numbering of qd::Sw3 for an
+// N^3 cube), tables in even/odd form
+template <int N, int PS, int DIM, bool ACC>
+struct SwC {
+    template <int S>
+    __device__ static void line(const double* in, double* out, const EOMat<N, N, S>& T, int l)
+    {
+        int ib, ist;
+        if (DIM == 0) { const int i1 = l % N, i2 = l / N; ib = N * i1 + PS * i2; ist = 1; }
+        else if (DIM == 1) { const int i0 = l % N, i2 = l / N; ib = i0 + PS * i2; ist = N; }
+        else { const int i0 = l % N, i1 = l / N; ib = i0 + N * i1; ist = PS; }
+        double v[N], y[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = in[ib + ist * j];
+        eo_apply(T, v, y);
+#pragma unroll
+        for (int q = 0; q < N; ++q) out[ib + ist * q] = ACC ? out[ib + ist * q] + y[q] : y[q];
+    }
+};
+// padded index of the dense point P = j0 + N j1 + N^2 j2
+template <int N, int PS>
+__device__ __forceinline__ int pad_pt(int P) { return P + (PS - N * N) * (P / (N * N)); }
 } // namespace sk
 
 // grid: one CTA per cell of [c_begin, c_end) (local canonical order), block SLay::NT, dynamic smem
@@ -131,7 +158,11 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     };
 
     // ---------------- P0: stage the cell's block (velocity + pressure, contiguous in both) ----------------
-    for (int i = tid; i < B; i += NT) U[i] = __ldg(x + lc * B + i);
+    for (int i = tid; i < B; i += NT) {
+        const double v = __ldg(x + lc * B + i);
+        if (i < 3 * N3) U[(i / N3) * L::NB + sk::pad_pt<N, L::PS>(i % N3)] = v;
+        else PR[i - 3 * N3] = v;
+    }
     __syncthreads();
 
     // ---------------- P1: gradients (9 D sweeps), pressure A_p along j2, face traces ----------------
@@ -161,20 +192,20 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
             const int ce = slot < 3 ? slot + 3 * h : (h ? -1 : slot + 3);
             if (ce < 0) continue;
             const int c = ce / 3, e = ce % 3;
-            const double* in = U + c * N3;
-            double* out = G + ce * N3;
-            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.eD, l);
-            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.eD, l);
-            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.eD, l);
+            const double* in = U + c * L::NB;
+            double* out = G + ce * L::NB;
+            if (e == 0) sk::SwC<N, L::PS, 0, false>::line(in, out, T.eD, l);
+            else if (e == 1) sk::SwC<N, L::PS, 1, false>::line(in, out, T.eD, l);
+            else sk::SwC<N, L::PS, 2, false>::line(in, out, T.eD, l);
         }
     } else {
         for (int t = tid; t < 9 * N2; t += NT) {
             const int ce = t / N2, l = t % N2, c = ce / 3, e = ce % 3;
-            const double* in = U + c * N3;
-            double* out = G + ce * N3;
-            if (e == 0) qd::Sw3<N, N, N, 0, N, false, false>::line(in, out, T.eD, l);
-            else if (e == 1) qd::Sw3<N, N, N, 1, N, false, false>::line(in, out, T.eD, l);
-            else qd::Sw3<N, N, N, 2, N, false, false>::line(in, out, T.eD, l);
+            const double* in = U + c * L::NB;
+            double* out = G + ce * L::NB;
+            if (e == 0) sk::SwC<N, L::PS, 0, false>::line(in, out, T.eD, l);
+            else if (e == 1) sk::SwC<N, L::PS, 1, false>::line(in, out, T.eD, l);
+            else sk::SwC<N, L::PS, 2, false>::line(in, out, T.eD, l);
         }
     }
     for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, NP, 2, N, false, false>::line(PR, TA, T.eAP, t);
@@ -193,7 +224,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         double uo = 0, go = 0, un = 0, gn = 0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            const double vo = U[c * N3 + pidx<N>(d, j, a, bq)];
+            const double vo = U[c * L::NB + sk::pad_pt<N, L::PS>(pidx<N>(d, j, a, bq))];
             uo = fma(es[j], vo, uo);
             go = fma(ds[j], vo, go);
             const double vn = PREF ? vnb[k][j] : (nb ? __ldg(nb + c * N3 + pidx<N>(d, j, a, bq)) : 0.0);
@@ -255,7 +286,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
         for (int c = 0; c < 3; ++c) {
 #pragma unroll
             for (int e = 0; e < 3; ++e) {
-                double* g = G + (3 * c + e) * N3 + P;
+                double* g = G + (3 * c + e) * L::NB + sk::pad_pt<N, L::PS>(P);
                 const double ihe = e == 0 ? ih0 : (e == 1 ? ih1 : ih2);
                 const double ge = *g * ihe;            // physical d u_c / d x_e
                 if (c == e) div += ge;
@@ -324,7 +355,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     // ---------------- P5: stage 3 (D^T per direction into RU, A_p^T for the pressure), face A_p^T ----------------
     for (int t = tid; t < 3 * N2; t += NT) {
         const int c = t / N2, l = t % N2;
-        qd::Sw3<N, N, N, 0, N, true, false>::line(G + (3 * c) * N3, U + c * N3, T.eDt, l);
+        sk::SwC<N, L::PS, 0, false>::line(G + (3 * c) * L::NB, U + c * L::NB, T.eDt, l);
     }
     for (int t = tid; t < N2; t += NT) qd::Sw3<N, N, N, 0, NP, true, false>::line(PQ, TB, T.eAPt, t);
     for (int t = tid; t < 6 * N; t += NT) {
@@ -335,7 +366,7 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     __syncthreads();
     for (int t = tid; t < 3 * N2; t += NT) {
         const int c = t / N2, l = t % N2;
-        qd::Sw3<N, N, N, 1, N, true, true>::line(G + (3 * c + 1) * N3, U + c * N3, T.eDt, l);
+        sk::SwC<N, L::PS, 1, true>::line(G + (3 * c + 1) * L::NB, U + c * L::NB, T.eDt, l);
     }
     for (int t = tid; t < NP * N; t += NT) qd::Sw3<NP, N, N, 1, NP, true, false>::line(TB, TA, T.eAPt, t);
     for (int t = tid; t < 6 * NP; t += NT) {
@@ -346,13 +377,13 @@ k_stokes(const double* __restrict__ x, const double* __restrict__ xb, const doub
     __syncthreads();
     for (int t = tid; t < 3 * N2; t += NT) {
         const int c = t / N2, l = t % N2;
-        qd::Sw3<N, N, N, 2, N, true, true>::line(G + (3 * c + 2) * N3, U + c * N3, T.eDt, l);
+        sk::SwC<N, L::PS, 2, true>::line(G + (3 * c + 2) * L::NB, U + c * L::NB, T.eDt, l);
     }
     for (int t = tid; t < NP2; t += NT) qd::Sw3<NP, NP, N, 2, NP, true, false>::line(TA, PR, T.eAPt, t);
     __syncthreads();
     // ---------------- P6: add the face back-projections along the normals, write the block once ----------------
     for (int i = tid; i < B; i += NT) {
-        double v = U[i];
+        double v = i < 3 * N3 ? U[(i / N3) * L::NB + sk::pad_pt<N, L::PS>(i % N3)] : PR[i - 3 * N3];
         if (i < 3 * N3) {
             const int c = i / N3, P = i % N3;
             const int j[3] = {P % N, (P / N) % N, P / N2};
