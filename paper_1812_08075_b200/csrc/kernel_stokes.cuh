@@ -54,7 +54,7 @@ struct SLay {
     // per-cell shared buffers (doubles)
     static constexpr int U = 0;            // velocity (3 blocks of NB), later the velocity residual RU
     static constexpr int PR = U + 3 * NB;  // pressure (NP3), later the pressure residual RP
-    static constexpr int G = PR + NP3;     // 9 reference gradients [c][e] (NB each), later the fluxes Q[c][e]
+    static constexpr int G = PR + (NP3 + 1) / 2 * 2; // 9 reference gradients [c][e] (NB each, 16-B aligned), later the fluxes Q[c][e]
     static constexpr int PQ = G + 9 * NB;  // p at the points (dense N3), later -W div u
     static constexpr int TA = PQ + N3;     // [NP][NP][N]
     static constexpr int TB = TA + NP2 * N; // [NP][N][N]
@@ -79,11 +79,33 @@ struct SwC {
         else if (DIM == 1) { const int i0 = l % N, i2 = l / N; ib = i0 + PS * i2; ist = N; }
         else { const int i0 = l % N, i1 = l / N; ib = i0 + N * i1; ist = PS; }
         double v[N], y[N];
+        if constexpr (DIM == 0 && PS != N * N) { // (padded n = 4 blocks: a j0 line is 16-B aligned: 2 x 16-B accesses)
 #pragma unroll
-        for (int j = 0; j < N; ++j) v[j] = in[ib + ist * j];
+            for (int j = 0; j < N; j += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(in + ib + j);
+                v[j] = t.x;
+                v[j + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) v[j] = in[ib + ist * j];
+        }
         eo_apply(T, v, y);
+        if constexpr (DIM == 0 && PS != N * N) {
 #pragma unroll
-        for (int q = 0; q < N; ++q) out[ib + ist * q] = ACC ? out[ib + ist * q] + y[q] : y[q];
+            for (int q = 0; q < N; q += 2) {
+                double2* o = reinterpret_cast<double2*>(out + ib + q);
+                if (ACC) {
+                    const double2 t = *o;
+                    *o = make_double2(t.x + y[q], t.y + y[q + 1]);
+                } else {
+                    *o = make_double2(y[q], y[q + 1]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < N; ++q) out[ib + ist * q] = ACC ? out[ib + ist * q] + y[q] : y[q];
+        }
     }
 };
 // padded index of the dense point P = j0 + N j1 + N^2 j2
