@@ -575,6 +575,33 @@ def main():
                "how": "pinned H2D of u0 and z, dg_apply_jacobian, D2H of r" if args.jacobian else
                ("dg_apply_host (pinned host x -> H2D -> kernels -> D2H r, plane-chunk pipelined)"
                 if world == 1 else "per rank: pinned H2D of the slab, halo exchange + kernels, D2H of r")}
+        if world == 1 and not args.jacobian:
+            # the e2e leg's own ceiling on this box: the same bytes as plain pinned copies, H2D and D2H concurrently
+            # on two streams in dg_apply_host's 32 chunks, no kernels (tools/mb_pcie.py standalone)
+            cd_in, cd_out = torch.empty_like(x), torch.empty_like(x)
+            s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+            nb = [x.numel() * i // 32 for i in range(33)]
+
+            def copies():
+                s_in.wait_stream(torch.cuda.current_stream())
+                s_out.wait_stream(torch.cuda.current_stream())
+                for i in range(32):
+                    with torch.cuda.stream(s_in):
+                        cd_in[nb[i]:nb[i + 1]].copy_(xh[nb[i]:nb[i + 1]], non_blocking=True)
+                    with torch.cuda.stream(s_out):
+                        rh[nb[i]:nb[i + 1]].copy_(cd_out[nb[i]:nb[i + 1]], non_blocking=True)
+                torch.cuda.current_stream().wait_stream(s_in)
+                torch.cuda.current_stream().wait_stream(s_out)
+                torch.cuda.synchronize()
+            copies()
+            t0 = time.perf_counter()
+            for _ in range(KE):
+                copies()
+            tc = (time.perf_counter() - t0) / KE
+            e2e["copy_ceiling"] = {"ms": tc * 1e3, "value": w.ndofs / tc,
+                                   "frac": (tc * KE) / te,
+                                   "how": "pinned H2D of x and D2H of r concurrently (2 streams, 32 chunks), no kernels"}
+            del cd_in, cd_out
         del xh, rh, uh
 
     # ---- CPU baseline (rank 0, N = 1 only): the oracle as it stands on all host cores; for the small configs
