@@ -12,6 +12,7 @@ nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_rea
 SMI=$!
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
 kill $SMI
+python tools/mb_pcie.py > $O/pcie.json 2>&1
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.json 2> $O/bench_ref.err
 for C in 0 1 2 4; do timeout 900 python bench.py --config $C --steps 20 --warmup 5 --cpu-seconds 8 > $O/bench_cfg$C.json 2> $O/bench_cfg$C.err; done
 timeout 900 python bench.py --config 2 --quad 7 --steps 5 --warmup 3 --no-e2e --cpu-seconds 6 > $O/bench_cfg2_quad7.json 2> $O/bench_cfg2_quad7.err
