@@ -35,3 +35,11 @@ def test_reference_arm_nonzero_rank_is_silent():
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert p.returncode == 0
     assert p.stdout.strip() == ""
+
+
+def test_gpu_arm_rejects_gpus_world_mismatch():
+    """--gpus N without N ranks must not produce a mislabelled single-GPU line (the check runs before any CUDA use)."""
+    p = _run(["--gpus", "2", "--steps", "1", "--warmup", "3"], env={"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert p.returncode != 0
+    assert p.stdout.strip() == ""
+    assert "WORLD_SIZE" in p.stderr
