@@ -575,9 +575,10 @@ def main():
                "how": "pinned H2D of u0 and z, dg_apply_jacobian, D2H of r" if args.jacobian else
                ("dg_apply_host (pinned host x -> H2D -> kernels -> D2H r, plane-chunk pipelined)"
                 if world == 1 else "per rank: pinned H2D of the slab, halo exchange + kernels, D2H of r")}
-        if world == 1 and not args.jacobian:
+        if world == 1 and not args.jacobian and 8 * w.ndofs >= (256 << 20):
             # the e2e leg's own ceiling on this box: the same bytes as plain pinned copies, H2D and D2H concurrently
-            # on two streams in dg_apply_host's 32 chunks, no kernels (tools/mb_pcie.py standalone)
+            # on two streams in dg_apply_host's 32 chunks, no kernels (tools/mb_pcie.py standalone); only for vectors
+            # >= 256 MB: below that the 64 Python-issued copies are launch-bound and say nothing about the link
             cd_in, cd_out = torch.empty_like(x), torch.empty_like(x)
             s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
             nb = [x.numel() * i // 32 for i in range(33)]
