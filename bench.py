@@ -629,6 +629,32 @@ def main():
                             + (": one rank, the wrap halos sent / received to itself (--dist-loopback)" if world == 1 else ""),
                 "overlap": "interior planes on the compute stream while the exchange runs on a high-priority stream; "
                            "NVTX ranges slab:pack / slab:interior / slab:halo / slab:boundary"}
+        if isinstance(sop, _DistSlab) and ap.traces and op.nplanes >= 3:
+            # SURVEY §8(d) interior / halo / boundary breakdown (no nsys on this pool): the step's pieces through the
+            # same context, each launched alone and timed with events on the launching stream; what the overlapped
+            # step costs beyond their sum is the exchange time the interior planes did not hide
+            tlo, thi = (torch.empty(op.halo_ndofs, dtype=torch.float64, device=dev) for _ in range(2))
+            op.pack_halo(x, tlo, thi)
+            L = op.nplanes
+
+            def _phase(fn, reps=20):
+                fn()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                a.record(stream)
+                for _ in range(reps):
+                    fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                return a.elapsed_time(b) / reps
+            t_pack = _phase(lambda: op.pack_halo(x, tlo, thi))
+            t_int = _phase(lambda: op.apply_planes_tr(x, thi, tlo, r, 1, L - 1))
+            t_bnd = _phase(lambda: (op.apply_planes_tr(x, thi, tlo, r, 0, 1), op.apply_planes_tr(x, thi, tlo, r, L - 1, L)))
+            med = statistics.median(step_ms)
+            halo["phases_ms"] = {"pack": t_pack, "interior": t_int, "boundary": t_bnd, "sum": t_pack + t_int + t_bnd,
+                                 "step_median": med, "exposed_exchange": med - (t_pack + t_int + t_bnd),
+                                 "how": "each piece alone on the compute stream (events, 20 launches); exposed_exchange = "
+                                        "step median - sum (the exchange and stream hand-offs the interior did not hide)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
